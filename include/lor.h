@@ -1,0 +1,162 @@
+/*
+ * lor.h -- C ABI of the B200-native batched low-order-refined (LOR) assembly library
+ * (liblor_b200.so).  arXiv 2210.12253, Step S1.2 "Low-order-refined matrix assembly"
+ * and its auxiliary discrete operators (l.390-445, Algorithm 1).
+ *
+ * Problem statement: a user holds a degree-p bilinear form on a
+ * conforming quad/hex mesh and asks for "the LOR discretization ... assembled ... in parallel
+ * CSR format", plus the discrete gradient (AMS) and discrete curl (ADS).
+ *
+ * Conventions (all entry points):
+ *   * Ownership.  Host inputs are copied during lor_setup; the caller may free them on return.
+ *     Outputs go into CALLER-ALLOCATED DEVICE buffers whose sizes come from lor_query*.  The
+ *     library never frees caller memory.  Internal workspaces live in the context and are
+ *     released by lor_destroy.
+ *   * Errors.  Every call returns a lor_status; nothing throws or aborts across the ABI.
+ *     lor_last_error(ctx) gives a message (including element / sub-cell for geometry errors).
+ *   * Asynchrony.  Assembly calls are enqueued on the context's CUDA stream and return without
+ *     synchronising.  Device-side errors (det J <= 0) are reported by lor_sync.  lor_query* are
+ *     synchronous host calls whose values are fixed at setup (the pattern is topological).
+ *   * Threads.  A context is not thread-safe; one context per rank (process) per GPU.
+ *   * Index widths.  col is int32 of GLOBAL ids (n_global < 2^31); row_ptr is int64 and
+ *     LOCAL (row_ptr[0] = 0); each rank owns the contiguous global rows
+ *     [row_begin, row_begin + n_rows_local) (ParCSR convention).
+ *   * Pattern.  Structural: every pair of dofs sharing a LOR cell, explicit zeros kept; both
+ *     triangles; columns ascending within each row (readings P-3/P-4/P-5).
+ *   * Numbering / orientation / signs: DESIGN.md "Numbering": vertices, then
+ *     edges, faces, element interiors; rank-major renumbering by owner = rank of the minimal
+ *     element containing the dof.
+ */
+#ifndef LOR_B200_H
+#define LOR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lor_ctx_s *lor_ctx; /* opaque, one per GPU / rank */
+
+typedef enum { LOR_H1 = 0, LOR_ND = 1, LOR_RT = 2 } lor_space;
+/* sub-cell quadrature (reading P-1): vertex = tensor 2-point Gauss-Lobatto
+ * (geometric factors at the sub-element vertices); gauss2 = tensor 2-point Gauss */
+typedef enum { LOR_QUAD_VERTEX = 0, LOR_QUAD_GAUSS2 = 1 } lor_quad;
+
+typedef enum {
+  LOR_OK = 0,
+  LOR_ERR_INVALID_ARGUMENT = 1,
+  LOR_ERR_DEGENERATE_GEOMETRY = 2,
+  LOR_ERR_OUT_OF_MEMORY = 3,
+  LOR_ERR_CUDA = 4,
+  LOR_ERR_NCCL = 5,
+  LOR_ERR_UNSUPPORTED = 6,
+  LOR_ERR_BUFFER_TOO_SMALL = 7
+} lor_status;
+
+typedef struct {
+  int dim;                      /* 2 or 3                                                     */
+  int p;                        /* polynomial degree, 1 <= p <= 8                             */
+  int64_t n_vert;               /* coarse vertices                                            */
+  const double *vert_xyz;       /* HOST [n_vert][dim] (used only when elem_nodes == NULL)      */
+  int64_t n_elem;               /* coarse (macro) elements, GLOBAL count                       */
+  const int64_t *elem_vert;     /* HOST [n_elem][2^dim], local corner order a + 2b + 4c;
+                                   every rank passes the whole mesh (the coarse mesh is small) */
+  const double *elem_nodes;     /* HOST [n_elem][dim][(p+1)^dim]: the high-order coordinate
+                                   E-vector at the tensor Gauss-Lobatto points (PAPER.md
+                                   l.342-345).  Only this rank's elements are read.  NULL =>
+                                   (bi/tri)linear interpolation of vert_xyz at GLL points.     */
+  int rank, nranks;             /* this process and the job size                              */
+  const int64_t *elem_rank_begin; /* HOST [nranks+1] contiguous element ranges per rank;
+                                   NULL allowed when nranks == 1                              */
+  const void *nccl_unique_id;   /* HOST 128-byte ncclUniqueId from lor_nccl_get_unique_id on
+                                   rank 0, broadcast by the caller; NULL when nranks == 1      */
+  void *cuda_stream;            /* cudaStream_t for all work (NULL = legacy default stream)    */
+  int device;                   /* CUDA device ordinal of this rank                            */
+} lor_setup_args;
+
+/* Caller-owned DEVICE buffers.  cap_nnz = capacity of col/val (entries); row_ptr must hold
+ * n_rows_local + 1 entries. */
+typedef struct {
+  int64_t *row_ptr;
+  int32_t *col;
+  double *val;
+  int64_t cap_nnz;
+} lor_csr;
+
+/* Setup (untimed in the paper's sense, "reuse of the element restriction"):
+ * coarse topology, canonical numbering + signs, ownership, rank-major ids, per-element
+ * topology records, interface exchange plan and NCCL communicator, device uploads.
+ * Errors: INVALID_ARGUMENT (dim, p, null pointers, inconsistent ranks, n_global >= 2^31,
+ * negative corner orientation), OUT_OF_MEMORY, CUDA, NCCL. */
+lor_status lor_setup(const lor_setup_args *args, lor_ctx *out);
+lor_status lor_destroy(lor_ctx ctx);
+
+/* Waits on the context stream; returns DEGENERATE_GEOMETRY if any sub-cell had det J <= 0
+ * in an earlier call (message names element and sub-cell), CUDA on launch failures. */
+lor_status lor_sync(lor_ctx ctx);
+const char *lor_last_error(lor_ctx ctx);
+
+/* Sizes of the assembled operator of `space` on this rank (synchronous, fixed at setup). */
+lor_status lor_query(lor_ctx ctx, lor_space space, int64_t *n_rows_local, int64_t *row_begin,
+                     int64_t *n_rows_global, int64_t *nnz_local);
+/* which = 0: discrete gradient (rows: owned ND dofs, cols: global H1 dofs);
+ * which = 1: discrete curl (rows: owned RT dofs, cols: global ND dofs; dim == 3). */
+lor_status lor_query_discrete(lor_ctx ctx, int which, int64_t *n_rows_local, int64_t *nnz_local,
+                              int64_t *n_cols_global);
+
+/* LOR matrix assembly, Steps A1-A3: per macro element the p^d sub-cell
+ * matrices at GLL-point geometry (A1), the processor-local CSR with row counts, scan and
+ * column/value fill (A2), and on nranks > 1 the interface exchange over NCCL that replaces the
+ * P^T A P triple product (A3).  Forms: H1 alpha grad.grad + beta mass; ND alpha curl.curl +
+ * beta mass; RT alpha div.div + beta mass (constant coefficients, reading P-2).
+ * ND/RT with dim == 2 -> UNSUPPORTED.  Output: row_ptr[n_rows_local+1], col/val[nnz_local]. */
+lor_status lor_assemble_h1(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
+lor_status lor_assemble_nd(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
+lor_status lor_assemble_rt(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
+
+/* Discrete gradient, Algorithm 1: row i (owned ND dof) has -sigma_i at the
+ * H1 id of the edge's local tail and +sigma_i at its head, columns sorted; row_ptr[i] = 2i.
+ * Discrete curl: row f (owned RT dof) has +-1 on its 4 LOR edges
+ * (right-hand-rule circulation about the face's global normal, in each edge's global
+ * orientation), columns sorted; row_ptr[f] = 4f.  No communication. */
+lor_status lor_discrete_grad(lor_ctx ctx, lor_csr *out);
+lor_status lor_discrete_curl(lor_ctx ctx, lor_csr *out);
+
+/* Element restriction of `space` for this rank's elements:
+ * elem_dofs[n_elem_local][ndof_per_el] global ids in the macro-element local order of
+ * DESIGN.md, signs[...] in {-1,+1} (NULL allowed; must be NULL-or-valid for H1).
+ * DEVICE buffers.  n_elem_local = elem_rank_begin[rank+1] - elem_rank_begin[rank]. */
+lor_status lor_dof_map(lor_ctx ctx, lor_space space, int32_t *elem_dofs, int8_t *signs);
+lor_status lor_query_elements(lor_ctx ctx, int64_t *elem_begin, int64_t *n_elem_local, int *ndof_per_el_h1,
+                              int *ndof_per_el_nd, int *ndof_per_el_rt);
+
+/* Replace this rank's coordinate E-vector (mesh motion / per-step inputs):
+ * elem_nodes = [n_elem_local][dim][(p+1)^dim] for elements elem_rank_begin[rank] .. +n_elem_local,
+ * HOST (pinned for asynchrony) or DEVICE memory; enqueued on the context stream. */
+lor_status lor_update_coordinates(lor_ctx ctx, const double *elem_nodes);
+
+/* Exchange mode for nranks > 1 (A3 replacement).  LOR_EXCHANGE_NCCL (0, default when
+ * nccl_unique_id was given): ncclSend/ncclRecv of interface partial rows inside the assembly call.
+ * LOR_EXCHANGE_MANUAL (1, default without a unique id): single-process emulation of several ranks
+ * (e.g. tests on one GPU) -- the assembly call stops before the exchange; the caller moves each
+ * peer's partial rows with lor_exchange_copy(dst, src, space) and completes dst's rows with
+ * lor_assemble_finish.  Both modes run the same kernels on the same buffers. */
+lor_status lor_set_exchange(lor_ctx ctx, int mode);
+lor_status lor_exchange_copy(lor_ctx dst, lor_ctx src, lor_space space);
+lor_status lor_assemble_finish(lor_ctx ctx, lor_space space, lor_csr *out);
+
+/* Rank 0 creates the NCCL unique id (128 bytes) that the caller broadcasts to all ranks. */
+lor_status lor_nccl_get_unique_id(void *out128);
+
+/* Number of this library's kernels launched on the context since setup (instrumentation). */
+int64_t lor_kernel_launches(lor_ctx ctx);
+
+/* Per-phase device timing of the last assembly call in milliseconds (count, scan, element,
+ * exchange+finalize); valid after lor_sync.  Returns number of phases written (<= 8). */
+int lor_last_phase_ms(lor_ctx ctx, float *ms, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOR_B200_H */

@@ -1,0 +1,110 @@
+"""In-tree build of liblor_b200.so (sm_100a) -- the native library behind the C ABI include/lor.h.
+
+The fused element kernel is instantiated per (dim, space, p); each instantiation is its own
+generated translation unit so nvcc runs them in parallel.  Output:
+paper_2210_12253_b200/liblor_b200.so (git-ignored, travels to the GPU box with the tree).
+
+    python -m paper_2210_12253_b200.build          # incremental
+    LOR_BUILD_P=2,4 python -m ...                   # dev: only some degrees (others -> UNSUPPORTED)
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import hashlib
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(ROOT, "build", "lor")
+LIB = os.path.join(HERE, "liblor_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-I", CSRC,
+         "-Wno-deprecated-gpu-targets"]
+
+COMBOS = [(2, 0), (3, 0), (3, 1), (3, 2)]  # (dim, space): H1 2D, H1 3D, ND, RT
+SPACE_NAME = {0: "SP_H1", 1: "SP_ND", 2: "SP_RT"}
+
+
+def _sources_hash() -> str:
+    h = hashlib.sha256()
+    for name in sorted(os.listdir(CSRC)):
+        if name.endswith((".cu", ".cuh", ".h", ".cpp")):
+            with open(os.path.join(CSRC, name), "rb") as f:
+                h.update(name.encode() + f.read())
+    with open(os.path.join(ROOT, "include", "lor.h"), "rb") as f:
+        h.update(f.read())
+    h.update(" ".join(FLAGS + ARCH).encode())
+    h.update(os.environ.get("LOR_BUILD_P", "").encode())
+    return h.hexdigest()[:16]
+
+
+def _gen_units(plist):
+    os.makedirs(BUILD, exist_ok=True)
+    units = []
+    for dim, sp in COMBOS:
+        for p in range(1, 9):
+            name = f"asm_{dim}_{sp}_{p}"
+            path = os.path.join(BUILD, name + ".cu")
+            if p in plist:
+                body = (f'#include "lor_asm.cuh"\nnamespace lorb {{\n'
+                        f"cudaError_t launch_asm_{dim}_{sp}_{p}(const AsmArgs &a, int quad, cudaStream_t st, int *smem_out) {{\n"
+                        f"  return launch_asm_kz<{dim}, {SPACE_NAME[sp]}, {p}>(a, quad, st, smem_out);\n}}\n}}\n")
+            else:
+                body = (f'#include "lor_kernels.h"\nnamespace lorb {{\n'
+                        f"cudaError_t launch_asm_{dim}_{sp}_{p}(const AsmArgs &, int, cudaStream_t, int *smem_out) {{\n"
+                        f"  if (smem_out) *smem_out = 0;\n  return cudaErrorInvalidValue;\n}}\n}}\n")
+            old = open(path).read() if os.path.exists(path) else None
+            if old != body:
+                with open(path, "w") as f:
+                    f.write(body)
+            units.append(path)
+    return units
+
+
+def _compile(src, obj, extra=()):
+    cmd = [NVCC] + FLAGS + ARCH + list(extra) + ["-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    return obj
+
+
+def build(force: bool = False, verbose: bool = True) -> str:
+    plist = [int(v) for v in os.environ.get("LOR_BUILD_P", "1,2,3,4,5,6,7,8").split(",") if v.strip()]
+    stamp = os.path.join(BUILD, "stamp")
+    key = _sources_hash()
+    if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == key:
+        return LIB
+    units = _gen_units(plist)
+    jobs = [(os.path.join(CSRC, "lor_kernels.cu"), os.path.join(BUILD, "lor_kernels.o")),
+            (os.path.join(CSRC, "lor_capi.cu"), os.path.join(BUILD, "lor_capi.o")),
+            (os.path.join(CSRC, "lor_plan.cpp"), os.path.join(BUILD, "lor_plan.o"))]
+    jobs += [(u, u[:-3] + ".o") for u in units]
+    # largest first (ND / high p) for better packing
+    jobs.sort(key=lambda j: (("_3_1_" in j[0]) * 10 + ("_3_0_" in j[0]) * 5 + int(j[0][-4]) if "asm_" in j[0] else 100),
+              reverse=True)
+    nw = max(1, min(len(jobs), os.cpu_count() or 4))
+    if verbose:
+        print(f"[lor build] {len(jobs)} translation units on {nw} workers (p in {plist})", flush=True)
+    with cf.ThreadPoolExecutor(nw) as ex:
+        futs = [ex.submit(_compile, s, o) for s, o in jobs]
+        objs = [f.result() for f in futs]
+    tmp = LIB + f".tmp{os.getpid()}"
+    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, LIB)
+    with open(stamp, "w") as f:
+        f.write(key)
+    if verbose:
+        print(f"[lor build] wrote {LIB}", flush=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

@@ -1,0 +1,584 @@
+// lor_capi.cu -- C ABI (include/lor.h) of the B200 LOR library: context, device memory, launch
+// orchestration on the caller's stream, NCCL point-to-point exchange of interface partial rows.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lor.h"
+#include "lor_internal.h"
+#include "lor_kernels.h"
+#include "lor_plan.h"
+
+// ---- minimal NCCL ABI (loaded with dlopen only when nranks > 1) ----------------------------------
+typedef struct ncclComm *ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef enum { ncclSuccess = 0 } ncclResult_t;
+typedef enum { ncclInt8 = 0, ncclChar = 0, ncclUint8 = 1 } ncclDataType_t;
+
+namespace {
+
+struct NcclApi {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string &err) {
+    if (h) return true;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { err = "cannot dlopen libnccl.so.2"; return false; }
+#define LOAD(sym, name)                                          \
+  sym = reinterpret_cast<decltype(sym)>(dlsym(h, name));         \
+  if (!sym) { err = std::string("missing NCCL symbol ") + name; return false; }
+    LOAD(GetUniqueId, "ncclGetUniqueId");
+    LOAD(CommInitRank, "ncclCommInitRank");
+    LOAD(CommDestroy, "ncclCommDestroy");
+    LOAD(Send, "ncclSend");
+    LOAD(Recv, "ncclRecv");
+    LOAD(GroupStart, "ncclGroupStart");
+    LOAD(GroupEnd, "ncclGroupEnd");
+    LOAD(GetErrorString, "ncclGetErrorString");
+#undef LOAD
+    return true;
+  }
+};
+NcclApi g_nccl;
+
+using namespace lorb;
+
+struct SpaceDev {
+  bool valid = false;
+  int ndpe = 0, maxl = 0, rstride = 0;
+  int64_t n_global = 0, row_begin = 0, n_local = 0, nnz_local = 0;
+  int32_t *base[4] = {nullptr, nullptr, nullptr, nullptr};
+  ElemSpace *esp = nullptr;
+  Ose *ose = nullptr;
+  int32_t *ose_slots = nullptr, *counters = nullptr, *defer = nullptr;
+  int n_ose = 0, n_defer = 0;
+  RecEntry *scratch = nullptr;
+  int64_t n_records = 0;
+  int32_t *cnt = nullptr;
+  unsigned long long *scan_status = nullptr;
+  unsigned int *tile_ctr = nullptr;
+  std::vector<int64_t> recv_begin, recv_count, send_begin, send_count;
+  int pending_exchange = 0;  // manual exchange mode: assembly waiting for lor_assemble_finish
+};
+
+}  // namespace
+
+struct lor_ctx_s {
+  int dim = 0, p = 0, rank = 0, nranks = 1, device = 0;
+  int64_t nel = 0, elem_begin = 0, nel_local = 0, ntopo = 0;
+  cudaStream_t stream = nullptr;
+  ElemTopo *topo = nullptr;
+  double *X = nullptr;
+  int64_t xstride = 0;
+  SpaceDev sp[3];
+  int *err = nullptr;
+  ncclComm_t comm = nullptr;
+  int exchange_mode = 0;  // 0 NCCL, 1 manual
+  std::string last_error;
+  int64_t launches = 0;
+  cudaEvent_t ev[8] = {};
+  int nphase = 0;
+  int fin_smem = 0;
+  std::vector<void *> allocs;
+};
+
+namespace {
+
+lor_status fail(lor_ctx c, lor_status st, const std::string &msg) {
+  if (c) c->last_error = msg;
+  return st;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                  \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return fail(ctx, _e == cudaErrorMemoryAllocation ? LOR_ERR_OUT_OF_MEMORY : LOR_ERR_CUDA, \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                       \
+  } while (0)
+
+template <class T>
+cudaError_t dev_upload(lor_ctx c, T **dst, const T *src, size_t n) {
+  *dst = nullptr;
+  if (n == 0) return cudaSuccess;
+  cudaError_t e = cudaMalloc((void **)dst, sizeof(T) * n);
+  if (e != cudaSuccess) return e;
+  c->allocs.push_back(*dst);
+  return cudaMemcpy(*dst, src, sizeof(T) * n, cudaMemcpyHostToDevice);
+}
+template <class T>
+cudaError_t dev_alloc(lor_ctx c, T **dst, size_t n) {
+  *dst = nullptr;
+  if (n == 0) return cudaSuccess;
+  cudaError_t e = cudaMalloc((void **)dst, sizeof(T) * n);
+  if (e != cudaSuccess) return e;
+  c->allocs.push_back(*dst);
+  return cudaMemset(*dst, 0, sizeof(T) * n);
+}
+
+void fill_base(const SpaceDev &S, const int32_t *out[4]) {
+  for (int t = 0; t < 4; ++t) out[t] = S.base[t];
+}
+
+lor_status run_count_scan(lor_ctx c, int s, int64_t *row_ptr) {
+  SpaceDev &S = c->sp[s];
+  if (S.n_local > 0) CUDA_TRY(c, cudaMemsetAsync(S.cnt, 0, sizeof(int32_t) * S.n_local, c->stream));
+  CountArgs ca;
+  ca.p = c->p;
+  ca.ndpe = S.ndpe;
+  ca.ntopo = c->ntopo;
+  ca.topo = c->topo;
+  fill_base(S, ca.base);
+  ca.row_begin = S.row_begin;
+  ca.cnt = S.cnt;
+  CUDA_TRY(c, launch_count(c->dim, s, ca, c->stream));
+  c->launches++;
+  CUDA_TRY(c, launch_scan(S.cnt, row_ptr, S.n_local, S.scan_status, S.tile_ctr, c->stream));
+  c->launches++;
+  return LOR_OK;
+}
+
+lor_status exchange_nccl(lor_ctx c, int s) {
+  SpaceDev &S = c->sp[s];
+  const size_t rb = (size_t)S.rstride * sizeof(RecEntry);
+  if (g_nccl.GroupStart() != ncclSuccess) return fail(c, LOR_ERR_NCCL, "ncclGroupStart");
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) continue;
+    if (S.send_count[q] > 0) {
+      ncclResult_t r = g_nccl.Send(reinterpret_cast<char *>(S.scratch) + S.send_begin[q] * rb, S.send_count[q] * rb,
+                                   ncclUint8, q, c->comm, c->stream);
+      if (r != ncclSuccess) { g_nccl.GroupEnd(); return fail(c, LOR_ERR_NCCL, g_nccl.GetErrorString(r)); }
+    }
+    if (S.recv_count[q] > 0) {
+      ncclResult_t r = g_nccl.Recv(reinterpret_cast<char *>(S.scratch) + S.recv_begin[q] * rb, S.recv_count[q] * rb,
+                                   ncclUint8, q, c->comm, c->stream);
+      if (r != ncclSuccess) { g_nccl.GroupEnd(); return fail(c, LOR_ERR_NCCL, g_nccl.GetErrorString(r)); }
+    }
+  }
+  if (g_nccl.GroupEnd() != ncclSuccess) return fail(c, LOR_ERR_NCCL, "ncclGroupEnd");
+  return LOR_OK;
+}
+
+lor_status finish(lor_ctx c, int s, lor_csr *out) {
+  SpaceDev &S = c->sp[s];
+  FinArgs f;
+  f.n = S.n_defer;
+  f.list = S.defer;
+  f.ose = S.ose;
+  f.ose_slots = S.ose_slots;
+  f.scratch = S.scratch;
+  f.rstride = S.rstride;
+  f.row_begin = S.row_begin;
+  f.row_ptr = out->row_ptr;
+  f.col = out->col;
+  f.val = out->val;
+  f.smem_bytes = c->fin_smem;
+  CUDA_TRY(c, launch_finalize_list(f, c->stream));
+  if (f.n > 0) c->launches++;
+  return LOR_OK;
+}
+
+lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, lor_csr *out) {
+  if (!c) return LOR_ERR_INVALID_ARGUMENT;
+  if (s < 0 || s > 2 || !c->sp[s].valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available for this mesh");
+  if (quad != LOR_QUAD_VERTEX && quad != LOR_QUAD_GAUSS2) return fail(c, LOR_ERR_INVALID_ARGUMENT, "bad quadrature");
+  SpaceDev &S = c->sp[s];
+  if (!out || !out->row_ptr || (S.nnz_local > 0 && (!out->col || !out->val)))
+    return fail(c, LOR_ERR_INVALID_ARGUMENT, "null output buffer");
+  if (out->cap_nnz < S.nnz_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < nnz_local");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  c->nphase = 0;
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  lor_status st = run_count_scan(c, s, out->row_ptr);
+  if (st) return st;
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  AsmArgs a;
+  a.nel_local = c->nel_local;
+  a.elem_begin = c->elem_begin;
+  a.topo = c->topo;
+  a.esp = S.esp;
+  a.X = c->X;
+  a.xstride = c->xstride;
+  fill_base(S, a.base);
+  a.row_begin = S.row_begin;
+  a.row_ptr = out->row_ptr;
+  a.col = out->col;
+  a.val = out->val;
+  a.scratch = S.scratch;
+  a.rstride = S.rstride;
+  a.ose = S.ose;
+  a.ose_slots = S.ose_slots;
+  a.counters = S.counters;
+  a.alpha = alpha;
+  a.beta = beta;
+  a.err = c->err;
+  CUDA_TRY(c, launch_assemble(c->dim, s, c->p, (int)quad, a, c->stream, nullptr));
+  if (c->nel_local > 0) c->launches++;
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  if (c->nranks > 1) {
+    if (c->exchange_mode == 1) {
+      S.pending_exchange = 1;
+      return LOR_OK;
+    }
+    st = exchange_nccl(c, s);
+    if (st) return st;
+  }
+  st = finish(c, s, out);
+  if (st) return st;
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  return LOR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lor_status lor_nccl_get_unique_id(void *out128) {
+  if (!out128) return LOR_ERR_INVALID_ARGUMENT;
+  std::string err;
+  if (!g_nccl.load(err)) return LOR_ERR_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return LOR_ERR_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return LOR_OK;
+}
+
+lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
+  if (!out) return LOR_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (!args) return LOR_ERR_INVALID_ARGUMENT;
+  const lor_setup_args &A = *args;
+  if (!(A.dim == 2 || A.dim == 3) || A.p < 1 || A.p > 8 || A.n_vert <= 0 || A.n_elem <= 0 || !A.elem_vert ||
+      A.nranks < 1 || A.rank < 0 || A.rank >= A.nranks || (!A.elem_nodes && !A.vert_xyz) ||
+      (A.nranks > 1 && !A.elem_rank_begin))
+    return LOR_ERR_INVALID_ARGUMENT;
+  lor_ctx c = new lor_ctx_s();
+  c->dim = A.dim;
+  c->p = A.p;
+  c->rank = A.rank;
+  c->nranks = A.nranks;
+  c->device = A.device;
+  c->stream = reinterpret_cast<cudaStream_t>(A.cuda_stream);
+  c->nel = A.n_elem;
+  auto bail = [&](lor_status st, const std::string &msg) {
+    lor_destroy(c);
+    (void)msg;
+    return st;
+  };
+  if (cudaSetDevice(A.device) != cudaSuccess) return bail(LOR_ERR_CUDA, "cudaSetDevice");
+  HostPlan plan;
+  try {
+    PlanInput in;
+    in.dim = A.dim;
+    in.p = A.p;
+    in.rank = A.rank;
+    in.nranks = A.nranks;
+    in.n_vert = A.n_vert;
+    in.n_elem = A.n_elem;
+    in.elem_vert = A.elem_vert;
+    in.elem_rank_begin = A.elem_rank_begin;
+    plan.build(in);
+  } catch (const std::exception &ex) {
+    fprintf(stderr, "lor_setup: %s\n", ex.what());
+    return bail(LOR_ERR_INVALID_ARGUMENT, ex.what());
+  }
+  c->elem_begin = plan.elem_begin;
+  c->nel_local = plan.nel_local;
+  c->ntopo = (int64_t)plan.topo.size();
+  // coordinates: local elements, element stride padded to 16 doubles (128 B)
+  const int np = (A.dim == 3) ? (A.p + 1) * (A.p + 1) * (A.p + 1) : (A.p + 1) * (A.p + 1);
+  const int64_t raw = (int64_t)A.dim * np;
+  c->xstride = (raw + 15) / 16 * 16;
+  {
+    std::vector<double> tmp;
+    const double *src = nullptr;
+    if (A.elem_nodes) src = A.elem_nodes + plan.elem_begin * raw;
+    else {
+      interpolate_evector(A.dim, A.p, A.vert_xyz, A.elem_vert, plan.elem_begin, plan.nel_local, tmp);
+      src = tmp.data();
+    }
+    std::vector<double> padded((size_t)(plan.nel_local * c->xstride), 0.0);
+    for (int64_t e = 0; e < plan.nel_local; ++e) memcpy(&padded[e * c->xstride], src + e * raw, sizeof(double) * raw);
+    if (dev_upload(c, &c->X, padded.data(), padded.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "X");
+  }
+  if (dev_upload(c, &c->topo, plan.topo.data(), plan.topo.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "topo");
+  if (dev_alloc(c, &c->err, 4) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "err");
+  for (int i = 0; i < 8; ++i) cudaEventCreate(&c->ev[i]);
+  int max_smem = 0;
+  for (int s = 0; s < 3; ++s) {
+    const SpacePlan &P = plan.sp[s];
+    SpaceDev &S = c->sp[s];
+    S.valid = P.valid;
+    if (!P.valid) continue;
+    S.ndpe = P.ndpe;
+    S.maxl = P.maxl;
+    S.rstride = (P.maxl * 16 + 127) / 128 * 8;  // records padded to whole 128-byte lines
+    S.n_global = P.n_global;
+    S.row_begin = P.row_begin;
+    S.n_local = P.n_local;
+    for (int t = 0; t < 4; ++t)
+      if (dev_upload(c, &S.base[t], P.base[t].data(), P.base[t].size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "base");
+    if (dev_upload(c, &S.esp, P.esp.data(), P.esp.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "esp");
+    if (dev_upload(c, &S.ose, P.ose.data(), P.ose.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "ose");
+    if (dev_upload(c, &S.ose_slots, P.ose_slots.data(), P.ose_slots.size()) != cudaSuccess)
+      return bail(LOR_ERR_OUT_OF_MEMORY, "ose_slots");
+    if (dev_upload(c, &S.defer, P.defer.data(), P.defer.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "defer");
+    S.n_ose = (int)P.ose.size();
+    S.n_defer = (int)P.defer.size();
+    if (dev_alloc(c, &S.counters, P.ose.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "counters");
+    S.n_records = P.n_records;
+    if (P.n_records > 0) {
+      cudaError_t e = cudaMalloc((void **)&S.scratch, (size_t)P.n_records * S.rstride * sizeof(RecEntry));
+      if (e != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "scratch");
+      c->allocs.push_back(S.scratch);
+    }
+    if (dev_alloc(c, &S.cnt, (size_t)std::max<int64_t>(P.n_local, 1)) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "cnt");
+    if (dev_alloc(c, &S.scan_status, (size_t)scan_status_words(P.n_local)) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "scan");
+    if (dev_alloc(c, &S.tile_ctr, 1) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "tile");
+    S.recv_begin = P.recv_begin;
+    S.recv_count = P.recv_count;
+    S.send_begin = P.send_begin;
+    S.send_count = P.send_count;
+    int smem = 0;
+    AsmArgs dummy{};
+    launch_assemble(A.dim, s, A.p, 0, dummy, c->stream, &smem);
+    max_smem = std::max(max_smem, smem);
+  }
+  c->fin_smem = 48 * 1024;
+  // NCCL communicator
+  if (A.nranks > 1 && A.nccl_unique_id) {
+    std::string err;
+    if (!g_nccl.load(err)) return bail(LOR_ERR_NCCL, err);
+    ncclUniqueId id;
+    memcpy(&id, A.nccl_unique_id, sizeof(id));
+    if (g_nccl.CommInitRank(&c->comm, A.nranks, id, A.rank) != ncclSuccess) return bail(LOR_ERR_NCCL, "ncclCommInitRank");
+  } else if (A.nranks > 1) {
+    c->exchange_mode = 1;  // no communicator: single-process emulation (lor_exchange_copy)
+  }
+  // the pattern is topological: count + scan once so lor_query can report nnz
+  for (int s = 0; s < 3; ++s) {
+    SpaceDev &S = c->sp[s];
+    if (!S.valid) continue;
+    int64_t *rp = nullptr;
+    if (cudaMalloc((void **)&rp, sizeof(int64_t) * (S.n_local + 1)) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "rp");
+    if (run_count_scan(c, s, rp) != LOR_OK) { cudaFree(rp); return bail(LOR_ERR_CUDA, c->last_error); }
+    int64_t nnz = 0;
+    cudaStreamSynchronize(c->stream);
+    if (cudaMemcpy(&nnz, rp + S.n_local, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaFree(rp);
+      return bail(LOR_ERR_CUDA, "nnz readback");
+    }
+    cudaFree(rp);
+    S.nnz_local = nnz;
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(LOR_ERR_CUDA, "setup sync");
+  *out = c;
+  return LOR_OK;
+}
+
+lor_status lor_destroy(lor_ctx c) {
+  if (!c) return LOR_OK;
+  cudaSetDevice(c->device);
+  if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  for (void *p : c->allocs) cudaFree(p);
+  for (int i = 0; i < 8; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  delete c;
+  return LOR_OK;
+}
+
+lor_status lor_sync(lor_ctx c) {
+  if (!c) return LOR_ERR_INVALID_ARGUMENT;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  int err[4];
+  CUDA_TRY(c, cudaMemcpy(err, c->err, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err[0]) {
+    cudaMemset(c->err, 0, sizeof(err));
+    char buf[160];
+    snprintf(buf, sizeof buf, "degenerate-geometry(element=%d, cell=%d): det J <= 0", err[1], err[2]);
+    return fail(c, LOR_ERR_DEGENERATE_GEOMETRY, buf);
+  }
+  return LOR_OK;
+}
+
+const char *lor_last_error(lor_ctx c) { return c ? c->last_error.c_str() : "null context"; }
+
+lor_status lor_query(lor_ctx c, lor_space space, int64_t *n_rows_local, int64_t *row_begin, int64_t *n_rows_global,
+                     int64_t *nnz_local) {
+  if (!c || space < 0 || space > 2) return LOR_ERR_INVALID_ARGUMENT;
+  const SpaceDev &S = c->sp[space];
+  if (!S.valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
+  if (n_rows_local) *n_rows_local = S.n_local;
+  if (row_begin) *row_begin = S.row_begin;
+  if (n_rows_global) *n_rows_global = S.n_global;
+  if (nnz_local) *nnz_local = S.nnz_local;
+  return LOR_OK;
+}
+
+lor_status lor_query_discrete(lor_ctx c, int which, int64_t *n_rows_local, int64_t *nnz_local, int64_t *n_cols_global) {
+  if (!c || (which != 0 && which != 1)) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim != 3) return fail(c, LOR_ERR_UNSUPPORTED, "discrete operators need dim == 3");
+  const SpaceDev &R = c->sp[which == 0 ? SP_ND : SP_RT];
+  const SpaceDev &C = c->sp[which == 0 ? SP_H1 : SP_ND];
+  if (n_rows_local) *n_rows_local = R.n_local;
+  if (nnz_local) *nnz_local = R.n_local * (which == 0 ? 2 : 4);
+  if (n_cols_global) *n_cols_global = C.n_global;
+  return LOR_OK;
+}
+
+lor_status lor_assemble_h1(lor_ctx c, double alpha, double beta, lor_quad quad, lor_csr *out) {
+  return assemble(c, SP_H1, alpha, beta, quad, out);
+}
+lor_status lor_assemble_nd(lor_ctx c, double alpha, double beta, lor_quad quad, lor_csr *out) {
+  return assemble(c, SP_ND, alpha, beta, quad, out);
+}
+lor_status lor_assemble_rt(lor_ctx c, double alpha, double beta, lor_quad quad, lor_csr *out) {
+  return assemble(c, SP_RT, alpha, beta, quad, out);
+}
+
+lor_status lor_update_coordinates(lor_ctx c, const double *elem_nodes) {
+  if (!c || !elem_nodes) return LOR_ERR_INVALID_ARGUMENT;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int np = (c->dim == 3) ? (c->p + 1) * (c->p + 1) * (c->p + 1) : (c->p + 1) * (c->p + 1);
+  const size_t raw = (size_t)c->dim * np * sizeof(double);
+  if (c->nel_local > 0)
+    CUDA_TRY(c, cudaMemcpy2DAsync(c->X, c->xstride * sizeof(double), elem_nodes, raw, raw, (size_t)c->nel_local,
+                                  cudaMemcpyDefault, c->stream));
+  return LOR_OK;
+}
+
+lor_status lor_set_exchange(lor_ctx c, int mode) {
+  if (!c || (mode != 0 && mode != 1)) return LOR_ERR_INVALID_ARGUMENT;
+  if (mode == 0 && c->nranks > 1 && !c->comm) return fail(c, LOR_ERR_NCCL, "no NCCL communicator");
+  c->exchange_mode = mode;
+  return LOR_OK;
+}
+
+lor_status lor_exchange_copy(lor_ctx dst, lor_ctx src, lor_space space) {
+  if (!dst || !src || space < 0 || space > 2) return LOR_ERR_INVALID_ARGUMENT;
+  SpaceDev &D = dst->sp[space];
+  SpaceDev &S = src->sp[space];
+  const int q = src->rank, r = dst->rank;
+  if (D.recv_count[q] != S.send_count[r]) return fail(dst, LOR_ERR_INVALID_ARGUMENT, "exchange plan mismatch");
+  if (D.recv_count[q] == 0) return LOR_OK;
+  const size_t rb = (size_t)S.rstride * sizeof(RecEntry);
+  CUDA_TRY(dst, cudaStreamSynchronize(src->stream));
+  CUDA_TRY(dst, cudaMemcpyAsync(reinterpret_cast<char *>(D.scratch) + D.recv_begin[q] * rb,
+                                reinterpret_cast<char *>(S.scratch) + S.send_begin[r] * rb, D.recv_count[q] * rb,
+                                cudaMemcpyDeviceToDevice, dst->stream));
+  return LOR_OK;
+}
+
+lor_status lor_assemble_finish(lor_ctx c, lor_space space, lor_csr *out) {
+  if (!c || space < 0 || space > 2 || !out) return LOR_ERR_INVALID_ARGUMENT;
+  SpaceDev &S = c->sp[space];
+  if (!S.pending_exchange) return LOR_OK;
+  S.pending_exchange = 0;
+  lor_status st = finish(c, space, out);
+  if (st) return st;
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  return LOR_OK;
+}
+
+lor_status lor_discrete_grad(lor_ctx c, lor_csr *out) {
+  if (!c || !out) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim != 3) return fail(c, LOR_ERR_UNSUPPORTED, "dim == 3 only");
+  const SpaceDev &R = c->sp[SP_ND];
+  if (out->cap_nnz < 2 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 2 n_rows");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  DiscArgs a;
+  a.p = c->p;
+  a.nel_local = c->nel_local;
+  a.topo = c->topo;
+  fill_base(R, a.base_row);
+  fill_base(c->sp[SP_H1], a.base_col);
+  a.row_begin = R.row_begin;
+  a.col = out->col;
+  a.val = out->val;
+  CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 2, c->stream));
+  CUDA_TRY(c, launch_discrete(0, a, c->stream));
+  c->launches += 2;
+  return LOR_OK;
+}
+
+lor_status lor_discrete_curl(lor_ctx c, lor_csr *out) {
+  if (!c || !out) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim != 3) return fail(c, LOR_ERR_UNSUPPORTED, "dim == 3 only");
+  const SpaceDev &R = c->sp[SP_RT];
+  if (out->cap_nnz < 4 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 4 n_rows");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  DiscArgs a;
+  a.p = c->p;
+  a.nel_local = c->nel_local;
+  a.topo = c->topo;
+  fill_base(R, a.base_row);
+  fill_base(c->sp[SP_ND], a.base_col);
+  a.row_begin = R.row_begin;
+  a.col = out->col;
+  a.val = out->val;
+  CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 4, c->stream));
+  CUDA_TRY(c, launch_discrete(1, a, c->stream));
+  c->launches += 2;
+  return LOR_OK;
+}
+
+lor_status lor_dof_map(lor_ctx c, lor_space space, int32_t *elem_dofs, int8_t *signs) {
+  if (!c || space < 0 || space > 2 || !elem_dofs) return LOR_ERR_INVALID_ARGUMENT;
+  const SpaceDev &S = c->sp[space];
+  if (!S.valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  DofmapArgs a;
+  a.p = c->p;
+  a.ndpe = S.ndpe;
+  a.nel_local = c->nel_local;
+  a.topo = c->topo;
+  fill_base(S, a.base);
+  a.map = elem_dofs;
+  a.sign = signs;
+  CUDA_TRY(c, launch_dofmap(c->dim, space, a, c->stream));
+  c->launches++;
+  return LOR_OK;
+}
+
+lor_status lor_query_elements(lor_ctx c, int64_t *elem_begin, int64_t *n_elem_local, int *nh1, int *nnd, int *nrt) {
+  if (!c) return LOR_ERR_INVALID_ARGUMENT;
+  if (elem_begin) *elem_begin = c->elem_begin;
+  if (n_elem_local) *n_elem_local = c->nel_local;
+  if (nh1) *nh1 = c->sp[0].ndpe;
+  if (nnd) *nnd = c->sp[1].ndpe;
+  if (nrt) *nrt = c->sp[2].ndpe;
+  return LOR_OK;
+}
+
+int64_t lor_kernel_launches(lor_ctx c) { return c ? c->launches : 0; }
+
+int lor_last_phase_ms(lor_ctx c, float *ms, int cap) {
+  if (!c || !ms) return 0;
+  int n = 0;
+  for (int i = 0; i + 1 < c->nphase && n < cap; ++i) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, c->ev[i], c->ev[i + 1]) != cudaSuccess) t = -1.f;
+    ms[n++] = t;
+  }
+  return n;
+}
+
+}  // extern "C"

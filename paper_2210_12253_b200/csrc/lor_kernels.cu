@@ -1,0 +1,389 @@
+// lor_kernels.cu -- hand-written sm_100a fp64 kernels of the B200 LOR assembly library.
+//
+// Per assembly call (PAPER.md Step S1.2, A1-A3):
+//   k_count     A2 part 1: per (element, local row) the number of columns this element "owns"
+//               under the minimal-macro-element rule; exclusive rows are
+//               stored, shared rows accumulated with integer atomics.
+//   k_scan      A2: decoupled look-back exclusive scan -> int64 row_ptr.
+//   k_assemble  A1 + A2 part 2, fused: one CTA per macro element ("one block of
+//               threads per macro element"): sub-cell matrices from the E-vector geometry staged
+//               in shared memory (never written to HBM), then per local row the values gathered
+//               from the <= 2^d cells containing it and the columns emitted in ascending global
+//               order from the element's affine "block" numbering (no sort).  Rows owned by one
+//               element go straight to CSR; rows on shared coarse entities go to per-element
+//               partial-row records, merged by the LAST element to arrive (integer counter),
+//               which writes the final row -- the "minimal element" duplicate rule of l.358 is
+//               replaced by exact weighted merge counts.
+//   k_finalize_deferred  interface rows whose partial rows came over NCCL (A3 replacement).
+//   k_grad / k_curl      discrete gradient (Algorithm 1, l.417-438) / curl (l.440-445).
+//   k_dofmap    element restriction (for parity tests of the numbering).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lor_cells.cuh"
+#include "lor_device.cuh"
+#include "lor_kernels.h"
+#include "lor_asm.cuh"
+
+namespace lorb {
+
+// ================================================================================ k_count
+template <int DIM, int SP>
+__global__ void __launch_bounds__(128) k_count(CountArgs A) {
+  constexpr int S = Tr<DIM, SP>::S;
+  const int64_t ei = blockIdx.x;
+  if (ei >= A.ntopo) return;
+  __shared__ ElemTopo T;
+  {
+    const int4 *src = reinterpret_cast<const int4 *>(A.topo + ei);
+    int4 *dst = reinterpret_cast<int4 *>(&T);
+    for (int i = threadIdx.x; i < (int)(sizeof(ElemTopo) / 16); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int p = A.p;
+  const int ndpe = A.ndpe;
+  for (int l = threadIdx.x; l < ndpe; l += blockDim.x) {
+    int s, x[3];
+    decode_local<DIM, SP>(p, l, s, x);
+    const int tr = row_tau<DIM, SP>(p, s, x);
+    if (!(T.flags[tr] & TF_OWNED)) continue;
+    Blk B;
+    block_affine<DIM, SP>(p, s, tr, T, A.base, B);
+    const int gid = B.g0 + B.str[0] * x[0] + B.str[1] * x[1] + B.str[2] * x[2];
+    int cr[3];
+    for (int a = 0; a < 3; ++a) cr[a] = (a < DIM) ? coord_cls(vkind<SP>(s, a), x[a], p) : 1;
+    int cnt = 0;
+#pragma unroll
+    for (int s2 = 0; s2 < S; ++s2) {
+      int L[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (a < DIM) {
+            int lo, hi;
+            seg_bounds<SP>(p, s, s2, a, x[a], c, lo, hi);
+            L[a][c] = hi >= lo ? hi - lo + 1 : 0;
+          } else {
+            L[a][c] = (c == 1) ? 1 : 0;
+          }
+        }
+#pragma unroll
+      for (int cz = 0; cz < 3; ++cz)
+#pragma unroll
+        for (int cy = 0; cy < 3; ++cy)
+#pragma unroll
+          for (int cx = 0; cx < 3; ++cx) {
+            const int n = L[0][cx] * L[1][cy] * L[2][cz];
+            if (n == 0) continue;
+            int tj = join_cls(cr[0], cx) + 3 * join_cls(cr[1], cy);
+            if (DIM == 3) tj += 9 * join_cls(cr[2], cz);
+            if (T.flags[tj] & TF_MIN) cnt += n;
+          }
+    }
+    int32_t *dst = A.cnt + (gid - A.row_begin);
+    if (T.val[tr] <= 1) *dst = cnt;
+    else atomicAdd(dst, cnt);
+  }
+}
+
+// ================================================================================ k_scan
+// Decoupled look-back exclusive scan (single pass).  Tile = 128 threads x 16 items.
+constexpr int SCAN_T = 128, SCAN_I = 16, SCAN_TILE = SCAN_T * SCAN_I;
+constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(SCAN_T) k_scan(const int32_t *__restrict__ cnt, int64_t *__restrict__ row_ptr, int64_t n,
+                                                 unsigned long long *status, unsigned int *tile_ctr) {
+  __shared__ unsigned int s_tile;
+  __shared__ long long s_warp[SCAN_T / 32];
+  __shared__ long long s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_I;
+  int v[SCAN_I];
+  long long tsum = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_I; ++i) {
+    const int64_t k = base + i;
+    v[i] = (k < n) ? cnt[k] : 0;
+    tsum += v[i];
+  }
+  // block-level exclusive scan of thread sums
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long incl = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  long long woff = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < SCAN_T / 32; ++w) {
+    if (w < wid) woff += s_warp[w];
+    total += s_warp[w];
+  }
+  const long long texcl = woff + incl - tsum;
+  // look-back (warp 0)
+  if (wid == 0) {
+    long long prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(status + tile, FLAG_P | (unsigned long long)total);
+      }
+    } else {
+      if (lane == 0) atomicExch(status + tile, FLAG_A | (unsigned long long)total);
+      int64_t look = tile - 1;
+      while (true) {
+        const int64_t idx = look - lane;
+        unsigned long long st = 0;
+        if (idx >= 0) {
+          do {
+            st = atomicAdd(status + idx, 0ull);
+          } while ((st >> 62) == 0);
+        } else {
+          st = FLAG_P;  // before the first tile: inclusive prefix 0
+        }
+        const unsigned pmask = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        // lanes up to (and including) the first P flag contribute
+        const int firstp = pmask ? __ffs(pmask) - 1 : 32;
+        long long contrib = (lane <= firstp) ? (long long)(st & VAL_MASK) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+        prefix += contrib;
+        if (pmask) break;
+        look -= 32;
+      }
+      if (lane == 0) atomicExch(status + tile, FLAG_P | (unsigned long long)(prefix + total));
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  long long run = s_prefix + texcl;
+#pragma unroll
+  for (int i = 0; i < SCAN_I; ++i) {
+    const int64_t k = base + i;
+    if (k < n) row_ptr[k] = run;
+    run += v[i];
+  }
+  if (base <= n - 1 && n - 1 < base + SCAN_I) row_ptr[n] = run;  // thread holding the last item
+  if (n == 0 && tile == 0 && threadIdx.x == 0) row_ptr[0] = 0;
+}
+
+__global__ void __launch_bounds__(128) k_finalize_list(FinArgs F) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int i = blockIdx.x;
+  if (i >= F.n) return;
+  const Ose O = F.ose[F.list[i]];
+  finalize_ose(O, F.ose_slots, F.scratch, F.rstride, F.row_begin, F.row_ptr, F.col, F.val, smem, F.smem_bytes);
+}
+
+// ================================================================================ G, C, dof map
+// One CTA per local element; the row's element writes it if it is the minimal element containing
+// the row's entity (rows owned by this rank).  Columns sorted ascending (reading P-5).
+template <int WHICH>  // 0 = gradient (ND rows, H1 cols), 1 = curl (RT rows, ND cols)
+__global__ void __launch_bounds__(128) k_discrete(DiscArgs A) {
+  constexpr int RSP = WHICH == 0 ? SP_ND : SP_RT;
+  constexpr int CSP = WHICH == 0 ? SP_H1 : SP_ND;
+  constexpr int CS = Tr<3, CSP>::S;
+  __shared__ ElemTopo T;
+  __shared__ Blk brow[81];
+  __shared__ Blk bcol[81];
+  const int64_t el = blockIdx.x;
+  if (el >= A.nel_local) return;
+  {
+    const int4 *src = reinterpret_cast<const int4 *>(A.topo + el);
+    int4 *dst = reinterpret_cast<int4 *>(&T);
+    for (int i = threadIdx.x; i < (int)(sizeof(ElemTopo) / 16); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int p = A.p;
+  if (threadIdx.x < 81) {
+    const int s = threadIdx.x / 27, tau = threadIdx.x % 27;
+    block_affine<3, RSP>(p, s, tau, T, A.base_row, brow[threadIdx.x]);
+    if (s < CS) block_affine<3, CSP>(p, s, tau, T, A.base_col, bcol[threadIdx.x]);
+  }
+  __syncthreads();
+  const int ndpe = (WHICH == 0) ? 3 * p * (p + 1) * (p + 1) : 3 * p * p * (p + 1);
+  for (int l = threadIdx.x; l < ndpe; l += blockDim.x) {
+    int s, x[3];
+    decode_local<3, RSP>(p, l, s, x);
+    const int tr = row_tau<3, RSP>(p, s, x);
+    if (!(T.flags[tr] & TF_OWNED) || !(T.flags[tr] & TF_MIN)) continue;
+    const Blk &B = brow[s * 27 + tr];
+    const int gid = B.g0 + B.str[0] * x[0] + B.str[1] * x[1] + B.str[2] * x[2];
+    const int64_t row = gid - A.row_begin;
+    if (WHICH == 0) {
+      int y[3] = {x[0], x[1], x[2]};
+      const int tt = row_tau<3, SP_H1>(p, 0, y);
+      const Blk &Bt = bcol[tt];
+      const int gt = Bt.g0 + Bt.str[0] * y[0] + Bt.str[1] * y[1] + Bt.str[2] * y[2];
+      y[s] += 1;
+      const int th = row_tau<3, SP_H1>(p, 0, y);
+      const Blk &Bh = bcol[th];
+      const int gh = Bh.g0 + Bh.str[0] * y[0] + Bh.str[1] * y[1] + Bh.str[2] * y[2];
+      const double sg = (double)B.sigma;
+      const bool sw = gh < gt;
+      A.col[2 * row] = sw ? gh : gt;
+      A.col[2 * row + 1] = sw ? gt : gh;
+      A.val[2 * row] = sw ? sg : -sg;
+      A.val[2 * row + 1] = sw ? -sg : sg;
+    } else {
+      // face (s, x): cyclic in-face axes (u', v') = (s+1, s+2) mod 3; edges:
+      // u'-edge at v'=0 (+1), v'-edge at u'=1 (+1), u'-edge at v'=1 (-1), v'-edge at u'=0 (-1)
+      const int up = (s + 1) % 3, vp = (s + 2) % 3;
+      int c[4];
+      double v[4];
+      const int eax[4] = {up, vp, up, vp};
+      const int eoff[4] = {0, 1, 1, 0};
+      const double es[4] = {1.0, 1.0, -1.0, -1.0};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int y[3] = {x[0], x[1], x[2]};
+        const int other = (eax[q] == up) ? vp : up;
+        y[other] += eoff[q];
+        const int te = row_tau<3, SP_ND>(p, eax[q], y);
+        const Blk &Be = bcol[eax[q] * 27 + te];
+        c[q] = Be.g0 + Be.str[0] * y[0] + Be.str[1] * y[1] + Be.str[2] * y[2];
+        v[q] = es[q] * (double)B.sigma * (double)Be.sigma;
+      }
+      // sort 4 (network)
+#define CSWAP(i, j)                                   \
+  if (c[j] < c[i]) {                                  \
+    int tc = c[i]; c[i] = c[j]; c[j] = tc;            \
+    double tv = v[i]; v[i] = v[j]; v[j] = tv;         \
+  }
+      CSWAP(0, 1) CSWAP(2, 3) CSWAP(0, 2) CSWAP(1, 3) CSWAP(1, 2)
+#undef CSWAP
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        A.col[4 * row + q] = c[q];
+        A.val[4 * row + q] = v[q];
+      }
+    }
+  }
+}
+
+template <int DIM, int SP>
+__global__ void __launch_bounds__(128) k_dofmap(DofmapArgs A) {
+  __shared__ ElemTopo T;
+  __shared__ Blk blk[81];
+  const int64_t el = blockIdx.x;
+  if (el >= A.nel_local) return;
+  {
+    const int4 *src = reinterpret_cast<const int4 *>(A.topo + el);
+    int4 *dst = reinterpret_cast<int4 *>(&T);
+    for (int i = threadIdx.x; i < (int)(sizeof(ElemTopo) / 16); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  constexpr int S = Tr<DIM, SP>::S;
+  if (threadIdx.x < S * 27) {
+    const int s = threadIdx.x / 27, tau = threadIdx.x % 27;
+    if (DIM == 2 && tau >= 9) blk[threadIdx.x].size = 0;
+    else block_affine<DIM, SP>(A.p, s, tau, T, A.base, blk[threadIdx.x]);
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < A.ndpe; l += blockDim.x) {
+    int s, x[3];
+    decode_local<DIM, SP>(A.p, l, s, x);
+    const int tr = row_tau<DIM, SP>(A.p, s, x);
+    const Blk &B = blk[s * 27 + tr];
+    A.map[el * A.ndpe + l] = B.g0 + B.str[0] * x[0] + B.str[1] * x[1] + B.str[2] * x[2];
+    if (A.sign) A.sign[el * A.ndpe + l] = B.sigma;
+  }
+}
+
+__global__ void k_rowptr_stride(int64_t *row_ptr, int64_t n, int w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    row_ptr[i] = (int64_t)w * i;
+}
+
+cudaError_t launch_rowptr_stride(int64_t *row_ptr, int64_t n, int w, cudaStream_t st) {
+  int64_t blocks = (n + 1 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_rowptr_stride<<<(unsigned)blocks, 256, 0, st>>>(row_ptr, n, w);
+  return cudaGetLastError();
+}
+
+// ================================================================================ launchers
+template <int DIM, int SP>
+static cudaError_t launch_count_t(const CountArgs &a, int64_t grid, cudaStream_t st) {
+  if (grid <= 0) return cudaSuccess;
+  k_count<DIM, SP><<<(unsigned)grid, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count(int dim, int space, const CountArgs &a, cudaStream_t st) {
+  if (dim == 2) return launch_count_t<2, SP_H1>(a, a.ntopo, st);
+  if (space == SP_H1) return launch_count_t<3, SP_H1>(a, a.ntopo, st);
+  if (space == SP_ND) return launch_count_t<3, SP_ND>(a, a.ntopo, st);
+  return launch_count_t<3, SP_RT>(a, a.ntopo, st);
+}
+
+cudaError_t launch_scan(const int32_t *cnt, int64_t *row_ptr, int64_t n, unsigned long long *status,
+                        unsigned int *tile_ctr, cudaStream_t st) {
+  const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (tiles + 1), st);
+  cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned int), st);
+  k_scan<<<(unsigned)(tiles > 0 ? tiles : 1), SCAN_T, 0, st>>>(cnt, row_ptr, n, status, tile_ctr);
+  return cudaGetLastError();
+}
+
+int64_t scan_status_words(int64_t n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 1; }
+
+// per-(dim, space, p) launchers live in generated translation units (build.py)
+#define LOR_DECL_ASM(D, SPC, P) cudaError_t launch_asm_##D##_##SPC##_##P(const AsmArgs &, int, cudaStream_t, int *);
+#define LOR_DECL_ALLP(D, SPC) LOR_DECL_ASM(D, SPC, 1) LOR_DECL_ASM(D, SPC, 2) LOR_DECL_ASM(D, SPC, 3) \
+  LOR_DECL_ASM(D, SPC, 4) LOR_DECL_ASM(D, SPC, 5) LOR_DECL_ASM(D, SPC, 6) LOR_DECL_ASM(D, SPC, 7) LOR_DECL_ASM(D, SPC, 8)
+LOR_DECL_ALLP(2, 0)
+LOR_DECL_ALLP(3, 0)
+LOR_DECL_ALLP(3, 1)
+LOR_DECL_ALLP(3, 2)
+
+#define LOR_SWITCH_P(D, SPC)                                          \
+  switch (p) {                                                        \
+    case 1: return launch_asm_##D##_##SPC##_1(a, quad, st, smem_out); \
+    case 2: return launch_asm_##D##_##SPC##_2(a, quad, st, smem_out); \
+    case 3: return launch_asm_##D##_##SPC##_3(a, quad, st, smem_out); \
+    case 4: return launch_asm_##D##_##SPC##_4(a, quad, st, smem_out); \
+    case 5: return launch_asm_##D##_##SPC##_5(a, quad, st, smem_out); \
+    case 6: return launch_asm_##D##_##SPC##_6(a, quad, st, smem_out); \
+    case 7: return launch_asm_##D##_##SPC##_7(a, quad, st, smem_out); \
+    case 8: return launch_asm_##D##_##SPC##_8(a, quad, st, smem_out); \
+    default: return cudaErrorInvalidValue;                            \
+  }
+
+cudaError_t launch_assemble(int dim, int space, int p, int quad, const AsmArgs &a, cudaStream_t st, int *smem_out) {
+  if (dim == 2) { LOR_SWITCH_P(2, 0) }
+  if (space == SP_H1) { LOR_SWITCH_P(3, 0) }
+  if (space == SP_ND) { LOR_SWITCH_P(3, 1) }
+  LOR_SWITCH_P(3, 2)
+}
+
+cudaError_t launch_finalize_list(const FinArgs &f, cudaStream_t st) {
+  if (f.n <= 0) return cudaSuccess;
+  cudaFuncSetAttribute(k_finalize_list, cudaFuncAttributeMaxDynamicSharedMemorySize, f.smem_bytes);
+  k_finalize_list<<<(unsigned)f.n, 128, f.smem_bytes, st>>>(f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_discrete(int which, const DiscArgs &a, cudaStream_t st) {
+  if (a.nel_local <= 0) return cudaSuccess;
+  if (which == 0) k_discrete<0><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  else k_discrete<1><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dofmap(int dim, int space, const DofmapArgs &a, cudaStream_t st) {
+  if (a.nel_local <= 0) return cudaSuccess;
+  if (dim == 2) k_dofmap<2, SP_H1><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  else if (space == SP_H1) k_dofmap<3, SP_H1><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  else if (space == SP_ND) k_dofmap<3, SP_ND><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  else k_dofmap<3, SP_RT><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace lorb

@@ -1,0 +1,220 @@
+"""Thin Python binding of the C ABI in include/lor.h (argument marshalling only).
+
+Every step of the assembly runs in liblor_b200.so (hand-written sm_100a kernels).  There is no
+CPU or PyTorch fallback: if the library or a GPU is missing, constructing ``LOR`` raises.
+PyTorch provides device memory (the caller-owned output buffers) and the CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblor_b200.so")
+
+H1, ND, RT = 0, 1, 2
+SPACES = {"h1": H1, "nd": ND, "rt": RT}
+QUADS = {"vertex": 0, "gauss2": 1}
+STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "DEGENERATE_GEOMETRY", 3: "OUT_OF_MEMORY", 4: "CUDA", 5: "NCCL",
+          6: "UNSUPPORTED", 7: "BUFFER_TOO_SMALL"}
+
+
+class LorError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"lor error {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _SetupArgs(C.Structure):
+    _fields_ = [("dim", C.c_int), ("p", C.c_int), ("n_vert", C.c_int64), ("vert_xyz", C.c_void_p),
+                ("n_elem", C.c_int64), ("elem_vert", C.c_void_p), ("elem_nodes", C.c_void_p), ("rank", C.c_int),
+                ("nranks", C.c_int), ("elem_rank_begin", C.c_void_p), ("nccl_unique_id", C.c_void_p),
+                ("cuda_stream", C.c_void_p), ("device", C.c_int)]
+
+
+class _Csr(C.Structure):
+    _fields_ = [("row_ptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p), ("cap_nnz", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load liblor_b200.so from the package directory (never a fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LorError(-1, f"{LIB_PATH} not built; run python -m paper_2210_12253_b200.build")
+        L = C.CDLL(LIB_PATH)
+        L.lor_last_error.restype = C.c_char_p
+        L.lor_kernel_launches.restype = C.c_int64
+        L.lor_setup.argtypes = [C.POINTER(_SetupArgs), C.POINTER(C.c_void_p)]
+        for name in ("lor_destroy", "lor_sync"):
+            getattr(L, name).argtypes = [C.c_void_p]
+        L.lor_last_error.argtypes = [C.c_void_p]
+        L.lor_kernel_launches.argtypes = [C.c_void_p]
+        L.lor_query.argtypes = [C.c_void_p, C.c_int] + [C.POINTER(C.c_int64)] * 4
+        L.lor_query_discrete.argtypes = [C.c_void_p, C.c_int] + [C.POINTER(C.c_int64)] * 3
+        for name in ("lor_assemble_h1", "lor_assemble_nd", "lor_assemble_rt"):
+            getattr(L, name).argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int, C.POINTER(_Csr)]
+        L.lor_discrete_grad.argtypes = [C.c_void_p, C.POINTER(_Csr)]
+        L.lor_discrete_curl.argtypes = [C.c_void_p, C.POINTER(_Csr)]
+        L.lor_dof_map.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.lor_query_elements.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.lor_nccl_get_unique_id.argtypes = [C.c_void_p]
+        L.lor_set_exchange.argtypes = [C.c_void_p, C.c_int]
+        L.lor_exchange_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        L.lor_assemble_finish.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Csr)]
+        L.lor_update_coordinates.argtypes = [C.c_void_p, C.c_void_p]
+        L.lor_last_phase_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int]
+        _lib = L
+    return _lib
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    rc = lib().lor_nccl_get_unique_id(buf)
+    if rc:
+        raise LorError(rc, "ncclGetUniqueId")
+    return bytes(buf)
+
+
+class LOR:
+    """One context per rank/GPU.  ``mesh`` provides ``dim, p, vert, elem, X`` (numpy)."""
+
+    def __init__(self, mesh, *, rank=0, nranks=1, elem_rank_begin=None, nccl_id: bytes | None = None,
+                 stream=None, device=None, use_evector=True):
+        import torch
+        if not torch.cuda.is_available():
+            raise LorError(4, "no CUDA device: the LOR library has no CPU path")
+        self.torch = torch
+        self.device = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.dim, self.p = int(mesh.dim), int(mesh.p)
+        self._vert = np.ascontiguousarray(mesh.vert, dtype=np.float64)
+        self._elem = np.ascontiguousarray(mesh.elem, dtype=np.int64)
+        self._X = np.ascontiguousarray(mesh.X, dtype=np.float64) if use_evector else None
+        erb = elem_rank_begin if elem_rank_begin is not None else (
+            mesh.elem_rank_begin if (nranks > 1 and getattr(mesh, "elem_rank_begin", None) is not None) else None)
+        self._erb = np.ascontiguousarray(erb, dtype=np.int64) if erb is not None else None
+        self._nccl = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        a = _SetupArgs()
+        a.dim, a.p = self.dim, self.p
+        a.n_vert = self._vert.shape[0]
+        a.vert_xyz = self._vert.ctypes.data
+        a.n_elem = self._elem.shape[0]
+        a.elem_vert = self._elem.ctypes.data
+        a.elem_nodes = self._X.ctypes.data if self._X is not None else None
+        a.rank, a.nranks = rank, nranks
+        a.elem_rank_begin = self._erb.ctypes.data if self._erb is not None else None
+        a.nccl_unique_id = C.cast(self._nccl, C.c_void_p) if self._nccl is not None else None
+        a.cuda_stream = self.stream.cuda_stream
+        a.device = self.device.index
+        h = C.c_void_p()
+        rc = lib().lor_setup(C.byref(a), C.byref(h))
+        if rc:
+            raise LorError(rc, "lor_setup failed (see stderr)")
+        self.h = h
+        self.rank, self.nranks = rank, nranks
+        eb, ne = C.c_int64(), C.c_int64()
+        n1, n2, n3 = C.c_int(), C.c_int(), C.c_int()
+        self._check(lib().lor_query_elements(self.h, C.byref(eb), C.byref(ne), C.byref(n1), C.byref(n2), C.byref(n3)))
+        self.elem_begin, self.n_elem_local = eb.value, ne.value
+        self.ndpe = {H1: n1.value, ND: n2.value, RT: n3.value}
+
+    # ------------------------------------------------------------------ plumbing
+    def _check(self, rc):
+        if rc:
+            raise LorError(rc, lib().lor_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().lor_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        self._check(lib().lor_sync(self.h))
+
+    def launches(self) -> int:
+        return int(lib().lor_kernel_launches(self.h))
+
+    def phase_ms(self):
+        buf = (C.c_float * 8)()
+        n = lib().lor_last_phase_ms(self.h, buf, 8)
+        return [buf[i] for i in range(n)]
+
+    def update_coordinates(self, X_local):
+        """X_local: this rank's E-vector slice, a torch tensor (pinned host or device) or numpy array."""
+        ptr = X_local.data_ptr() if hasattr(X_local, "data_ptr") else X_local.ctypes.data
+        self._check(lib().lor_update_coordinates(self.h, C.c_void_p(ptr)))
+
+    def set_exchange(self, mode: int):
+        self._check(lib().lor_set_exchange(self.h, mode))
+
+    # ------------------------------------------------------------------ queries
+    def query(self, space):
+        sp = SPACES.get(space, space)
+        v = [C.c_int64() for _ in range(4)]
+        self._check(lib().lor_query(self.h, sp, *[C.byref(x) for x in v]))
+        return dict(n_local=v[0].value, row_begin=v[1].value, n_global=v[2].value, nnz=v[3].value)
+
+    def query_discrete(self, which):
+        w = {"grad": 0, "curl": 1}.get(which, which)
+        v = [C.c_int64() for _ in range(3)]
+        self._check(lib().lor_query_discrete(self.h, w, *[C.byref(x) for x in v]))
+        return dict(n_local=v[0].value, nnz=v[1].value, n_cols=v[2].value)
+
+    # ------------------------------------------------------------------ outputs
+    def alloc(self, n_rows, nnz):
+        t = self.torch
+        return (t.empty(n_rows + 1, dtype=t.int64, device=self.device), t.empty(max(nnz, 1), dtype=t.int32, device=self.device),
+                t.empty(max(nnz, 1), dtype=t.float64, device=self.device))
+
+    @staticmethod
+    def _csr(rp, col, val):
+        c = _Csr()
+        c.row_ptr, c.col, c.val = rp.data_ptr(), col.data_ptr(), val.data_ptr()
+        c.cap_nnz = col.numel()
+        return c
+
+    def assemble(self, space="h1", alpha=1.0, beta=1.0, quad="vertex", out=None):
+        """Enqueue LOR assembly on the context stream; returns (row_ptr, col, val) device tensors."""
+        sp = SPACES.get(space, space)
+        q = self.query(sp)
+        if out is None:
+            out = self.alloc(q["n_local"], q["nnz"])
+        fn = (lib().lor_assemble_h1, lib().lor_assemble_nd, lib().lor_assemble_rt)[sp]
+        self._check(fn(self.h, C.c_double(alpha), C.c_double(beta), QUADS.get(quad, quad), C.byref(self._csr(*out))))
+        return out
+
+    def exchange_copy_from(self, src: "LOR", space):
+        self._check(lib().lor_exchange_copy(self.h, src.h, SPACES.get(space, space)))
+
+    def assemble_finish(self, space, out):
+        self._check(lib().lor_assemble_finish(self.h, SPACES.get(space, space), C.byref(self._csr(*out))))
+
+    def discrete(self, which="grad", out=None):
+        q = self.query_discrete(which)
+        if out is None:
+            out = self.alloc(q["n_local"], q["nnz"])
+        fn = lib().lor_discrete_grad if which in ("grad", 0) else lib().lor_discrete_curl
+        self._check(fn(self.h, C.byref(self._csr(*out))))
+        return out
+
+    def dof_map(self, space="h1"):
+        t = self.torch
+        sp = SPACES.get(space, space)
+        n = self.ndpe[sp]
+        m = t.empty((self.n_elem_local, n), dtype=t.int32, device=self.device)
+        s = t.empty((self.n_elem_local, n), dtype=t.int8, device=self.device)
+        self._check(lib().lor_dof_map(self.h, sp, C.c_void_p(m.data_ptr()), C.c_void_p(s.data_ptr())))
+        return m, s

@@ -1,0 +1,154 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bit-exact: row_ptr, col, dof maps, signs, discrete gradient/curl.  Values: DESIGN.md P-10 rule.
+Meshes: Cartesian, jittered, Kershaw, orientation-scrambled; every p = 1..8 on small meshes that
+still span several elements and ragged tails; both quadrature rules; multi-rank emulation.
+"""
+import numpy as np
+import pytest
+
+from paper_2210_12253_b200 import meshgen as mg
+from tests.parity import compare_full, compare_rows, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return torch
+
+
+def run_case(O, mesh, space, quad="vertex", alpha=1.0, beta=1.0, what=""):
+    from paper_2210_12253_b200.lor import LOR
+    ctx = LOR(mesh)
+    q = ctx.query(space)
+    rp, col, val = ctx.assemble(space, alpha, beta, quad)
+    ctx.sync()
+    ref = O.assemble(mesh, space, quad, alpha, beta)
+    assert q["nnz"] == ref.nnz, f"{what}: nnz gpu {q['nnz']} oracle {ref.nnz}"
+    assert q["n_local"] == ref.row_ptr.shape[0] - 1
+    res = compare_full(to_host(rp), to_host(col), to_host(val), ref, 0, q["n_local"], what)
+    ctx.close()
+    return res
+
+
+def test_c1_2d(torch_cuda, oracle_lib):
+    m, form = mg.config_mesh("C1")
+    for quad in ("vertex", "gauss2"):
+        run_case(oracle_lib, m, "h1", quad, 1.0, 0.0, f"C1 {quad}")
+        run_case(oracle_lib, m, "h1", quad, 1.0, 1.0, f"C1 {quad} mass")
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_2d_p(torch_cuda, oracle_lib, p):
+    m = mg.box_mesh(2, (3, 2), p, jitter=True, scramble=True)
+    run_case(oracle_lib, m, "h1", "vertex", 1.3, 0.7, f"2D p={p}")
+
+
+@pytest.mark.parametrize("space", ["h1", "nd", "rt"])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_3d_p(torch_cuda, oracle_lib, space, p):
+    shape = (3, 2, 2) if p <= 4 else (2, 2, 2)
+    m = mg.box_mesh(3, shape, p, jitter=True, scramble=True)
+    run_case(oracle_lib, m, space, "vertex", 1.3, 0.7, f"{space} p={p}")
+
+
+@pytest.mark.parametrize("space", ["h1", "nd", "rt"])
+@pytest.mark.parametrize("kind", ["cartesian", "kershaw", "gauss2"])
+def test_3d_geometries(torch_cuda, oracle_lib, space, kind):
+    if kind == "cartesian":
+        m, quad = mg.box_mesh(3, (3, 3, 2), 4), "vertex"
+    elif kind == "kershaw":
+        m, quad = mg.box_mesh(3, (6, 2, 2), 3, kershaw=0.3), "vertex"
+    else:
+        m, quad = mg.box_mesh(3, (2, 3, 2), 3, jitter=True, scramble=True), "gauss2"
+    run_case(oracle_lib, m, space, quad, 1.0, 1.0, f"{space} {kind}")
+
+
+@pytest.mark.parametrize("space", ["h1", "nd", "rt"])
+def test_dof_maps_bit_exact(torch_cuda, oracle_lib, space):
+    from paper_2210_12253_b200.lor import LOR
+    m = mg.box_mesh(3, (3, 2, 2), 3, jitter=True, scramble=True)
+    ctx = LOR(m)
+    gm, gs = ctx.dof_map(space)
+    om, os_ = oracle_lib.dof_map(m, space)
+    np.testing.assert_array_equal(to_host(gm), om)
+    if space != "h1":
+        np.testing.assert_array_equal(to_host(gs), os_)
+
+
+@pytest.mark.parametrize("which", ["grad", "curl"])
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_discrete_bit_exact(torch_cuda, oracle_lib, which, p):
+    from paper_2210_12253_b200.lor import LOR
+    m = mg.box_mesh(3, (3, 2, 2), p, jitter=True, scramble=True)
+    ctx = LOR(m)
+    rp, col, val = ctx.discrete(which)
+    ctx.sync()
+    ref = oracle_lib.discrete(m, which)
+    np.testing.assert_array_equal(to_host(rp), ref.row_ptr)
+    np.testing.assert_array_equal(to_host(col), ref.col)
+    np.testing.assert_array_equal(to_host(val), ref.val)
+
+
+@pytest.mark.parametrize("space", ["h1", "nd", "rt"])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_multirank_emulated(torch_cuda, oracle_lib, space, nranks):
+    """several ranks in one process on one GPU: manual exchange of interface partial rows
+    (same kernels and buffers as the NCCL path); union of owned rows == oracle (rank-major)."""
+    from paper_2210_12253_b200.lor import LOR
+    p = 3
+    m = mg.box_mesh(3, (2, 2, 2 * nranks), p, jitter=True, scramble=True, nranks=nranks)
+    ctxs = [LOR(m, rank=r, nranks=nranks) for r in range(nranks)]
+    outs = [c.assemble(space, 1.0, 1.0, "vertex") for c in ctxs]
+    for c in ctxs:
+        c.sync()
+    for r, c in enumerate(ctxs):
+        for q, src in enumerate(ctxs):
+            if q != r:
+                c.exchange_copy_from(src, space)
+        c.assemble_finish(space, outs[r])
+        c.sync()
+    ref = oracle_lib.assemble(m, space, "vertex", 1.0, 1.0)
+    for r, c in enumerate(ctxs):
+        q = c.query(space)
+        rp, col, val = (to_host(t) for t in outs[r])
+        compare_full(rp, col, val, ref, q["row_begin"], q["n_local"], f"{space} rank {r}/{nranks}")
+
+
+def test_degenerate_geometry_reported(torch_cuda):
+    from paper_2210_12253_b200.lor import LOR, LorError
+    m = mg.box_mesh(3, (2, 2, 2), 2)
+    X = m.X.copy()
+    X[3, 0, :] = X[3, 0, ::-1].copy()  # mirror one element in x: det J < 0
+    m.X = X
+    ctx = LOR(m)
+    ctx.assemble("h1")
+    with pytest.raises(LorError) as ei:
+        ctx.sync()
+    assert "degenerate-geometry(element=3" in str(ei.value)
+
+
+def test_full_size_c2_row_sampled(torch_cuda, oracle_lib):
+    """BASELINE configs[1] (C2: 32^3 hexes, p=4, H1 diffusion+mass) in the launch configuration
+    bench.py times: all rows' counts from the pattern closed form, sampled rows vs the oracle."""
+    from paper_2210_12253_b200.lor import LOR
+    m, form = mg.config_mesh("C2")
+    ctx = LOR(m)
+    q = ctx.query("h1")
+    N = 32 * 4
+    assert q["n_local"] == (N + 1) ** 3 and q["nnz"] == (3 * N + 1) ** 3
+    rp, col, val = ctx.assemble("h1", form["alpha"], form["beta"], form["quad"])
+    ctx.sync()
+    rp, col, val = to_host(rp), to_host(col), to_host(val)
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([rng.integers(0, q["n_local"], 3000), [0, q["n_local"] - 1]]))
+    ref = oracle_lib.assemble_rows(m, rows, "h1", "vertex", form["alpha"], form["beta"])
+    compare_rows(rp, col, val, ref, 0, what="C2 sampled")
+    # properties that hold at any size: sorted unique columns, symmetric pattern sample
+    d = np.diff(rp)
+    assert d.min() >= 8 and d.max() == 27
+    assert (np.diff(col.astype(np.int64)).reshape(-1)[np.diff(np.repeat(np.arange(q["n_local"]), d)) == 0] > 0).all()
