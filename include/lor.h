@@ -146,6 +146,13 @@ lor_status lor_set_exchange(lor_ctx ctx, int mode);
 lor_status lor_exchange_copy(lor_ctx dst, lor_ctx src, lor_space space);
 lor_status lor_assemble_finish(lor_ctx ctx, lor_space space, lor_csr *out);
 
+/* Host-only dry run of lor_setup's plan for one rank (no GPU touched): per space s = 0..2,
+ * info[8*s + 0..7] = {valid, n_global, row_begin, n_rows_local, n_records, n_shared_owned,
+ * n_deferred (owned shared entities with remote contributors), n_ghost_elements};
+ * send_counts / recv_counts [3][nranks] = partial-row records exchanged with each peer (NULL ok).
+ * Used by the multi-rank CPU tests (gloo) to check that the ranks' plans agree. */
+lor_status lor_plan_dry_run(const lor_setup_args *args, int64_t *info, int64_t *send_counts, int64_t *recv_counts);
+
 /* Rank 0 creates the NCCL unique id (128 bytes) that the caller broadcasts to all ranks. */
 lor_status lor_nccl_get_unique_id(void *out128);
 

@@ -65,12 +65,31 @@ def _gen_units(plist):
     return units
 
 
-def _compile(src, obj, extra=()):
+def _headers_hash() -> str:
+    h = hashlib.sha256()
+    for name in sorted(os.listdir(CSRC)):
+        if name.endswith((".cuh", ".h")):
+            with open(os.path.join(CSRC, name), "rb") as f:
+                h.update(name.encode() + f.read())
+    with open(os.path.join(ROOT, "include", "lor.h"), "rb") as f:
+        h.update(f.read())
+    h.update(" ".join(FLAGS + ARCH).encode())
+    return h.hexdigest()
+
+
+def _compile(src, obj, hkey, extra=()):
+    with open(src, "rb") as f:
+        key = hashlib.sha256(f.read() + hkey.encode()).hexdigest()[:16]
+    kfile = obj + ".key"
+    if os.path.exists(obj) and os.path.exists(kfile) and open(kfile).read() == key:
+        return obj, False
     cmd = [NVCC] + FLAGS + ARCH + list(extra) + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
-    return obj
+    with open(kfile, "w") as f:
+        f.write(key)
+    return obj, True
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
@@ -90,9 +109,13 @@ def build(force: bool = False, verbose: bool = True) -> str:
     nw = max(1, min(len(jobs), os.cpu_count() or 4))
     if verbose:
         print(f"[lor build] {len(jobs)} translation units on {nw} workers (p in {plist})", flush=True)
+    hkey = _headers_hash()
     with cf.ThreadPoolExecutor(nw) as ex:
-        futs = [ex.submit(_compile, s, o) for s, o in jobs]
-        objs = [f.result() for f in futs]
+        futs = [ex.submit(_compile, s, o, hkey) for s, o in jobs]
+        res = [f.result() for f in futs]
+    objs = [o for o, _ in res]
+    if verbose:
+        print(f"[lor build] recompiled {sum(r for _, r in res)} of {len(res)}", flush=True)
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)

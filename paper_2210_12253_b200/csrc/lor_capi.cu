@@ -260,6 +260,47 @@ lor_status lor_nccl_get_unique_id(void *out128) {
   return LOR_OK;
 }
 
+lor_status lor_plan_dry_run(const lor_setup_args *args, int64_t *info, int64_t *send_counts, int64_t *recv_counts) {
+  if (!args || !info) return LOR_ERR_INVALID_ARGUMENT;
+  const lor_setup_args &A = *args;
+  if (!(A.dim == 2 || A.dim == 3) || A.p < 1 || A.p > 8 || A.n_vert <= 0 || A.n_elem <= 0 || !A.elem_vert ||
+      A.nranks < 1 || A.rank < 0 || A.rank >= A.nranks || (A.nranks > 1 && !A.elem_rank_begin))
+    return LOR_ERR_INVALID_ARGUMENT;
+  HostPlan plan;
+  try {
+    PlanInput in;
+    in.dim = A.dim;
+    in.p = A.p;
+    in.rank = A.rank;
+    in.nranks = A.nranks;
+    in.n_vert = A.n_vert;
+    in.n_elem = A.n_elem;
+    in.elem_vert = A.elem_vert;
+    in.elem_rank_begin = A.elem_rank_begin;
+    plan.build(in);
+  } catch (const std::exception &ex) {
+    fprintf(stderr, "lor_plan_dry_run: %s\n", ex.what());
+    return LOR_ERR_INVALID_ARGUMENT;
+  }
+  for (int s = 0; s < 3; ++s) {
+    const SpacePlan &P = plan.sp[s];
+    int64_t *o = info + 8 * s;
+    o[0] = P.valid;
+    o[1] = P.n_global;
+    o[2] = P.row_begin;
+    o[3] = P.n_local;
+    o[4] = P.n_records;
+    o[5] = (int64_t)P.ose.size();
+    o[6] = (int64_t)P.defer.size();
+    o[7] = (int64_t)plan.ghost.size();
+    for (int q = 0; q < A.nranks; ++q) {
+      if (send_counts) send_counts[s * A.nranks + q] = P.valid ? P.send_count[q] : 0;
+      if (recv_counts) recv_counts[s * A.nranks + q] = P.valid ? P.recv_count[q] : 0;
+    }
+  }
+  return LOR_OK;
+}
+
 lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
   if (!out) return LOR_ERR_INVALID_ARGUMENT;
   *out = nullptr;

@@ -68,6 +68,7 @@ def lib():
         L.lor_set_exchange.argtypes = [C.c_void_p, C.c_int]
         L.lor_exchange_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
         L.lor_assemble_finish.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Csr)]
+        L.lor_plan_dry_run.argtypes = [C.POINTER(_SetupArgs), C.c_void_p, C.c_void_p, C.c_void_p]
         L.lor_update_coordinates.argtypes = [C.c_void_p, C.c_void_p]
         L.lor_last_phase_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int]
         _lib = L
@@ -80,6 +81,28 @@ def nccl_unique_id() -> bytes:
     if rc:
         raise LorError(rc, "ncclGetUniqueId")
     return bytes(buf)
+
+
+def plan_dry_run(mesh, rank=0, nranks=1, elem_rank_begin=None):
+    """Host-only plan of one rank (no GPU): returns (info[3][8], send[3][nranks], recv[3][nranks])."""
+    vert = np.ascontiguousarray(mesh.vert, dtype=np.float64)
+    elem = np.ascontiguousarray(mesh.elem, dtype=np.int64)
+    erb = elem_rank_begin if elem_rank_begin is not None else mesh.elem_rank_begin
+    erb = np.ascontiguousarray(erb if nranks > 1 else [0, elem.shape[0]], dtype=np.int64)
+    a = _SetupArgs()
+    a.dim, a.p = int(mesh.dim), int(mesh.p)
+    a.n_vert, a.vert_xyz = vert.shape[0], vert.ctypes.data
+    a.n_elem, a.elem_vert = elem.shape[0], elem.ctypes.data
+    a.elem_nodes = None
+    a.rank, a.nranks = rank, nranks
+    a.elem_rank_begin = erb.ctypes.data
+    info = np.zeros((3, 8), dtype=np.int64)
+    send = np.zeros((3, nranks), dtype=np.int64)
+    recv = np.zeros((3, nranks), dtype=np.int64)
+    rc = lib().lor_plan_dry_run(C.byref(a), info.ctypes.data, send.ctypes.data, recv.ctypes.data)
+    if rc:
+        raise LorError(rc, "lor_plan_dry_run")
+    return info, send, recv
 
 
 class LOR:
