@@ -153,6 +153,11 @@ lor_status lor_assemble_finish(lor_ctx ctx, lor_space space, lor_csr *out);
  * Used by the multi-rank CPU tests (gloo) to check that the ranks' plans agree. */
 lor_status lor_plan_dry_run(const lor_setup_args *args, int64_t *info, int64_t *send_counts, int64_t *recv_counts);
 
+/* Diagnostics: copy internal setup tables of `space` to host memory (what = 0: row-class slot
+ * table uint32[S][729][W]; 1: block-size table uint8[S][729][3*27 or 27]).  Returns bytes copied
+ * (0 on error / cap too small). */
+int64_t lor_debug_dump(lor_ctx ctx, int what, lor_space space, void *host_out, int64_t cap_bytes);
+
 /* Rank 0 creates the NCCL unique id (128 bytes) that the caller broadcasts to all ranks. */
 lor_status lor_nccl_get_unique_id(void *out128);
 

@@ -21,7 +21,7 @@ __device__ __forceinline__ void report_error(int *err, int code, int64_t e, int 
   }
 }
 
-// length of the class-c segment of the clipped stencil range of column sub-lattice s2 along axis a
+// bounds of the class-c segment of the clipped stencil range of column sub-lattice s2 along axis a
 template <int SP>
 __device__ __forceinline__ void seg_bounds(int p, int s, int s2, int a, int x, int c, int &lo, int &hi) {
   const bool vk = vkind<SP>(s2, a);
@@ -38,6 +38,10 @@ __device__ __forceinline__ void seg_bounds(int p, int s, int s2, int a, int x, i
   else { lo = blo < 1 ? 1 : blo; hi = bhi > p - 1 ? p - 1 : bhi; }
 }
 
+// lattice extent of sub-lattice s along axis a
+template <int SP>
+__host__ __device__ constexpr int ext_of(int p, int s, int a) { return vkind<SP>(s, a) ? p + 1 : p; }
+
 // decode a local dof index (macro-element local order) into (sub-lattice, lattice coords)
 template <int DIM, int SP>
 __device__ __forceinline__ void decode_local(int p, int l, int &s, int x[3]) {
@@ -51,12 +55,11 @@ __device__ __forceinline__ void decode_local(int p, int l, int &s, int x[3]) {
   const int blk = (SP == SP_ND) ? p * (p + 1) * (p + 1) : (p + 1) * p * p;
   s = l / blk;
   int r = l - s * blk;
-  int ext[3];
-  for (int a = 0; a < 3; ++a) ext[a] = vkind<SP>(s, a) ? p + 1 : p;
-  x[0] = r % ext[0];
-  r /= ext[0];
-  x[1] = r % ext[1];
-  x[2] = r / ext[1];
+  const int e0 = ext_of<SP>(p, s, 0), e1 = ext_of<SP>(p, s, 1);
+  x[0] = r % e0;
+  r /= e0;
+  x[1] = r % e1;
+  x[2] = r / e1;
 }
 
 template <int DIM, int SP>
@@ -66,6 +69,20 @@ __device__ __forceinline__ int row_tau(int p, int s, const int x[3]) {
   return t;
 }
 
+// row key: per axis (min(x,2), min(ext-1-x,2)) -> 0..8, combined base 9
+template <int DIM, int SP>
+__device__ __forceinline__ int row_key(int p, int s, const int x[3]) {
+  int k = 0, m = 1;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    const int ext = ext_of<SP>(p, s, a);
+    const int kl = x[a] < 2 ? x[a] : 2, d = ext - 1 - x[a], kh = d < 2 ? d : 2;
+    k += (kl * 3 + kh) * m;
+    m *= 9;
+  }
+  return k;
+}
+
 // join entity of a row (classes cr) and a column (classes cc): fixed where both sit on the same side
 __device__ __forceinline__ int join_cls(int cr, int cc) { return (cr == cc && cr != 1) ? cr : 1; }
 
@@ -73,36 +90,48 @@ __device__ __forceinline__ int join_cls(int cr, int cc) { return (cr == cc && cr
 template <int DIM, int SP, int P, int KZ>
 struct AsmCfg {
   using T_ = Tr<DIM, SP>;
-  static constexpr int S = T_::S, W = T_::W, NENT = T_::NENT, NSLOT = T_::NSLOT;
+  static constexpr int S = T_::S, W = T_::W, NENT = T_::NENT, NSLOT = T_::NSLOT, MAXL = T_::MAXL;
   static constexpr int NB = S * 27;                               // block table entries
   static constexpr int NPTS = ipow_c(P + 1, DIM);                 // lattice points (coords)
-  static constexpr int CPL = DIM == 3 ? P * P : P * P;            // cells per layer (2D: all)
+  static constexpr int NDPE = SP == SP_H1 ? NPTS : (SP == SP_ND ? 3 * P * (P + 1) * (P + 1) : 3 * P * P * (P + 1));
+  static constexpr int CPL = P * P;                               // cells per layer (2D: all)
   static constexpr int NRING = DIM == 3 ? (KZ == P ? P : KZ + 1) : 1;
   static constexpr int NCELL = NRING * CPL;                       // cells resident in smem
-  static constexpr int BATCH = 128;                               // rows per batch (= threads)
+  static constexpr int NW = 4;                                    // warps per CTA
+  static constexpr int RG = 16;                                   // rows per warp group
+  static constexpr int NBP = (NB + 7) / 8 * 8;                    // P0 entries per row (uint16)
   // shared memory layout (bytes)
   static constexpr int OFF_BLK = 0;
-  static constexpr int OFF_BL = OFF_BLK + NB * (int)sizeof(Blk);
-  static constexpr int OFF_X = (OFF_BL + NB + 15) / 16 * 16;
-  static constexpr int OFF_CM = OFF_X + DIM * NPTS * 8;
-  static constexpr int OFF_RG = OFF_CM + NENT * NCELL * 8;                 // row gids [BATCH][W]
-  static constexpr int OFF_RV = OFF_RG + BATCH * W * 4;                    // row vals [BATCH][W]
-  static constexpr int OFF_RM = OFF_RV + BATCH * W * 8;                    // row mults [BATCH][W]
-  static constexpr int OFF_P0 = (OFF_RM + BATCH * W + 15) / 16 * 16;       // P0 [NB][BATCH] int16
-  static constexpr int OFF_META = OFF_P0 + NB * BATCH * 2;                 // per row: out (int64), len, mode
-  static constexpr int SMEM = OFF_META + BATCH * 16;
+  static constexpr int OFF_OS = OFF_BLK + NB * (int)sizeof(Blk);            // ordsig[NB] uint16
+  static constexpr int OFF_BL = OFF_OS + NB * 2;                           // blist[NB] uint8
+  static constexpr int OFF_GM = (OFF_BL + NB + 15) / 16 * 16;              // gmap[NDPE] int32
+  static constexpr int OFF_BS = OFF_GM + NDPE * 4;                         // bsg[NDPE] uint8
+  static constexpr int OFF_X = (OFF_BS + NDPE + 15) / 16 * 16;
+  static constexpr int OFF_CM = (OFF_X + DIM * NPTS * 8 + 15) / 16 * 16;
+  static constexpr int OFF_VB = (OFF_CM + NENT * NCELL * 8 + 15) / 16 * 16;  // per warp: RG rows x W values
+  static constexpr int OFF_RM = (OFF_VB + NW * RG * W * 8 + 15) / 16 * 16;   // per warp: RG row records
+  static constexpr int OFF_P0 = OFF_RM + NW * RG * 32;                     // per warp: RG x P0[NBP] uint16
+  static constexpr int RMS = (MAXL + 7) / 8 * 8;                  // merge-plan row (uint16 entries)
+  static constexpr int TMPB = tab_tzs(NB) + RMS * 2;              // per-row staging of table rows
+  static constexpr int OFF_TMP = (OFF_P0 + NW * RG * NBP * 2 + 15) / 16 * 16;
+  static constexpr int OFF_DL = OFF_TMP + NW * RG * TMPB;                  // dl[S][W] int8 (slot -> local offset)
+  static constexpr int SMEM = (OFF_DL + S * W + 15) / 16 * 16;
 };
 
-struct RowMeta {
-  int64_t out;  // DIRECT: CSR offset; RECORD: scratch entry offset
-  int32_t len;
-  int32_t mode;  // 0 skip, 1 direct, 2 record
+// per-row record kept by the row's thread for the warp-wide emission
+struct __align__(16) RowRec {
+  int64_t out;     // mode 1, 3: CSR offset of the row; mode 2: scratch entry offset of the record
+  int64_t recid;   // mode 3: record id (recd row); mode 2: record length (header)
+  int32_t lb[3];   // local index of the row position in each column sub-lattice's layout
+  uint16_t rk;     // row key
+  uint8_t mode;    // 0 skip, 1 own row, 2 partial-row record (merged at run time), 3 planned shared row
+  uint8_t s;       // sub-lattice
 };
+static_assert(sizeof(RowRec) == 32, "RowRec");
 
 // per-row value accumulation: acc[slot] = sum over cells containing the row of the cell matrix row
 template <int DIM, int SP, int P, int RS, int NC>
-__device__ __forceinline__ void row_values(const double *__restrict__ cm, const int x[3], int lay0, int nring,
-                                           double *acc) {
+__device__ __forceinline__ void row_values(const double *__restrict__ cm, const int x[3], int nring, double *acc) {
   constexpr int W = Tr<DIM, SP>::W;
 #pragma unroll
   for (int j = 0; j < W; ++j) acc[j] = 0.0;
@@ -178,81 +207,6 @@ __device__ __forceinline__ void row_values(const double *__restrict__ cm, const 
   }
 }
 
-// positions, global ids and merge multiplicities of the row's stencil slots -> row buffers
-template <int DIM, int SP, int P, int RS>
-__device__ __forceinline__ int row_emit(const Blk *__restrict__ blk, const uint8_t *__restrict__ blist, int nb,
-                                        const ElemTopo &T, const int x[3], int sig_row, const double *acc,
-                                        int16_t *__restrict__ p0, int32_t *__restrict__ rg, double *__restrict__ rv,
-                                        uint8_t *__restrict__ rm) {
-  using C = Tr<DIM, SP>;
-  constexpr int S = C::S;
-  constexpr int BATCH = 128;
-  // P0 of every block present in the row: prefix of sub-box sizes in ascending block-base order
-  int run = 0;
-  for (int i = 0; i < nb; ++i) {
-    const int b = blist[i];
-    const int s2 = b / 27, t2 = b - 27 * s2;
-    int n = 1;
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) {
-      int lo, hi;
-      seg_bounds<SP>(P, RS, s2, a, x[a], cls_of(t2, a), lo, hi);
-      n *= hi >= lo ? hi - lo + 1 : 0;
-    }
-    p0[b * BATCH] = (int16_t)run;
-    run += n;
-  }
-  int cr[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) cr[a] = (a < DIM) ? coord_cls(vkind<SP>(RS, a), x[a], P) : 1;
-  // slots
-#pragma unroll
-  for (int s2 = 0; s2 < S; ++s2) {
-#pragma unroll
-    for (int dz = (DIM == 3 ? st_lo<SP>(RS, s2, 2) : 0); dz <= (DIM == 3 ? st_hi<SP>(RS, s2, 2) : 0); ++dz)
-#pragma unroll
-      for (int dy = st_lo<SP>(RS, s2, 1); dy <= st_hi<SP>(RS, s2, 1); ++dy)
-#pragma unroll
-        for (int dx = st_lo<SP>(RS, s2, 0); dx <= st_hi<SP>(RS, s2, 0); ++dx) {
-          const int y[3] = {x[0] + dx, x[1] + dy, DIM == 3 ? x[2] + dz : 0};
-          bool in = true;
-#pragma unroll
-          for (int a = 0; a < DIM; ++a) in &= (y[a] >= 0) && (y[a] <= (vkind<SP>(s2, a) ? P : P - 1));
-          if (!in) continue;
-          int cc[3] = {1, 1, 1};
-#pragma unroll
-          for (int a = 0; a < DIM; ++a) cc[a] = coord_cls(vkind<SP>(s2, a), y[a], P);
-          const int t2 = cc[0] + 3 * cc[1] + (DIM == 3 ? 9 * cc[2] : 0);
-          const int b = s2 * 27 + t2;
-          const Blk &B = blk[b];
-          // lexicographic rank inside the sub-box, axes ordered by |stride|
-          int off[3], len[3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            off[a] = 0;
-            len[a] = 1;
-          }
-#pragma unroll
-          for (int a = 0; a < DIM; ++a) {
-            int lo, hi;
-            seg_bounds<SP>(P, RS, s2, a, x[a], cc[a], lo, hi);
-            len[a] = hi - lo + 1;
-            off[a] = B.str[a] >= 0 ? y[a] - lo : hi - y[a];
-          }
-          const int f = B.ord & 3, m = (B.ord >> 2) & 3, sl = (B.ord >> 4) & 3;
-          const int pos = p0[b * BATCH] + off[f] + len[f] * (off[m] + len[m] * off[sl]);
-          const int gid = B.g0 + B.str[0] * y[0] + B.str[1] * y[1] + B.str[2] * y[2];
-          int tj = join_cls(cr[0], cc[0]) + 3 * join_cls(cr[1], cc[1]);
-          if (DIM == 3) tj += 9 * join_cls(cr[2], cc[2]);
-          const int slot = st_slot<DIM, SP>(RS, s2, dx, dy, dz);
-          rg[pos * BATCH] = gid;
-          rv[pos * BATCH] = acc[slot] * (double)(sig_row * B.sigma);
-          rm[pos * BATCH] = T.val[tj];
-        }
-  }
-  return run;
-}
-
 template <int DIM, int SP, int P, int QUAD>
 __device__ __forceinline__ bool compute_cell(const double *__restrict__ X, int cx, int cy, int cz, double alpha,
                                              double beta, double *__restrict__ out, int NC, int ci) {
@@ -300,114 +254,189 @@ __device__ __forceinline__ bool compute_cell(const double *__restrict__ X, int c
   }
 }
 
+// ---------------------------------------------------------------------- shared-row merge
 // CTA-cooperative merge of the partial rows of one owned shared entity into final CSR rows.
-// For row g with contributing elements i = 0..k-1 (element order) each holding a sorted partial
-// list L_i with per-entry multiplicity m (number of lists holding that column), the final
-// position of column v is  sum_i sum_{u in L_i, u < v} 1/m(u)  (exact, integer weights), and its
-// value is the sum over the lists holding v in element order (deterministic).
-static __device__ __noinline__ void finalize_ose(const Ose O, const int32_t *__restrict__ ose_slots, const RecEntry *scratch, int rstride,
-                             int64_t row_begin, const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col,
-                             double *__restrict__ val, unsigned char *smem, int smem_bytes) {
-  const int k = O.k, maxl = rstride;
-  // per list: len, weights prefix (maxl+1), cols, vals
-  const int per_list = 4 + (maxl + 1) * 4 + maxl * 4 + maxl * 8;
-  int rp = smem_bytes / (k * per_list);
+// Row g has k contributing elements (element order); list m = that element's partial row, sorted,
+// made of runs of equal block base (a block = the dofs of one coarse entity in one sub-lattice,
+// a contiguous range of global ids, identical in every element that holds it).  Phase A (one
+// thread per row) merges the k block-run lists by base: union blocks in ascending order, their
+// offsets P0 in the final row and the start of each block in every list holding it.  Phase B (one
+// thread per list entry) writes the final entry for the first list holding its block:
+// position P0(u) + offset in block, value = sum over the lists holding the block in element order
+// (deterministic, no atomics).
+struct FinScratch {
+  int maxl, kmax, nu;  // per-row capacities
+};
+
+static __device__ __noinline__ void finalize_ose(const Ose O, const int32_t *__restrict__ ose_slots, const RecEntry *scratch,
+                                                 int rstride, int maxl, int maxu, int64_t row_begin,
+                                                 const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col,
+                                                 double *__restrict__ val, unsigned char *smem, int smem_bytes) {
+  const int k = O.k;
+  // per row: len[k] int, rec[k] int64 (entry offset), bb[k][maxl] int, uidx[k][maxl] uint8,
+  //          U: nu int, p0u[maxu] int16, first[maxu] uint8, start[maxu][k] int8
+  const int per_row = k * 4 + k * 8 + k * maxl * 4 + k * maxl + 4 + maxu * 3 + maxu * k + 16;
+  int rp = smem_bytes / per_row;
   if (rp > O.nrows) rp = O.nrows;
-  if (rp < 1) rp = 1;  // smem too small is prevented on the host
-  int *s_len = reinterpret_cast<int *>(smem);
-  int *s_w = s_len + rp * k;
-  int *s_col = s_w + rp * k * (maxl + 1);
-  const int ints_before = rp * k * (2 * maxl + 2);  // even: s_val stays 8-byte aligned
-  double *s_val = reinterpret_cast<double *>(s_len + ints_before);
+  if (rp < 1) rp = 1;
+  int64_t *s_rec = reinterpret_cast<int64_t *>(smem);             // [rp][k]
+  int *s_len = reinterpret_cast<int *>(s_rec + rp * k);            // [rp][k]
+  int *s_bb = s_len + rp * k;                                      // [rp][k][maxl]
+  int *s_nu = s_bb + rp * k * maxl;                                // [rp]
+  int16_t *s_p0u = reinterpret_cast<int16_t *>(s_nu + rp);         // [rp][maxu]
+  uint8_t *s_first = reinterpret_cast<uint8_t *>(s_p0u + rp * maxu);  // [rp][maxu]
+  int8_t *s_start = reinterpret_cast<int8_t *>(s_first + rp * maxu);   // [rp][maxu][k]
+  uint8_t *s_uidx = reinterpret_cast<uint8_t *>(s_start + rp * maxu * k);  // [rp][k][maxl]
   for (int r0 = 0; r0 < O.nrows; r0 += rp) {
     const int nr = (O.nrows - r0 < rp) ? O.nrows - r0 : rp;
     const int nl = nr * k;
     for (int li = threadIdx.x; li < nl; li += blockDim.x) {
-      const int row = li / k, slot = li - row * k;
-      const int64_t rec = (int64_t)ose_slots[O.slot_off + slot] + r0 + row;
-      const int meta = __ldcg(&scratch[rec * rstride].meta);
-      s_len[li] = meta >> 8;
+      const int row = li / k, m = li - row * k;
+      const int64_t rec = ((int64_t)ose_slots[O.slot_off + m] + r0 + row) * rstride;
+      s_rec[li] = rec;
+      s_len[li] = __ldcg(&scratch[rec + rstride - 1].col);
     }
     __syncthreads();
     for (int it = threadIdx.x; it < nl * maxl; it += blockDim.x) {
       const int li = it / maxl, e = it - li * maxl;
-      if (e >= s_len[li]) continue;
-      const int row = li / k, slot = li - row * k;
-      const int64_t rec = (int64_t)ose_slots[O.slot_off + slot] + r0 + row;
-      const RecEntry *src = scratch + rec * rstride + e;
-      const int c = __ldcg(&src->col);
-      const int meta = __ldcg(&src->meta);
-      const double v = __ldcg(&src->val);
-      s_col[li * maxl + e] = c;
-      s_val[li * maxl + e] = v;
-      s_w[li * (maxl + 1) + e + 1] = WEIGHT_L / (meta & 255);
+      if (e < s_len[li]) s_bb[it] = __ldcg(&scratch[s_rec[li] + e].bbase);
     }
     __syncthreads();
-    for (int li = threadIdx.x; li < nl; li += blockDim.x) {  // exclusive prefix of weights
-      int *w = s_w + li * (maxl + 1);
-      w[0] = 0;
-      for (int e = 0; e < s_len[li]; ++e) w[e + 1] += w[e];
+    // phase A: k-way merge of block runs (one thread per row)
+    for (int row = threadIdx.x; row < nr; row += blockDim.x) {
+      int ptr[MAX_VALENCE];
+      for (int m = 0; m < k; ++m) ptr[m] = 0;
+      int u = 0, P = 0;
+      while (true) {
+        int minb = 0x7fffffff;
+        for (int m = 0; m < k; ++m) {
+          const int li = row * k + m;
+          if (ptr[m] < s_len[li]) {
+            const int b = s_bb[li * maxl + ptr[m]];
+            minb = b < minb ? b : minb;
+          }
+        }
+        if (minb == 0x7fffffff || u >= maxu) break;
+        int size = 0, first = -1;
+        for (int m = 0; m < k; ++m) {
+          const int li = row * k + m;
+          int8_t st = -1;
+          if (ptr[m] < s_len[li] && s_bb[li * maxl + ptr[m]] == minb) {
+            int e = ptr[m];
+            while (e < s_len[li] && s_bb[li * maxl + e] == minb) {
+              s_uidx[li * maxl + e] = (uint8_t)u;
+              ++e;
+            }
+            size = e - ptr[m];
+            st = (int8_t)ptr[m];
+            if (first < 0) first = m;
+            ptr[m] = e;
+          }
+          s_start[(row * maxu + u) * k + m] = st;
+        }
+        s_p0u[row * maxu + u] = (int16_t)P;
+        s_first[row * maxu + u] = (uint8_t)first;
+        P += size;
+        ++u;
+      }
+      s_nu[row] = u;
     }
     __syncthreads();
+    // phase B: one thread per list entry; the first list holding the block writes
     for (int it = threadIdx.x; it < nl * maxl; it += blockDim.x) {
       const int li = it / maxl, e = it - li * maxl;
       if (e >= s_len[li]) continue;
-      const int row = li / k, slot = li - row * k;
-      const int v = s_col[li * maxl + e];
-      int64_t wsum = 0;
-      bool first = true;
+      const int row = li / k, m = li - row * k;
+      const int u = s_uidx[it];
+      if (s_first[row * maxu + u] != m) continue;
+      const int o = e - s_start[(row * maxu + u) * k + m];
       double sum = 0.0;
-      for (int j = 0; j < k; ++j) {
-        const int lj = row * k + j;
-        if (j == slot) {
-          wsum += s_w[lj * (maxl + 1) + e];
-          sum += s_val[lj * maxl + e];
-          continue;
-        }
-        // lower bound of v in list j
-        int lo = 0, hi = s_len[lj];
-        const int *cj = s_col + lj * maxl;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (cj[mid] < v) lo = mid + 1;
-          else hi = mid;
-        }
-        wsum += s_w[lj * (maxl + 1) + lo];
-        if (lo < s_len[lj] && cj[lo] == v) {
-          if (j < slot) first = false;
-          sum += s_val[lj * maxl + lo];
-        }
+      for (int mm = 0; mm < k; ++mm) {
+        const int st = s_start[(row * maxu + u) * k + mm];
+        if (st >= 0) sum += __ldcg(&scratch[s_rec[row * k + mm] + st + o].val);
       }
-      if (first) {
-        const int64_t out = row_ptr[(int64_t)O.gid_base + r0 + row - row_begin] + wsum / WEIGHT_L;
-        col[out] = v;
-        val[out] = sum;
-      }
+      const int c = __ldcg(&scratch[s_rec[li] + e].col);
+      const int64_t out = row_ptr[(int64_t)O.gid_base + r0 + row - row_begin] + s_p0u[row * maxu + u] + o;
+      col[out] = c;
+      val[out] = sum;
     }
     __syncthreads();
   }
 }
 
+// Warp-wide emission of one row (lanes = stencil slots): each lane places its column at
+// P0(block) + rank inside the block's sub-box (setup table per orientation code of the block's
+// entity), so the row comes out in ascending global column order and the warp's stores cover a
+// contiguous range (coalesced).  P0 per block was prepared by the row's thread (p0r).
+template <int DIM, int SP, int P>
+__device__ __forceinline__ void emit_row(const AsmArgs &A, const RowRec &R, const double *__restrict__ vrow,
+                                         const uint16_t *__restrict__ p0r, const Blk *__restrict__ blk,
+                                         const ElemTopo &T, const int32_t *__restrict__ gmap,
+                                         const uint8_t *__restrict__ bsg, const int8_t *__restrict__ dlt, int lane) {
+  using C = Tr<DIM, SP>;
+  constexpr int W = C::W;
+  const int64_t key = (int64_t)R.s * NROWKEY + R.rk;
+  int32_t *colr = A.col + R.out;
+  double *valr = A.val + R.out;
+#pragma unroll
+  for (int j0 = 0; j0 < W; j0 += 32) {
+    const int j = j0 + lane;
+    if (j < W) {
+      const uint32_t w = __ldg(A.tabs.slot + key * W + j);
+      const int bw = w & 127;
+      if (bw != 127) {
+        const int s2 = (w >> 24) & 3;
+        const int l = R.lb[s2] + dlt[R.s * W + j];
+        const int gid = gmap[l];
+        const int bs = bsg[l];
+        const int b = bs & 127;
+        const int lex = __ldg(A.tabs.lex + ((key * W + j) << 3) + T.orient[b - 27 * s2]);
+        const unsigned pp = p0r[b];
+        const int pos = (int)(pp & 255u) + lex;
+        const double v = (bs & 128) ? -vrow[j] : vrow[j];
+        if (R.mode == 1) {
+          colr[pos] = gid;
+          valr[pos] = v;
+        } else if (R.mode == 3) {
+          colr[pos] = gid;  // identical in every element holding it
+          const unsigned ps = pp >> 8;
+          if (ps == 255u) valr[pos] = v;                 // block held by this element only
+          else A.recd[R.recid * W + ps + lex] = v;       // shared: summed by the last element to arrive
+        } else {
+          double2 *dst = reinterpret_cast<double2 *>(A.scratch) + R.out;
+          dst[pos] = make_double2(__longlong_as_double(((long long)(unsigned)blk[b].base << 32) | (unsigned)gid), v);
+        }
+      }
+    }
+  }
+  if (R.mode == 2 && lane == 0)  // record header: length
+    reinterpret_cast<double2 *>(A.scratch)[R.out + A.rstride - 1] =
+        make_double2(__longlong_as_double((long long)(unsigned)R.recid), 0.0);
+}
+
 template <int DIM, int SP, int P, int QUAD, int KZ>
-__global__ void __launch_bounds__(128) k_assemble(AsmArgs A) {
+__global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
   using CF = AsmCfg<DIM, SP, P, KZ>;
-  constexpr int S = CF::S, W = CF::W, NB = CF::NB, BATCH = CF::BATCH, NC = CF::NCELL;
+  constexpr int S = CF::S, W = CF::W, NB = CF::NB, NC = CF::NCELL;
   extern __shared__ __align__(16) unsigned char smem[];
   Blk *blk = reinterpret_cast<Blk *>(smem + CF::OFF_BLK);
+  uint16_t *ordsig = reinterpret_cast<uint16_t *>(smem + CF::OFF_OS);
   uint8_t *blist = smem + CF::OFF_BL;
+  int32_t *gmap = reinterpret_cast<int32_t *>(smem + CF::OFF_GM);
+  uint8_t *bsg = smem + CF::OFF_BS;
   double *X = reinterpret_cast<double *>(smem + CF::OFF_X);
   double *cm = reinterpret_cast<double *>(smem + CF::OFF_CM);
-  int32_t *rg = reinterpret_cast<int32_t *>(smem + CF::OFF_RG);
-  double *rv = reinterpret_cast<double *>(smem + CF::OFF_RV);
-  uint8_t *rm = smem + CF::OFF_RM;
-  int16_t *p0 = reinterpret_cast<int16_t *>(smem + CF::OFF_P0);
-  RowMeta *meta = reinterpret_cast<RowMeta *>(smem + CF::OFF_META);
   __shared__ ElemTopo T;
   __shared__ ElemSpace E;
   __shared__ int s_nb, s_fin_n, s_bad;
   __shared__ int s_fin[27];
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int RG = CF::RG, NBP = CF::NBP;
+  double *vb = reinterpret_cast<double *>(smem + CF::OFF_VB) + warp * RG * W;
+  RowRec *rr = reinterpret_cast<RowRec *>(smem + CF::OFF_RM) + warp * RG;
+  uint16_t *p0r = reinterpret_cast<uint16_t *>(smem + CF::OFF_P0) + warp * RG * NBP;
+  int8_t *dlt = reinterpret_cast<int8_t *>(smem + CF::OFF_DL);
   const int64_t el = blockIdx.x;  // local element index
   if (el >= A.nel_local) return;
   {
@@ -427,27 +456,58 @@ __global__ void __launch_bounds__(128) k_assemble(AsmArgs A) {
     if (tid == 0) { s_fin_n = 0; s_bad = 0; }
   }
   __syncthreads();
-  // ---- element block table + ascending-base order
+  // ---- element block table, canonical axis order/directions, ascending-base order
   if (tid < NB) {
     const int s = tid / 27, tau = tid - 27 * s;
     Blk B;
-    if (DIM == 2 && tau >= 9) { B.size = 0; B.g0 = 0; B.base = 0; B.sigma = 1; B.ord = 0; B.str[0] = B.str[1] = B.str[2] = 0; }
-    else block_affine<DIM, SP>(P, s, tau, T, A.base, B);
+    if (DIM == 2 && tau >= 9) {
+      B.size = 0; B.g0 = 0; B.base = 0; B.sigma = 1; B.ord = 0; B.str[0] = B.str[1] = B.str[2] = 0;
+    } else {
+      block_affine<DIM, SP>(P, s, tau, T, A.base, B);
+    }
     blk[tid] = B;
+    ordsig[tid] = (uint16_t)(B.ord | ((B.str[0] < 0) << 6) | ((B.str[1] < 0) << 7) | ((B.str[2] < 0) << 8));
   }
   __syncthreads();
-  if (tid < NB) {
-    const Blk &B = blk[tid];
-    if (B.size > 0) {
+  {
+    __shared__ int s_wcnt[4];
+    __shared__ uint8_t s_cl[NB];
+    const bool ne = tid < NB && blk[tid].size > 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, ne);
+    if (lane == 0) s_wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0;
+    for (int w2 = 0; w2 < warp; ++w2) off += s_wcnt[w2];
+    if (ne) s_cl[off + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)tid;
+    if (tid == 0) s_nb = s_wcnt[0] + s_wcnt[1] + s_wcnt[2] + s_wcnt[3];
+    __syncthreads();
+    const int ncomp = s_nb;
+    if (tid < ncomp) {
+      const int b = s_cl[tid];
+      const int mb = blk[b].base;
       int r = 0;
-      for (int b = 0; b < NB; ++b) r += (blk[b].size > 0 && blk[b].base < B.base);
-      blist[r] = (uint8_t)tid;
+      for (int j = 0; j < ncomp; ++j) r += blk[s_cl[j]].base < mb;
+      blist[r] = (uint8_t)b;
     }
   }
-  if (tid == 0) {
-    int n = 0;
-    for (int b = 0; b < NB; ++b) n += blk[b].size > 0;
-    s_nb = n;
+  // ---- slot -> local index offset relative to the row position in the column sub-lattice layout
+  for (int i = tid; i < S * W; i += blockDim.x) {
+    const int s = i / W, j = i - s * W;
+    int jj = j, s2 = 0;
+    while (s2 < S - 1 && jj >= st_n<DIM, SP>(s, s2)) { jj -= st_n<DIM, SP>(s, s2); ++s2; }
+    const int nx = st_hi<SP>(s, s2, 0) - st_lo<SP>(s, s2, 0) + 1, ny = st_hi<SP>(s, s2, 1) - st_lo<SP>(s, s2, 1) + 1;
+    const int dx = st_lo<SP>(s, s2, 0) + jj % nx, dy = st_lo<SP>(s, s2, 1) + (jj / nx) % ny;
+    const int dz = (DIM == 3) ? st_lo<SP>(s, s2, 2) + jj / (nx * ny) : 0;
+    dlt[i] = (int8_t)(dx + ext_of<SP>(P, s2, 0) * (dy + ext_of<SP>(P, s2, 1) * dz));
+  }
+  // ---- element restriction in shared memory: global id and block/sign of every local dof
+  for (int l = tid; l < CF::NDPE; l += blockDim.x) {
+    int s, x[3];
+    decode_local<DIM, SP>(P, l, s, x);
+    const int b = s * 27 + row_tau<DIM, SP>(P, s, x);
+    const Blk &B = blk[b];
+    gmap[l] = B.g0 + B.str[0] * x[0] + B.str[1] * x[1] + B.str[2] * x[2];
+    bsg[l] = (uint8_t)(b | (B.sigma < 0 ? 128 : 0));
   }
   __syncthreads();
   const int nb = s_nb;
@@ -457,8 +517,8 @@ __global__ void __launch_bounds__(128) k_assemble(AsmArgs A) {
   for (int ch = 0; ch < NCHUNK; ++ch) {
     const int k0 = (DIM == 3) ? ch * KZ : 0;
     const int k1 = (DIM == 3) ? ((k0 + KZ < P) ? k0 + KZ : P) : P;
-    // cells of layers [k0, k1)
     const int ncell = (DIM == 3) ? (k1 - k0) * P * P : P * P;
+    if (ch > 0) __syncthreads();  // previous chunk's rows done before its ring slots are reused
     for (int c = tid; c < ncell; c += blockDim.x) {
       const int cx = c % P, cy = (c / P) % P, cz = (DIM == 3) ? k0 + c / (P * P) : 0;
       const int ci = (DIM == 3) ? (((cz % CF::NRING) * P) + cy) * P + cx : cy * P + cx;
@@ -467,114 +527,127 @@ __global__ void __launch_bounds__(128) k_assemble(AsmArgs A) {
     __syncthreads();
     if (s_bad && tid == 0) report_error(A.err, 2, A.elem_begin + el, s_bad - 1);
     // rows of this chunk: per sub-lattice s the z range [k0, kend(s))
-    int nrow_s[S], zlo[S];
-    int nrows = 0;
+    int nrows = 0, nrow_s0 = 0, nrow_s1 = 0;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      const int ex = vkind<SP>(s, 0) ? P + 1 : P, ey = vkind<SP>(s, 1) ? P + 1 : P;
+      const int ex = ext_of<SP>(P, s, 0), ey = ext_of<SP>(P, s, 1);
       int zl = 0, zh = 1;
       if (DIM == 3) {
-        const bool vz = vkind<SP>(s, 2);
         zl = k0;
-        zh = k1 + ((vz && k1 == P) ? 1 : 0);
+        zh = k1 + ((vkind<SP>(s, 2) && k1 == P) ? 1 : 0);
       }
-      zlo[s] = zl;
-      nrow_s[s] = ex * ey * (zh - zl);
-      nrows += nrow_s[s];
+      const int n = ex * ey * (zh - zl);
+      if (s == 0) nrow_s0 = n;
+      if (s == 1) nrow_s1 = n;
+      nrows += n;
     }
-    for (int r0 = 0; r0 < nrows; r0 += BATCH) {
-      const int r = r0 + tid;
-      if (r < nrows) {
-        int s = 0, rr = r;
-        while (rr >= nrow_s[s]) { rr -= nrow_s[s]; ++s; }
-        const int ex = vkind<SP>(s, 0) ? P + 1 : P, ey = vkind<SP>(s, 1) ? P + 1 : P;
-        int x[3];
-        x[0] = rr % ex;
-        x[1] = (rr / ex) % ey;
-        x[2] = (DIM == 3) ? zlo[s] + rr / (ex * ey) : 0;
-        const int tr = row_tau<DIM, SP>(P, s, x);
-        const uint8_t fl = T.flags[tr], sf = E.sflags[tr];
-        RowMeta M;
-        M.len = 0;
-        M.mode = 0;
-        M.out = 0;
-        const bool owned = fl & TF_OWNED;
-        const bool rec = (sf & SF_SHARED) && (owned || (sf & SF_SEND));
-        if (owned || rec) {
-          const Blk &Br = blk[s * 27 + tr];
-          const int gid = Br.g0 + Br.str[0] * x[0] + Br.str[1] * x[1] + Br.str[2] * x[2];
-          double acc[W];
-          int len = 0;
-          const int lay0 = k0;
-          switch (s) {
-            case 0:
-              row_values<DIM, SP, P, 0, NC>(cm, x, lay0, CF::NRING, acc);
-              len = row_emit<DIM, SP, P, 0>(blk, blist, nb, T, x, Br.sigma, acc, p0 + tid, rg + tid, rv + tid, rm + tid);
-              break;
-            case 1:
-              if (S > 1) {
-                row_values<DIM, SP, P, (S > 1 ? 1 : 0), NC>(cm, x, lay0, CF::NRING, acc);
-                len = row_emit<DIM, SP, P, (S > 1 ? 1 : 0)>(blk, blist, nb, T, x, Br.sigma, acc, p0 + tid, rg + tid,
-                                                             rv + tid, rm + tid);
-              }
-              break;
-            default:
-              if (S > 2) {
-                row_values<DIM, SP, P, (S > 2 ? 2 : 0), NC>(cm, x, lay0, CF::NRING, acc);
-                len = row_emit<DIM, SP, P, (S > 2 ? 2 : 0)>(blk, blist, nb, T, x, Br.sigma, acc, p0 + tid, rg + tid,
-                                                             rv + tid, rm + tid);
-              }
-              break;
-          }
-          M.len = len;
-          if (!rec) {
-            M.mode = 1;
-            M.out = A.row_ptr[gid - A.row_begin];
-          } else {
-            M.mode = 2;
-            int type, li;
-            {
+    // groups of RG rows per warp: the row's thread accumulates its values and prepares P0 of its
+    // blocks (all global loads of the row issued here, in parallel across rows), then the warp
+    // emits the rows one at a time, lanes = stencil slots
+    for (int g0 = warp * RG; g0 < nrows; g0 += CF::NW * RG) {
+      const int r = g0 + lane;
+      if (lane < RG) {
+        RowRec R;
+        R.mode = 0;
+        R.out = 0;
+        R.recid = 0;
+        R.rk = 0;
+        R.s = 0;
+        R.lb[0] = R.lb[1] = R.lb[2] = 0;
+        if (r < nrows) {
+          int s = 0, rq = r;
+          if (S > 1 && rq >= nrow_s0) { rq -= nrow_s0; s = 1; if (rq >= nrow_s1) { rq -= nrow_s1; s = 2; } }
+          const int ex = ext_of<SP>(P, s, 0), ey = ext_of<SP>(P, s, 1);
+          int x[3];
+          x[0] = rq % ex;
+          x[1] = (rq / ex) % ey;
+          x[2] = (DIM == 3) ? k0 + rq / (ex * ey) : 0;
+          const int tr = row_tau<DIM, SP>(P, s, x);
+          const uint8_t fl = T.flags[tr], sf = E.sflags[tr];
+          const bool owned = fl & TF_OWNED;
+          const bool shared = sf & SF_SHARED;
+          const bool local_plan = shared && owned && !(sf & SF_DEFER) && !A.plan;  // mode 3
+          const bool rec = shared && (owned || (sf & SF_SEND)) && !local_plan;      // mode 2
+          if ((owned && !A.plan) || rec || local_plan) {
+            R.s = (uint8_t)s;
+            const int rk = row_key<DIM, SP>(P, s, x);
+            R.rk = (uint16_t)rk;
+#pragma unroll
+            for (int s2 = 0; s2 < S; ++s2) {
+              const int OFFS = (SP == SP_H1) ? 0 : s2 * (SP == SP_ND ? P * (P + 1) * (P + 1) : (P + 1) * P * P);
+              R.lb[s2] = OFFS + x[0] + ext_of<SP>(P, s2, 0) * (x[1] + ext_of<SP>(P, s2, 1) * x[2]);
+            }
+            const int lr = R.lb[s];
+            const int gid = gmap[lr];
+            const double sig_row = (bsg[lr] & 128) ? -1.0 : 1.0;
+            int t_in = 0;
+            if (shared) {
               const int c0 = cls_of(tr, 0), c1 = cls_of(tr, 1), c2 = DIM == 3 ? cls_of(tr, 2) : 1;
               const int nI = (c0 == 1) + (c1 == 1) + (DIM == 3 ? (c2 == 1) : 0);
-              type = (nI == 0) ? 0 : (nI == DIM ? 3 : (DIM == 3 ? nI : 1));
-              (void)li;
+              const int type = (nI == 0) ? 0 : (nI == DIM ? 3 : (DIM == 3 ? nI : 1));
+              t_in = gid - A.base[type][T.ent[tr]];
             }
-            const int t_in = gid - A.base[type][T.ent[tr]];
-            M.out = ((int64_t)E.rec[tr] + t_in) * A.rstride;
+            const int64_t recid = shared ? (int64_t)E.rec[tr] + t_in : 0;
+            // P0 of the row's blocks: the row's block-size table row (and for planned shared rows
+            // its merge-plan row) are fetched with 16-byte loads into the (still free) value row
+            constexpr int TZS = tab_tzs(NB);
+            const uint4 *tz4 = reinterpret_cast<const uint4 *>(A.tabs.size + ((int64_t)s * NROWKEY + rk) * TZS);
+            uint4 *tmp4 = reinterpret_cast<uint4 *>(smem + CF::OFF_TMP + (warp * RG + lane) * CF::TMPB);
+            uint8_t *tzs = reinterpret_cast<uint8_t *>(tmp4);
+#pragma unroll
+            for (int q = 0; q < TZS / 16; ++q) tmp4[q] = __ldg(tz4 + q);
+            uint16_t *pr = p0r + lane * NBP;
+            if (local_plan) {
+              R.mode = 3;
+              R.recid = recid;
+              R.out = A.row_ptr[gid - A.row_begin];
+              const uint4 *rm4 = reinterpret_cast<const uint4 *>(A.rmap + recid * A.maxl);
+              uint16_t *rms = reinterpret_cast<uint16_t *>(tmp4 + TZS / 16);
+              for (int q = 0; q < A.maxl / 8; ++q) reinterpret_cast<uint4 *>(rms)[q] = __ldg(rm4 + q);
+              int rn = 0;
+              for (int i = 0; i < nb; ++i) {
+                const int b = blist[i];
+                if (tzs[b]) pr[b] = rms[rn++];
+              }
+            } else {
+              int run = 0;
+              for (int i = 0; i < nb; ++i) {
+                const int b = blist[i];
+                pr[b] = (uint16_t)(run | 0xff00);
+                run += tzs[b];
+              }
+              if (!rec) {
+                R.mode = 1;
+                R.out = A.row_ptr[gid - A.row_begin];
+              } else {
+                R.mode = 2;
+                R.out = recid * A.rstride;
+                R.recid = run;
+              }
+            }
+            double acc[W];
+            switch (s) {
+              case 0: row_values<DIM, SP, P, 0, NC>(cm, x, CF::NRING, acc); break;
+              case 1: if (S > 1) row_values<DIM, SP, P, (S > 1 ? 1 : 0), NC>(cm, x, CF::NRING, acc); break;
+              default: if (S > 2) row_values<DIM, SP, P, (S > 2 ? 2 : 0), NC>(cm, x, CF::NRING, acc); break;
+            }
+#pragma unroll
+            for (int j = 0; j < W; ++j) vb[lane * W + j] = acc[j] * sig_row;
           }
         }
-        meta[tid] = M;
-      } else {
-        RowMeta M;
-        M.len = 0;
-        M.mode = 0;
-        M.out = 0;
-        meta[tid] = M;
+        rr[lane] = R;
       }
-      __syncthreads();
-      // coalesced write-out: consecutive threads -> consecutive entries of consecutive rows
-      for (int it = tid; it < BATCH * W; it += blockDim.x) {
-        const int row = it / W, e = it - row * W;
-        const RowMeta &M = meta[row];
-        if (e >= M.len) continue;
-        const int g = rg[e * BATCH + row];
-        const double v = rv[e * BATCH + row];
-        if (M.mode == 1) {
-          A.col[M.out + e] = g;
-          A.val[M.out + e] = v;
-        } else if (M.mode == 2) {
-          RecEntry R;
-          R.col = g;
-          R.meta = (int)rm[e * BATCH + row] | (M.len << 8);
-          R.val = v;
-          reinterpret_cast<double2 *>(A.scratch)[M.out + e] =
-              make_double2(__longlong_as_double(((long long)(unsigned)R.meta << 32) | (unsigned)R.col), R.val);
-        }
+      __syncwarp();
+      const int nr = (nrows - g0 < RG) ? nrows - g0 : RG;
+      for (int i = 0; i < nr; ++i) {
+        const RowRec &Ri = rr[i];
+        if (Ri.mode) emit_row<DIM, SP, P>(A, Ri, vb + i * W, p0r + i * NBP, blk, T, gmap, bsg, dlt, lane);
       }
-      __syncthreads();
+      __syncwarp();
     }
   }
-  // ---- arrival on shared owned entities; the last element to arrive merges their rows
+  if (A.plan) return;
+  // ---- arrival on shared owned entities; the last element to arrive adds up their shared values
   __threadfence();
   __syncthreads();
   if (tid < CF::NSLOT) {
@@ -582,9 +655,9 @@ __global__ void __launch_bounds__(128) k_assemble(AsmArgs A) {
     const uint8_t sf = E.sflags[tau];
     if ((sf & SF_SHARED) && !(sf & (SF_DEFER | SF_SEND)) && E.ose[tau] >= 0) {
       const int oi = E.ose[tau];
-      const Ose O = A.ose[oi];
+      const int kk = A.ose[oi].k;
       const int old = atomicAdd(A.counters + oi, 1);
-      if (old == O.k - 1) {
+      if (old == kk - 1) {
         A.counters[oi] = 0;
         const int pos = atomicAdd(&s_fin_n, 1);
         s_fin[pos] = oi;
@@ -595,17 +668,47 @@ __global__ void __launch_bounds__(128) k_assemble(AsmArgs A) {
   const int nfin = s_fin_n;
   if (nfin > 0) {
     __threadfence();
-    for (int i = 0; i < nfin; ++i) {
+    // entity info of everything this element finalizes, fetched once: first row-info index,
+    // rows, CSR base id, contributor record bases
+    __shared__ int s_fpre[28], s_frow0[27], s_fgid[27], s_fk[27];
+    __shared__ int s_fslot[27 * MAX_VALENCE];
+    for (int i = tid; i < nfin; i += blockDim.x) {
       const Ose O = A.ose[s_fin[i]];
-      finalize_ose(O, A.ose_slots, A.scratch, A.rstride, A.row_begin, A.row_ptr, A.col, A.val, smem + CF::OFF_CM,
-                   CF::SMEM - CF::OFF_CM);
-      __syncthreads();
+      s_frow0[i] = A.ose_row0[s_fin[i]];
+      s_fgid[i] = O.gid_base;
+      s_fk[i] = O.k;
+      s_fpre[i] = O.nrows * W;
+      for (int m = 0; m < O.k; ++m) s_fslot[i * MAX_VALENCE + m] = A.ose_slots[O.slot_off + m];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int acc2 = 0;
+      for (int i = 0; i < nfin; ++i) { const int n = s_fpre[i]; s_fpre[i] = acc2; acc2 += n; }
+      s_fpre[nfin] = acc2;
+    }
+    __syncthreads();
+    const int total = s_fpre[nfin];
+    int i = 0;
+    for (int it = tid; it < total; it += blockDim.x) {
+      while (it >= s_fpre[i + 1]) ++i;  // items ascend per thread: amortised O(1)
+      const int rem = it - s_fpre[i];
+      const int r = rem / W, sidx = rem - r * W;
+      const int64_t ri = (int64_t)s_frow0[i] + r;
+      const int nsh = A.rinfo_nsh[ri];
+      const int q = A.rinfo_spos[ri * W + sidx];
+      unsigned mask = A.rinfo_mask[ri * W + sidx];
+      if (sidx >= nsh) continue;
+      double sum = 0.0;
+      while (mask) {
+        const int m = __ffs(mask) - 1;
+        mask &= mask - 1;
+        sum += __ldcg(A.recd + ((int64_t)s_fslot[i * MAX_VALENCE + m] + r) * W + sidx);
+      }
+      A.val[A.row_ptr[(int64_t)s_fgid[i] + r - A.row_begin] + q] = sum;
     }
   }
 }
 
-
-// finalize_ose is defined (non-template) in lor_kernels.cu
 template <int DIM, int SP, int P, int KZ>
 cudaError_t launch_asm_p(const AsmArgs &a, int quad, cudaStream_t st, int *smem_out) {
   using CF = AsmCfg<DIM, SP, P, KZ>;

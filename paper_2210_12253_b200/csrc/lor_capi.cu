@@ -76,6 +76,14 @@ struct SpaceDev {
   unsigned int *tile_ctr = nullptr;
   std::vector<int64_t> recv_begin, recv_count, send_begin, send_count;
   int pending_exchange = 0;  // manual exchange mode: assembly waiting for lor_assemble_finish
+  uint32_t *tslot = nullptr, *tpb = nullptr;
+  uint8_t *tsize = nullptr, *tnpb = nullptr, *tlex = nullptr;
+  int W = 0;
+  // setup merge plan of shared rows
+  uint16_t *rmap = nullptr, *rinfo_mask = nullptr;
+  double *recd = nullptr;
+  int32_t *ose_row0 = nullptr;
+  uint8_t *rinfo_nsh = nullptr, *rinfo_spos = nullptr, *is_defer = nullptr;
 };
 
 }  // namespace
@@ -148,6 +156,7 @@ lor_status run_count_scan(lor_ctx c, int s, int64_t *row_ptr) {
   fill_base(S, ca.base);
   ca.row_begin = S.row_begin;
   ca.cnt = S.cnt;
+  ca.tabs = Tabs{S.tslot, S.tsize, S.tpb, S.tnpb, S.tlex};
   CUDA_TRY(c, launch_count(c->dim, s, ca, c->stream));
   c->launches++;
   CUDA_TRY(c, launch_scan(S.cnt, row_ptr, S.n_local, S.scan_status, S.tile_ctr, c->stream));
@@ -185,6 +194,8 @@ lor_status finish(lor_ctx c, int s, lor_csr *out) {
   f.ose_slots = S.ose_slots;
   f.scratch = S.scratch;
   f.rstride = S.rstride;
+  f.maxl = S.maxl;
+  f.maxu = S.W;
   f.row_begin = S.row_begin;
   f.row_ptr = out->row_ptr;
   f.col = out->col;
@@ -217,6 +228,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.X = c->X;
   a.xstride = c->xstride;
   fill_base(S, a.base);
+  a.tabs = Tabs{S.tslot, S.tsize, S.tpb, S.tnpb, S.tlex};
   a.row_begin = S.row_begin;
   a.row_ptr = out->row_ptr;
   a.col = out->col;
@@ -226,6 +238,14 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.ose = S.ose;
   a.ose_slots = S.ose_slots;
   a.counters = S.counters;
+  a.rmap = S.rmap;
+  a.recd = S.recd;
+  a.ose_row0 = S.ose_row0;
+  a.rinfo_nsh = S.rinfo_nsh;
+  a.rinfo_spos = S.rinfo_spos;
+  a.rinfo_mask = S.rinfo_mask;
+  a.maxl = (S.maxl + 7) / 8 * 8;
+  a.plan = 0;
   a.alpha = alpha;
   a.beta = beta;
   a.err = c->err;
@@ -370,7 +390,18 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     if (!P.valid) continue;
     S.ndpe = P.ndpe;
     S.maxl = P.maxl;
-    S.rstride = (P.maxl * 16 + 127) / 128 * 8;  // records padded to whole 128-byte lines
+    S.rstride = ((P.maxl + 1) * 16 + 127) / 128 * 8;  // entries + header, padded to whole 128-byte lines
+    S.W = (A.dim == 2) ? 9 : (s == SP_H1 ? 27 : (s == SP_ND ? 33 : 11));
+    {
+      const int64_t ns = tab_slot_entries(A.dim, s), nz = tab_size_entries(A.dim, s);
+      const int64_t nk = (A.dim == 2 || s == SP_H1) ? 729 : 3 * 729;
+      if (dev_alloc(c, &S.tslot, ns) != cudaSuccess || dev_alloc(c, &S.tsize, nz) != cudaSuccess ||
+          dev_alloc(c, &S.tpb, nz) != cudaSuccess || dev_alloc(c, &S.tnpb, nk) != cudaSuccess ||
+          dev_alloc(c, &S.tlex, ns * 8) != cudaSuccess)
+        return bail(LOR_ERR_OUT_OF_MEMORY, "tables");
+      if (launch_build_tables(A.dim, s, A.p, S.tslot, S.tsize, S.tpb, S.tnpb, S.tlex, c->stream) != cudaSuccess)
+        return bail(LOR_ERR_CUDA, "tables");
+    }
     S.n_global = P.n_global;
     S.row_begin = P.row_begin;
     S.n_local = P.n_local;
@@ -428,6 +459,66 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     }
     cudaFree(rp);
     S.nnz_local = nnz;
+  }
+  // setup merge plan of shared rows (topological): plan-mode assembly writes every shared row's
+  // partial-row records, then one merge per owned shared entity records where each block lands
+  for (int s = 0; s < 3; ++s) {
+    SpaceDev &S = c->sp[s];
+    if (!S.valid || S.n_ose == 0) continue;
+    const SpacePlan &P = plan.sp[s];
+    std::vector<int32_t> row0(P.ose.size());
+    std::vector<uint8_t> isdef(P.ose.size(), 0);
+    int64_t nri = 0;
+    for (size_t i = 0; i < P.ose.size(); ++i) { row0[i] = (int32_t)nri; nri += P.ose[i].nrows; }
+    for (int32_t d : P.defer) isdef[d] = 1;
+    if (dev_upload(c, &S.ose_row0, row0.data(), row0.size()) != cudaSuccess ||
+        dev_upload(c, &S.is_defer, isdef.data(), isdef.size()) != cudaSuccess ||
+        dev_alloc(c, &S.rinfo_nsh, (size_t)nri) != cudaSuccess ||
+        dev_alloc(c, &S.rinfo_spos, (size_t)nri * S.W) != cudaSuccess ||
+        dev_alloc(c, &S.rinfo_mask, (size_t)nri * S.W) != cudaSuccess ||
+        dev_alloc(c, &S.rmap, (size_t)S.n_records * ((S.maxl + 7) / 8 * 8)) != cudaSuccess ||
+        dev_alloc(c, &S.recd, (size_t)S.n_records * S.W) != cudaSuccess)
+      return bail(LOR_ERR_OUT_OF_MEMORY, "plan");
+    AsmArgs a{};
+    a.nel_local = c->nel_local;
+    a.elem_begin = c->elem_begin;
+    a.topo = c->topo;
+    a.esp = S.esp;
+    a.X = c->X;
+    a.xstride = c->xstride;
+    fill_base(S, a.base);
+    a.tabs = Tabs{S.tslot, S.tsize, S.tpb, S.tnpb, S.tlex};
+    a.row_begin = S.row_begin;
+    a.scratch = S.scratch;
+    a.rstride = S.rstride;
+    a.ose = S.ose;
+    a.ose_slots = S.ose_slots;
+    a.counters = S.counters;
+    a.maxl = (S.maxl + 7) / 8 * 8;
+    a.plan = 1;
+    a.alpha = 1.0;
+    a.beta = 1.0;
+    a.err = c->err;
+    if (launch_assemble(A.dim, s, A.p, 0, a, c->stream, nullptr) != cudaSuccess) return bail(LOR_ERR_CUDA, "plan asm");
+    PlanArgs pa;
+    pa.n = S.n_ose;
+    pa.ose = S.ose;
+    pa.ose_slots = S.ose_slots;
+    pa.is_defer = S.is_defer;
+    pa.scratch = S.scratch;
+    pa.rstride = S.rstride;
+    pa.maxl = (S.maxl + 7) / 8 * 8;
+    pa.W = S.W;
+    pa.rmap = S.rmap;
+    pa.ose_row0 = S.ose_row0;
+    pa.rinfo_nsh = S.rinfo_nsh;
+    pa.rinfo_spos = S.rinfo_spos;
+    pa.rinfo_mask = S.rinfo_mask;
+    if (launch_plan_merge(pa, S.n_ose, c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "plan merge");
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "plan sync");
+    int herr[4] = {0, 0, 0, 0};
+    cudaMemcpy(herr, c->err, sizeof(herr), cudaMemcpyDeviceToHost);
+    if (herr[0]) { cudaMemset(c->err, 0, sizeof(herr)); }  // geometry errors are reported by assembly calls
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(LOR_ERR_CUDA, "setup sync");
   *out = c;
@@ -610,6 +701,21 @@ lor_status lor_query_elements(lor_ctx c, int64_t *elem_begin, int64_t *n_elem_lo
 }
 
 int64_t lor_kernel_launches(lor_ctx c) { return c ? c->launches : 0; }
+
+int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int64_t cap) {
+  if (!c || space < 0 || space > 2 || !host_out || !c->sp[space].valid) return 0;
+  const SpaceDev &S = c->sp[space];
+  int64_t bytes = 0;
+  const void *src = nullptr;
+  if (what == 0) { bytes = tab_slot_entries(c->dim, space) * 4; src = S.tslot; }
+  else if (what == 1) { bytes = tab_size_entries(c->dim, space); src = S.tsize; }
+  else return 0;
+  if (bytes > cap) return 0;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (cudaMemcpy(host_out, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return bytes;
+}
 
 int lor_last_phase_ms(lor_ctx c, float *ms, int cap) {
   if (!c || !ms) return 0;

@@ -62,10 +62,11 @@ struct __align__(16) Ose {
   int32_t slot_off;   // offset into ose_slots (record base of each slot, element order)
 };
 
-// scratch record entry
+// scratch record entry.  A record = one element's partial row of a shared row: entries sorted by
+// column; the last entry of the record (index rstride-1) is the header {col = len}.
 struct __align__(16) RecEntry {
   int32_t col;
-  int32_t meta;  // mult | (len << 8)
+  int32_t bbase;  // base gid of the column's block: equal bases = same block in every element
   double val;
 };
 

@@ -27,13 +27,131 @@
 
 namespace lorb {
 
+// ================================================================================ tables
+// k_build_tables: one CTA per (sub-lattice s, row key rk).  Uses the same geometric helpers as the
+// reference-checked v1 kernels (seg_bounds / coord_cls / join_cls) on a representative row.
+template <int DIM, int SP>
+__global__ void k_build_tables(int p, uint32_t *tslot, uint8_t *tsize, uint32_t *tpb, uint8_t *tnpb, uint8_t *tlex) {
+  using C = Tr<DIM, SP>;
+  constexpr int S = C::S, W = C::W, NB = S * 27;
+  __shared__ int32_t s_zero[1];
+  if (threadIdx.x == 0) s_zero[0] = 0;
+  __syncthreads();
+  const int s = blockIdx.x / NROWKEY, rk = blockIdx.x % NROWKEY;
+  int x[3] = {0, 0, 0};
+  bool valid = true;
+  int kk = rk;
+  for (int a = 0; a < 3; ++a) {
+    const int key = kk % 9;
+    kk /= 9;
+    if (a >= DIM) { valid &= (key == 0); continue; }
+    const int ext = ext_of<SP>(p, s, a);
+    const int kl = key / 3, kh = key % 3;
+    int xa = (kl < 2) ? kl : ((kh < 2) ? ext - 1 - kh : 2);
+    const int dl = xa < 2 ? xa : 2, d = ext - 1 - xa, dh = d < 2 ? d : 2;
+    valid &= (xa >= 0 && xa < ext && dl == kl && dh == kh);
+    x[a] = xa;
+  }
+  uint32_t *ts = tslot + (int64_t)blockIdx.x * W;
+  uint8_t *tz = tsize + (int64_t)blockIdx.x * tab_tzs(NB);
+  uint32_t *tp = tpb + (int64_t)blockIdx.x * NB;
+  int cr[3] = {1, 1, 1};
+  for (int a = 0; a < DIM; ++a) cr[a] = coord_cls(vkind<SP>(s, a), x[a], p);
+  // slots.  Word: bits 0-6 column block b' = s2*27 + tau' (127 = slot outside the element),
+  // 7-11 join slot tau_J, 12-23 per axis a (at 12+4a) offset and length-1 inside the block's
+  // sub-box, 24-25 s2, 26-31 (dx+1) | (dy+1) << 2 | (dz+1) << 4.
+  for (int j = threadIdx.x; j < W; j += blockDim.x) {
+    uint32_t w = 127u;
+    if (valid) {
+      // find (s2, d) of slot j in the natural order
+      int jj = j, s2 = 0;
+      while (s2 < S && jj >= st_n<DIM, SP>(s, s2)) { jj -= st_n<DIM, SP>(s, s2); ++s2; }
+      const int nx = st_hi<SP>(s, s2, 0) - st_lo<SP>(s, s2, 0) + 1, ny = st_hi<SP>(s, s2, 1) - st_lo<SP>(s, s2, 1) + 1;
+      int d[3];
+      d[0] = st_lo<SP>(s, s2, 0) + jj % nx;
+      d[1] = st_lo<SP>(s, s2, 1) + (jj / nx) % ny;
+      d[2] = (DIM == 3) ? st_lo<SP>(s, s2, 2) + jj / (nx * ny) : 0;
+      int y[3] = {x[0] + d[0], x[1] + d[1], x[2] + d[2]};
+      bool in = true;
+      for (int a = 0; a < DIM; ++a) in &= (y[a] >= 0 && y[a] < ext_of<SP>(p, s2, a));
+      w = ((uint32_t)s2 << 24) | ((uint32_t)(d[0] + 1) << 26) | ((uint32_t)(d[1] + 1) << 28) | ((uint32_t)(d[2] + 1) << 30);
+      if (in) {
+        int cc[3] = {0, 0, 0};
+        for (int a = 0; a < DIM; ++a) cc[a] = coord_cls(vkind<SP>(s2, a), y[a], p);
+        const int t2 = cc[0] + 3 * cc[1] + (DIM == 3 ? 9 * cc[2] : 0);
+        int tj = join_cls(cr[0], cc[0]) + 3 * join_cls(cr[1], cc[1]);
+        if (DIM == 3) tj += 9 * join_cls(cr[2], cc[2]);
+        w |= (uint32_t)(s2 * 27 + t2) | ((uint32_t)tj << 7);
+        int off[3] = {0, 0, 0}, len[3] = {1, 1, 1};
+        for (int a = 0; a < DIM; ++a) {
+          int lo, hi;
+          seg_bounds<SP>(p, s, s2, a, x[a], cc[a], lo, hi);
+          w |= (uint32_t)(y[a] - lo) << (12 + 4 * a);
+          w |= (uint32_t)(hi - lo) << (14 + 4 * a);
+          off[a] = y[a] - lo;
+          len[a] = hi - lo + 1;
+        }
+        // lexicographic rank inside the sub-box for each orientation code of the block's entity:
+        // the block's canonical axis order / directions come from block_affine (bases irrelevant)
+        for (int code = 0; code < 8; ++code) {
+          ElemTopo Tz;
+          for (int q = 0; q < 27; ++q) { Tz.ent[q] = 0; Tz.orient[q] = 0; Tz.val[q] = 1; Tz.flags[q] = 0; }
+          Tz.orient[t2] = (uint8_t)code;
+          const int32_t *zb[4] = {s_zero, s_zero, s_zero, s_zero};
+          Blk B;
+          block_affine<DIM, SP>(p, s2, t2, Tz, zb, B);
+          int o2[3];
+          for (int a = 0; a < 3; ++a) o2[a] = (B.str[a] < 0) ? len[a] - 1 - off[a] : off[a];
+          const int f = B.ord & 3, m = (B.ord >> 2) & 3, sl = (B.ord >> 4) & 3;
+          tlex[((int64_t)blockIdx.x * W + j) * 8 + code] = (uint8_t)(o2[f] + len[f] * (o2[m] + len[m] * o2[sl]));
+        }
+      } else {
+        w |= 127u;
+      }
+    }
+    ts[j] = w;
+  }
+  // block sizes and the compact present-block list
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) {
+    int n = 0;
+    if (valid) {
+      const int s2 = b / 27, t2 = b % 27;
+      n = 1;
+      for (int a = 0; a < 3; ++a) {
+        const int c = cls_of(t2, a);
+        if (a >= DIM) { n *= (c == 0) ? 1 : 0; continue; }  // 2D blocks: tau < 9
+        int lo, hi;
+        seg_bounds<SP>(p, s, s2, a, x[a], c, lo, hi);
+        n *= hi >= lo ? hi - lo + 1 : 0;
+      }
+    }
+    tz[b] = (uint8_t)n;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int b = 0; b < NB; ++b) {
+      if (!tz[b]) continue;
+      const int t2 = b % 27;
+      int tj = join_cls(cr[0], cls_of(t2, 0)) + 3 * join_cls(cr[1], cls_of(t2, 1));
+      if (DIM == 3) tj += 9 * join_cls(cr[2], cls_of(t2, 2));
+      tp[n++] = (uint32_t)b | ((uint32_t)tj << 7) | ((uint32_t)tz[b] << 12);
+    }
+    tnpb[blockIdx.x] = (uint8_t)n;
+  }
+}
+
 // ================================================================================ k_count
+// A2 part 1: per (element, local row) the number of columns whose join entity
+// has this element as its minimal element; exclusive rows are stored, shared rows atomically added.
 template <int DIM, int SP>
 __global__ void __launch_bounds__(128) k_count(CountArgs A) {
   constexpr int S = Tr<DIM, SP>::S;
+  constexpr int NB = S * 27;
   const int64_t ei = blockIdx.x;
   if (ei >= A.ntopo) return;
   __shared__ ElemTopo T;
+  __shared__ Blk blk[NB];
   {
     const int4 *src = reinterpret_cast<const int4 *>(A.topo + ei);
     int4 *dst = reinterpret_cast<int4 *>(&T);
@@ -41,45 +159,28 @@ __global__ void __launch_bounds__(128) k_count(CountArgs A) {
   }
   __syncthreads();
   const int p = A.p;
+  for (int b = threadIdx.x; b < NB; b += blockDim.x) {
+    const int s = b / 27, tau = b % 27;
+    if (DIM == 2 && tau >= 9) { blk[b].size = 0; continue; }
+    if (T.flags[tau] & TF_OWNED) block_affine<DIM, SP>(p, s, tau, T, A.base, blk[b]);
+    else blk[b].size = 0;
+  }
+  __syncthreads();
   const int ndpe = A.ndpe;
   for (int l = threadIdx.x; l < ndpe; l += blockDim.x) {
     int s, x[3];
     decode_local<DIM, SP>(p, l, s, x);
     const int tr = row_tau<DIM, SP>(p, s, x);
     if (!(T.flags[tr] & TF_OWNED)) continue;
-    Blk B;
-    block_affine<DIM, SP>(p, s, tr, T, A.base, B);
+    const Blk &B = blk[s * 27 + tr];
     const int gid = B.g0 + B.str[0] * x[0] + B.str[1] * x[1] + B.str[2] * x[2];
-    int cr[3];
-    for (int a = 0; a < 3; ++a) cr[a] = (a < DIM) ? coord_cls(vkind<SP>(s, a), x[a], p) : 1;
+    const int key = s * NROWKEY + row_key<DIM, SP>(p, s, x);
+    const int n = __ldg(A.tabs.npb + key);
+    const uint32_t *pb = A.tabs.pb + (int64_t)key * NB;
     int cnt = 0;
-#pragma unroll
-    for (int s2 = 0; s2 < S; ++s2) {
-      int L[3][3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if (a < DIM) {
-            int lo, hi;
-            seg_bounds<SP>(p, s, s2, a, x[a], c, lo, hi);
-            L[a][c] = hi >= lo ? hi - lo + 1 : 0;
-          } else {
-            L[a][c] = (c == 1) ? 1 : 0;
-          }
-        }
-#pragma unroll
-      for (int cz = 0; cz < 3; ++cz)
-#pragma unroll
-        for (int cy = 0; cy < 3; ++cy)
-#pragma unroll
-          for (int cx = 0; cx < 3; ++cx) {
-            const int n = L[0][cx] * L[1][cy] * L[2][cz];
-            if (n == 0) continue;
-            int tj = join_cls(cr[0], cx) + 3 * join_cls(cr[1], cy);
-            if (DIM == 3) tj += 9 * join_cls(cr[2], cz);
-            if (T.flags[tj] & TF_MIN) cnt += n;
-          }
+    for (int i = 0; i < n; ++i) {
+      const uint32_t w = __ldg(pb + i);
+      if (T.flags[(w >> 7) & 31] & TF_MIN) cnt += (int)(w >> 12);
     }
     int32_t *dst = A.cnt + (gid - A.row_begin);
     if (T.val[tr] <= 1) *dst = cnt;
@@ -178,7 +279,74 @@ __global__ void __launch_bounds__(128) k_finalize_list(FinArgs F) {
   const int i = blockIdx.x;
   if (i >= F.n) return;
   const Ose O = F.ose[F.list[i]];
-  finalize_ose(O, F.ose_slots, F.scratch, F.rstride, F.row_begin, F.row_ptr, F.col, F.val, smem, F.smem_bytes);
+  finalize_ose(O, F.ose_slots, F.scratch, F.rstride, F.maxl, F.maxu, F.row_begin, F.row_ptr, F.col, F.val, smem,
+               F.smem_bytes);
+}
+
+// ================================================================================ setup merge plan
+// One CTA per owned shared entity whose contributors are all local; one thread per row.  Reads the
+// partial-row records written by k_assemble in plan mode (sorted entries tagged with their block
+// base), merges the block runs of the k contributors by base (the final row order) and records,
+// for every run of every contributor, its offset in the final row and -- if the block is held by
+// two or more contributors -- in the row's list of shared values, plus per row the final position
+// and contributor mask of every shared value.  Topological: computed once in lor_setup.
+__global__ void k_plan_merge(PlanArgs A) {
+  const int oi = blockIdx.x;
+  if (oi >= A.n || A.is_defer[oi]) return;
+  const Ose O = A.ose[oi];
+  const int k = O.k;
+  for (int r = threadIdx.x; r < O.nrows; r += blockDim.x) {
+    int64_t rid[MAX_VALENCE];
+    int len[MAX_VALENCE], ptr[MAX_VALENCE], run[MAX_VALENCE];
+    for (int m = 0; m < k; ++m) {
+      rid[m] = (int64_t)A.ose_slots[O.slot_off + m] + r;
+      len[m] = A.scratch[rid[m] * A.rstride + A.rstride - 1].col;
+      ptr[m] = 0;
+      run[m] = 0;
+    }
+    const int64_t ri = (int64_t)A.ose_row0[oi] + r;
+    int P = 0, nsh = 0;
+    while (true) {
+      int minb = 0x7fffffff;
+      for (int m = 0; m < k; ++m)
+        if (ptr[m] < len[m]) {
+          const int b = A.scratch[rid[m] * A.rstride + ptr[m]].bbase;
+          minb = b < minb ? b : minb;
+        }
+      if (minb == 0x7fffffff) break;
+      unsigned mask = 0;
+      int size = 0;
+      for (int m = 0; m < k; ++m) {
+        if (ptr[m] >= len[m] || A.scratch[rid[m] * A.rstride + ptr[m]].bbase != minb) continue;
+        int e = ptr[m];
+        while (e < len[m] && A.scratch[rid[m] * A.rstride + e].bbase == minb) ++e;
+        size = e - ptr[m];
+        mask |= 1u << m;
+      }
+      const bool sh = __popc(mask) >= 2;
+      for (int m = 0; m < k; ++m) {
+        if (!(mask & (1u << m))) continue;
+        A.rmap[rid[m] * A.maxl + run[m]] = (uint16_t)(P | ((sh ? nsh : 255) << 8));
+        ++run[m];
+        ptr[m] += size;
+      }
+      if (sh) {
+        for (int o = 0; o < size; ++o) {
+          A.rinfo_spos[ri * A.W + nsh + o] = (uint8_t)(P + o);
+          A.rinfo_mask[ri * A.W + nsh + o] = (uint16_t)mask;
+        }
+        nsh += size;
+      }
+      P += size;
+    }
+    A.rinfo_nsh[ri] = (uint8_t)nsh;
+  }
+}
+
+cudaError_t launch_plan_merge(const PlanArgs &a, int n_ose, cudaStream_t st) {
+  if (n_ose <= 0) return cudaSuccess;
+  k_plan_merge<<<(unsigned)n_ose, 64, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 // ================================================================================ G, C, dof map
@@ -321,6 +489,26 @@ cudaError_t launch_count(int dim, int space, const CountArgs &a, cudaStream_t st
   if (space == SP_H1) return launch_count_t<3, SP_H1>(a, a.ntopo, st);
   if (space == SP_ND) return launch_count_t<3, SP_ND>(a, a.ntopo, st);
   return launch_count_t<3, SP_RT>(a, a.ntopo, st);
+}
+
+int64_t tab_slot_entries(int dim, int space) {
+  if (dim == 2) return (int64_t)1 * NROWKEY * Tr<2, SP_H1>::W;
+  if (space == SP_H1) return (int64_t)1 * NROWKEY * Tr<3, SP_H1>::W;
+  if (space == SP_ND) return (int64_t)3 * NROWKEY * Tr<3, SP_ND>::W;
+  return (int64_t)3 * NROWKEY * Tr<3, SP_RT>::W;
+}
+int64_t tab_size_entries(int dim, int space) {
+  const int S = (dim == 2 || space == SP_H1) ? 1 : 3;
+  return (int64_t)S * NROWKEY * tab_tzs(S * 27);
+}
+
+cudaError_t launch_build_tables(int dim, int space, int p, uint32_t *slot, uint8_t *size, uint32_t *pb, uint8_t *npb,
+                                uint8_t *lex, cudaStream_t st) {
+  if (dim == 2) k_build_tables<2, SP_H1><<<NROWKEY, 64, 0, st>>>(p, slot, size, pb, npb, lex);
+  else if (space == SP_H1) k_build_tables<3, SP_H1><<<NROWKEY, 64, 0, st>>>(p, slot, size, pb, npb, lex);
+  else if (space == SP_ND) k_build_tables<3, SP_ND><<<3 * NROWKEY, 64, 0, st>>>(p, slot, size, pb, npb, lex);
+  else k_build_tables<3, SP_RT><<<3 * NROWKEY, 64, 0, st>>>(p, slot, size, pb, npb, lex);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_scan(const int32_t *cnt, int64_t *row_ptr, int64_t n, unsigned long long *status,

@@ -7,6 +7,26 @@
 
 namespace lorb {
 
+// Row-class tables (built once at setup by k_build_tables): a row's stencil
+// structure depends only on its sub-lattice s and, per axis, on (min(x,2), min(ext-1-x,2)) -- the
+// "row key" rk in [0, 729).  Per (s, rk):
+//   slot[W]  : bit 0 valid | bits 1-7 column block b' = s'*27 + tau' | bits 8-12 join slot tau_J |
+//              bits 13+4a.. : offset (2 bits) and length-1 (2 bits) of the column inside its
+//              block's sub-box along axis a (for the lexicographic rank inside the sub-box)
+//   size[NB] : size of the sub-box of block b' in the row's stencil (0 if absent)
+//   pb[NB], npb : compact list of present blocks: b' | tau_J << 7 | size << 12
+constexpr int NROWKEY = 729;
+// byte stride of a row of the block-size table (16-byte aligned rows for vector loads)
+__host__ __device__ constexpr int tab_tzs(int nb) { return (nb + 15) / 16 * 16; }
+struct Tabs {
+  const uint32_t *slot;
+  const uint8_t *size;
+  const uint32_t *pb;
+  const uint8_t *npb;
+  const uint8_t *lex;   // [S][729][W][8]: rank of the slot's column inside its block's sub-box, per
+                        // orientation code (ElemTopo::orient) of the column block's entity
+};
+
 struct CountArgs {
   int p, ndpe;
   int64_t ntopo;                 // local + ghost elements
@@ -14,6 +34,7 @@ struct CountArgs {
   const int32_t *base[4];        // entity first-dof ids (vertex, edge, face, interior)
   int64_t row_begin;
   int32_t *cnt;                  // [n_local] zero-initialised
+  Tabs tabs;
 };
 
 struct AsmArgs {
@@ -23,6 +44,7 @@ struct AsmArgs {
   const double *X;               // local E-vector, element stride xstride doubles
   int64_t xstride;
   const int32_t *base[4];
+  Tabs tabs;
   int64_t row_begin;
   const int64_t *row_ptr;
   int32_t *col;
@@ -32,8 +54,31 @@ struct AsmArgs {
   const Ose *ose;
   const int32_t *ose_slots;
   int32_t *counters;
+  // setup-time merge plan of shared rows whose contributors are all local
+  const uint16_t *rmap;          // [n_records][maxl]: per block run of the record: P0u | P0s << 8 (255 = exclusive);
+                                 // row stride maxl is a multiple of 8 (16-byte rows)
+  double *recd;                  // [n_records][W] compact shared values
+  const int32_t *ose_row0;       // [n_ose] first row-info index of the OSE
+  const uint8_t *rinfo_nsh;      // [n_rowinfo] number of shared positions of the row
+  const uint8_t *rinfo_spos;     // [n_rowinfo][W] final positions of the shared entries
+  const uint16_t *rinfo_mask;    // [n_rowinfo][W] contributor bit mask of each shared entry
+  int maxl;
+  int plan;                      // 1: setup plan pass (write records of every shared row, no CSR output)
   double alpha, beta;
   int *err;                      // [0] code, [1] element, [2] cell
+};
+
+struct PlanArgs {
+  int n;                         // number of local OSEs (not deferred)
+  const Ose *ose;
+  const int32_t *ose_slots;
+  const uint8_t *is_defer;       // [n_ose]
+  const RecEntry *scratch;
+  int rstride, maxl, W;
+  uint16_t *rmap;
+  const int32_t *ose_row0;
+  uint8_t *rinfo_nsh, *rinfo_spos;
+  uint16_t *rinfo_mask;
 };
 
 struct FinArgs {
@@ -42,7 +87,7 @@ struct FinArgs {
   const Ose *ose;
   const int32_t *ose_slots;
   const RecEntry *scratch;
-  int rstride;
+  int rstride, maxl, maxu;
   int64_t row_begin;
   const int64_t *row_ptr;
   int32_t *col;
@@ -71,12 +116,18 @@ struct DofmapArgs {
 };
 
 cudaError_t launch_count(int dim, int space, const CountArgs &a, cudaStream_t st);
+// table sizes (entries) and builder
+int64_t tab_slot_entries(int dim, int space);
+int64_t tab_size_entries(int dim, int space);
+cudaError_t launch_build_tables(int dim, int space, int p, uint32_t *slot, uint8_t *size, uint32_t *pb, uint8_t *npb,
+                                uint8_t *lex, cudaStream_t st);
 cudaError_t launch_scan(const int32_t *cnt, int64_t *row_ptr, int64_t n, unsigned long long *status,
                         unsigned int *tile_ctr, cudaStream_t st);
 int64_t scan_status_words(int64_t n);
 // smem_out != NULL: only report the dynamic shared memory the kernel needs
 cudaError_t launch_assemble(int dim, int space, int p, int quad, const AsmArgs &a, cudaStream_t st, int *smem_out);
 cudaError_t launch_finalize_list(const FinArgs &f, cudaStream_t st);
+cudaError_t launch_plan_merge(const PlanArgs &a, int n_ose, cudaStream_t st);
 cudaError_t launch_discrete(int which, const DiscArgs &a, cudaStream_t st);
 cudaError_t launch_rowptr_stride(int64_t *row_ptr, int64_t n, int w, cudaStream_t st);
 cudaError_t launch_dofmap(int dim, int space, const DofmapArgs &a, cudaStream_t st);

@@ -69,6 +69,8 @@ def lib():
         L.lor_exchange_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
         L.lor_assemble_finish.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Csr)]
         L.lor_plan_dry_run.argtypes = [C.POINTER(_SetupArgs), C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lor_debug_dump.restype = C.c_int64
+        L.lor_debug_dump.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
         L.lor_update_coordinates.argtypes = [C.c_void_p, C.c_void_p]
         L.lor_last_phase_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int]
         _lib = L
@@ -179,6 +181,11 @@ class LOR:
         """X_local: this rank's E-vector slice, a torch tensor (pinned host or device) or numpy array."""
         ptr = X_local.data_ptr() if hasattr(X_local, "data_ptr") else X_local.ctypes.data
         self._check(lib().lor_update_coordinates(self.h, C.c_void_p(ptr)))
+
+    def debug_dump(self, what, space="h1", cap=1 << 26):
+        buf = np.zeros(cap, dtype=np.uint8)
+        n = lib().lor_debug_dump(self.h, what, SPACES.get(space, space), buf.ctypes.data, cap)
+        return buf[:n]
 
     def set_exchange(self, mode: int):
         self._check(lib().lor_set_exchange(self.h, mode))
