@@ -207,6 +207,86 @@ __device__ __forceinline__ void row_values(const double *__restrict__ cm, const 
   }
 }
 
+// H1 (3D, vertex rule): one thread per (cell, corner); the eight corners of a cell are eight
+// consecutive lanes.  Corner q forms its Jacobian from the cell's edge vectors through q, the
+// tensor Q = w a adj adj^T / det and the ten corner contributions of SURVEY C.5; the 36 packed
+// entries of the cell matrix are then assembled with xor-shuffles inside the 8-lane group:
+//   (q,q)       = s^T Q_q s + w b det_q + sum_d Q_{q^d}[d][d]
+//   (q,q^d)     = -s_d (Q_q s)_d - s'_d (Q_{q^d} s')_d
+//   (q^d,q^d')  = s_d s_d' Q_q[d][d'] + (same at corner q^d^d')        (face diagonal)
+//   body diagonal = 0
+template <int P, int NC>
+__device__ __forceinline__ void cells_h1_corner(const double *__restrict__ X, double *__restrict__ cm, int k0, int ncell,
+                                                double alpha, double beta, int &bad) {
+  constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1;
+  constexpr int NRING_ = P;  // only used with KZ == P for H1 (whole element)
+  const int lane = threadIdx.x & 31;
+  const int items = ncell * 8;
+  const int ceil32 = (items + 31) / 32 * 32;
+  for (int it = threadIdx.x; it < ceil32; it += blockDim.x) {
+    const bool act = it < items;
+    const int c = act ? it >> 3 : 0, q = it & 7;
+    const int cx = c % P, cy = (c / P) % P, cz = k0 + c / (P * P);
+    auto pt = [&](int v, int d) -> double {
+      const int l = (cx + (v & 1)) + NP1 * ((cy + ((v >> 1) & 1)) + NP1 * (cz + ((v >> 2) & 1)));
+      return X[d * NPT + l];
+    };
+    double j[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int hi = q | (1 << d), lo = q & ~(1 << d);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) j[d][k] = pt(hi, k) - pt(lo, k);
+    }
+    double r[3][3];
+    cross3(j[1], j[2], r[0]);
+    cross3(j[2], j[0], r[1]);
+    cross3(j[0], j[1], r[2]);
+    const double det = dot3(j[0], r[0]);
+    if (act && !(det > 0.0)) bad = 1 + c;
+    const double sa = 0.125 * alpha / det;
+    double Q[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int e = d; e < 3; ++e) Q[d][e] = Q[e][d] = sa * dot3(r[d], r[e]);
+    double sg[3], Qs[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sg[d] = ((q >> d) & 1) ? 1.0 : -1.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) Qs[d] = Q[d][0] * sg[0] + Q[d][1] * sg[1] + Q[d][2] * sg[2];
+    double diag = sg[0] * Qs[0] + sg[1] * Qs[1] + sg[2] * Qs[2] + 0.125 * beta * det;
+    double edge[3], fdg[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      diag += __shfl_xor_sync(0xffffffffu, Q[d][d], 1 << d);
+      const double e = -sg[d] * Qs[d];
+      edge[d] = e + __shfl_xor_sync(0xffffffffu, e, 1 << d);
+    }
+    // face diagonals (d,d') = (0,1), (0,2), (1,2)
+    {
+      const double f01 = sg[0] * sg[1] * Q[0][1], f02 = sg[0] * sg[2] * Q[0][2], f12 = sg[1] * sg[2] * Q[1][2];
+      fdg[0] = f01 + __shfl_xor_sync(0xffffffffu, f01, 3);
+      fdg[1] = f02 + __shfl_xor_sync(0xffffffffu, f02, 5);
+      fdg[2] = f12 + __shfl_xor_sync(0xffffffffu, f12, 6);
+    }
+    (void)lane;
+    if (act) {
+      const int ci = (((cz % NRING_) * P) + cy) * P + cx;
+      double *o = cm + ci;
+      o[tri(8, q, q) * NC] = diag;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (!((q >> d) & 1)) o[tri(8, q, q ^ (1 << d)) * NC] = edge[d];
+      // face diagonal of (d,d') is written by the lower of its two corners q, q^d^d'
+      if (q < (q ^ 3)) o[tri(8, q ^ 1, q ^ 2) * NC] = fdg[0];
+      if (q < (q ^ 5)) o[tri(8, q ^ 1, q ^ 4) * NC] = fdg[1];
+      if (q < (q ^ 6)) o[tri(8, q ^ 2, q ^ 4) * NC] = fdg[2];
+      if (q < 4) o[tri(8, q, q ^ 7) * NC] = 0.0;
+    }
+  }
+}
+
 template <int DIM, int SP, int P, int QUAD>
 __device__ __forceinline__ bool compute_cell(const double *__restrict__ X, int cx, int cy, int cz, double alpha,
                                              double beta, double *__restrict__ out, int NC, int ci) {
@@ -369,7 +449,8 @@ static __device__ __noinline__ void finalize_ose(const Ose O, const int32_t *__r
 // entity), so the row comes out in ascending global column order and the warp's stores cover a
 // contiguous range (coalesced).  P0 per block was prepared by the row's thread (p0r).
 template <int DIM, int SP, int P>
-__device__ __forceinline__ void emit_row(const AsmArgs &A, const RowRec &R, const double *__restrict__ vrow,
+__device__ __forceinline__ void emit_row(const AsmArgs &A, const RowRec &R, const uint32_t *wpre,
+                                         const double *__restrict__ vrow,
                                          const uint16_t *__restrict__ p0r, const Blk *__restrict__ blk,
                                          const ElemTopo &T, const int32_t *__restrict__ gmap,
                                          const uint8_t *__restrict__ bsg, const int8_t *__restrict__ dlt, int lane) {
@@ -382,7 +463,7 @@ __device__ __forceinline__ void emit_row(const AsmArgs &A, const RowRec &R, cons
   for (int j0 = 0; j0 < W; j0 += 32) {
     const int j = j0 + lane;
     if (j < W) {
-      const uint32_t w = __ldg(A.tabs.slot + key * W + j);
+      const uint32_t w = wpre[j0 / 32];
       const int bw = w & 127;
       if (bw != 127) {
         const int s2 = (w >> 24) & 3;
@@ -519,10 +600,16 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
     const int k1 = (DIM == 3) ? ((k0 + KZ < P) ? k0 + KZ : P) : P;
     const int ncell = (DIM == 3) ? (k1 - k0) * P * P : P * P;
     if (ch > 0) __syncthreads();  // previous chunk's rows done before its ring slots are reused
-    for (int c = tid; c < ncell; c += blockDim.x) {
-      const int cx = c % P, cy = (c / P) % P, cz = (DIM == 3) ? k0 + c / (P * P) : 0;
-      const int ci = (DIM == 3) ? (((cz % CF::NRING) * P) + cy) * P + cx : cy * P + cx;
-      if (!compute_cell<DIM, SP, P, QUAD>(X, cx, cy, cz, A.alpha, A.beta, cm, NC, ci)) s_bad = 1 + cx + P * (cy + P * cz);
+    if (DIM == 3 && SP == SP_H1 && QUAD == 0 && KZ == P) {
+      int bad = 0;
+      cells_h1_corner<P, NC>(X, cm, k0, ncell, A.alpha, A.beta, bad);
+      if (bad) s_bad = bad;
+    } else {
+      for (int c = tid; c < ncell; c += blockDim.x) {
+        const int cx = c % P, cy = (c / P) % P, cz = (DIM == 3) ? k0 + c / (P * P) : 0;
+        const int ci = (DIM == 3) ? (((cz % CF::NRING) * P) + cy) * P + cx : cy * P + cx;
+        if (!compute_cell<DIM, SP, P, QUAD>(X, cx, cy, cz, A.alpha, A.beta, cm, NC, ci)) s_bad = 1 + cx + P * (cy + P * cz);
+      }
     }
     __syncthreads();
     if (s_bad && tid == 0) report_error(A.err, 2, A.elem_begin + el, s_bad - 1);
@@ -639,9 +726,31 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
       }
       __syncwarp();
       const int nr = (nrows - g0 < RG) ? nrows - g0 : RG;
+      // slot words of the next row are fetched while the current row is emitted
+      uint32_t wcur[(W + 31) / 32], wnext[(W + 31) / 32];
+      {
+        const RowRec &R0 = rr[0];
+        const int64_t key0 = (int64_t)R0.s * NROWKEY + R0.rk;
+#pragma unroll
+        for (int h = 0; h < (W + 31) / 32; ++h) {
+          const int j = h * 32 + lane;
+          wcur[h] = (j < W) ? __ldg(A.tabs.slot + key0 * W + j) : 127u;
+        }
+      }
       for (int i = 0; i < nr; ++i) {
+        if (i + 1 < nr) {
+          const RowRec &Rn = rr[i + 1];
+          const int64_t keyn = (int64_t)Rn.s * NROWKEY + Rn.rk;
+#pragma unroll
+          for (int h = 0; h < (W + 31) / 32; ++h) {
+            const int j = h * 32 + lane;
+            wnext[h] = (j < W) ? __ldg(A.tabs.slot + keyn * W + j) : 127u;
+          }
+        }
         const RowRec &Ri = rr[i];
-        if (Ri.mode) emit_row<DIM, SP, P>(A, Ri, vb + i * W, p0r + i * NBP, blk, T, gmap, bsg, dlt, lane);
+        if (Ri.mode) emit_row<DIM, SP, P>(A, Ri, wcur, vb + i * W, p0r + i * NBP, blk, T, gmap, bsg, dlt, lane);
+#pragma unroll
+        for (int h = 0; h < (W + 31) / 32; ++h) wcur[h] = wnext[h];
       }
       __syncwarp();
     }
@@ -669,22 +778,36 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
   if (nfin > 0) {
     __threadfence();
     // entity info of everything this element finalizes, fetched once: first row-info index,
-    // rows, CSR base id, contributor record bases
-    __shared__ int s_fpre[28], s_frow0[27], s_fgid[27], s_fk[27];
+    // contributor record bases and the CSR offset of every row
+    __shared__ int s_fpre[28], s_frow0[27], s_fk[27], s_rpre[28];
     __shared__ int s_fslot[27 * MAX_VALENCE];
+    constexpr int MAXFR = 512;  // finalized rows per element (<= 3 faces (p-1)^2 + 3 edges (p-1) + 1, with margin)
+    int64_t *s_rowoff = reinterpret_cast<int64_t *>(smem + CF::OFF_VB);  // value rows are free now
     for (int i = tid; i < nfin; i += blockDim.x) {
       const Ose O = A.ose[s_fin[i]];
       s_frow0[i] = A.ose_row0[s_fin[i]];
-      s_fgid[i] = O.gid_base;
-      s_fk[i] = O.k;
-      s_fpre[i] = O.nrows * W;
+      s_fk[i] = O.nrows;
       for (int m = 0; m < O.k; ++m) s_fslot[i * MAX_VALENCE + m] = A.ose_slots[O.slot_off + m];
     }
     __syncthreads();
     if (tid == 0) {
-      int acc2 = 0;
-      for (int i = 0; i < nfin; ++i) { const int n = s_fpre[i]; s_fpre[i] = acc2; acc2 += n; }
+      int acc2 = 0, accr = 0;
+      for (int i = 0; i < nfin; ++i) {
+        s_fpre[i] = acc2;
+        s_rpre[i] = accr;
+        acc2 += s_fk[i] * W;
+        accr += s_fk[i];
+      }
       s_fpre[nfin] = acc2;
+      s_rpre[nfin] = accr;
+    }
+    __syncthreads();
+    {
+      int i = 0;
+      for (int rr2 = tid; rr2 < s_rpre[nfin] && rr2 < MAXFR; rr2 += blockDim.x) {
+        while (rr2 >= s_rpre[i + 1]) ++i;
+        s_rowoff[rr2] = A.row_ptr[(int64_t)A.ose[s_fin[i]].gid_base + (rr2 - s_rpre[i]) - A.row_begin];
+      }
     }
     __syncthreads();
     const int total = s_fpre[nfin];
@@ -696,15 +819,19 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
       const int64_t ri = (int64_t)s_frow0[i] + r;
       const int nsh = A.rinfo_nsh[ri];
       const int q = A.rinfo_spos[ri * W + sidx];
-      unsigned mask = A.rinfo_mask[ri * W + sidx];
+      const unsigned mask = A.rinfo_mask[ri * W + sidx];
       if (sidx >= nsh) continue;
+      double part[MAX_VALENCE];
+#pragma unroll
+      for (int m = 0; m < MAX_VALENCE; ++m)
+        part[m] = (mask >> m) & 1u ? __ldcg(A.recd + ((int64_t)s_fslot[i * MAX_VALENCE + m] + r) * W + sidx) : 0.0;
       double sum = 0.0;
-      while (mask) {
-        const int m = __ffs(mask) - 1;
-        mask &= mask - 1;
-        sum += __ldcg(A.recd + ((int64_t)s_fslot[i * MAX_VALENCE + m] + r) * W + sidx);
-      }
-      A.val[A.row_ptr[(int64_t)s_fgid[i] + r - A.row_begin] + q] = sum;
+#pragma unroll
+      for (int m = 0; m < MAX_VALENCE; ++m)
+        if ((mask >> m) & 1u) sum += part[m];
+      const int rg2 = s_rpre[i] + r;
+      const int64_t ro = rg2 < MAXFR ? s_rowoff[rg2] : A.row_ptr[(int64_t)A.ose[s_fin[i]].gid_base + r - A.row_begin];
+      A.val[ro + q] = sum;
     }
   }
 }
