@@ -121,10 +121,10 @@ struct AsmCfg {
 // per-row record kept by the row's thread for the warp-wide emission
 struct __align__(16) RowRec {
   int64_t out;     // mode 1, 3: CSR offset of the row; mode 2: scratch entry offset of the record
-  int64_t recid;   // mode 3: record id (recd row); mode 2: record length (header)
+  int64_t recid;   // mode 4: natural record row; mode 2: record length (header)
   int32_t lb[3];   // local index of the row position in each column sub-lattice's layout
   uint16_t rk;     // row key
-  uint8_t mode;    // 0 skip, 1 own row, 2 partial-row record (merged at run time), 3 planned shared row
+  uint8_t mode;    // 0 skip, 1 own row, 2 partial-row record (sorted, merged at run time), 4 natural-order partial row
   uint8_t s;       // sub-lattice
 };
 static_assert(sizeof(RowRec) == 32, "RowRec");
@@ -471,28 +471,28 @@ __device__ __forceinline__ void emit_row(const AsmArgs &A, const RowRec &R, cons
         const int gid = gmap[l];
         const int bs = bsg[l];
         const int b = bs & 127;
-        const int lex = __ldg(A.tabs.lex + ((key * W + j) << 3) + T.orient[b - 27 * s2]);
-        const unsigned pp = p0r[b];
-        const int pos = (int)(pp & 255u) + lex;
-        const double v = (bs & 128) ? -vrow[j] : vrow[j];
-        if (R.mode == 1) {
-          colr[pos] = gid;
-          valr[pos] = v;
-        } else if (R.mode == 3) {
-          colr[pos] = gid;  // identical in every element holding it
-          const unsigned ps = pp >> 8;
-          if (ps == 255u) valr[pos] = v;                 // block held by this element only
-          else A.recd[R.recid * W + ps + lex] = v;       // shared: summed by the last element to arrive
+        if (R.mode == 4) {  // natural-order partial row: no position work
+          A.nval[R.recid * W + j] = (bs & 128) ? -vrow[j] : vrow[j];
+          A.ngid[R.recid * W + j] = gid;
         } else {
-          double2 *dst = reinterpret_cast<double2 *>(A.scratch) + R.out;
-          dst[pos] = make_double2(__longlong_as_double(((long long)(unsigned)blk[b].base << 32) | (unsigned)gid), v);
+          const int lex = __ldg(A.tabs.lex + ((key * W + j) << 3) + T.orient[b - 27 * s2]);
+          const int pos = (int)(p0r[b] & 255u) + lex;
+          const double v = (bs & 128) ? -vrow[j] : vrow[j];
+          if (R.mode == 1) {
+            colr[pos] = gid;
+            valr[pos] = v;
+          } else {
+            double2 *dst = reinterpret_cast<double2 *>(A.scratch) + R.out;
+            dst[pos] = make_double2(__longlong_as_double(((long long)(unsigned)blk[b].base << 32) | (unsigned)gid),
+                                    A.plan_mode ? (double)j : v);
+          }
         }
       }
     }
   }
-  if (R.mode == 2 && lane == 0)  // record header: length
-    reinterpret_cast<double2 *>(A.scratch)[R.out + A.rstride - 1] =
-        make_double2(__longlong_as_double((long long)(unsigned)R.recid), 0.0);
+  if (R.mode == 2 && lane == 0)  // record header: length, local row
+    reinterpret_cast<double2 *>(A.scratch)[R.out + A.rstride - 1] = make_double2(
+        __longlong_as_double(((long long)(unsigned)R.lb[R.s] << 32) | (long long)(unsigned)R.recid), 0.0);
 }
 
 template <int DIM, int SP, int P, int QUAD, int KZ>
@@ -653,9 +653,9 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
           const uint8_t fl = T.flags[tr], sf = E.sflags[tr];
           const bool owned = fl & TF_OWNED;
           const bool shared = sf & SF_SHARED;
-          const bool local_plan = shared && owned && !(sf & SF_DEFER) && !A.plan;  // mode 3
+          const bool local_plan = shared && owned && !(sf & SF_DEFER) && !A.plan_mode;  // mode 3
           const bool rec = shared && (owned || (sf & SF_SEND)) && !local_plan;      // mode 2
-          if ((owned && !A.plan) || rec || local_plan) {
+          if ((owned && !A.plan_mode) || rec || local_plan) {
             R.s = (uint8_t)s;
             const int rk = row_key<DIM, SP>(P, s, x);
             R.rk = (uint16_t)rk;
@@ -677,26 +677,17 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
             const int64_t recid = shared ? (int64_t)E.rec[tr] + t_in : 0;
             // P0 of the row's blocks: the row's block-size table row (and for planned shared rows
             // its merge-plan row) are fetched with 16-byte loads into the (still free) value row
-            constexpr int TZS = tab_tzs(NB);
-            const uint4 *tz4 = reinterpret_cast<const uint4 *>(A.tabs.size + ((int64_t)s * NROWKEY + rk) * TZS);
-            uint4 *tmp4 = reinterpret_cast<uint4 *>(smem + CF::OFF_TMP + (warp * RG + lane) * CF::TMPB);
-            uint8_t *tzs = reinterpret_cast<uint8_t *>(tmp4);
-#pragma unroll
-            for (int q = 0; q < TZS / 16; ++q) tmp4[q] = __ldg(tz4 + q);
             uint16_t *pr = p0r + lane * NBP;
             if (local_plan) {
-              R.mode = 3;
-              R.recid = recid;
-              R.out = A.row_ptr[gid - A.row_begin];
-              const uint4 *rm4 = reinterpret_cast<const uint4 *>(A.rmap + recid * A.maxl);
-              uint16_t *rms = reinterpret_cast<uint16_t *>(tmp4 + TZS / 16);
-              for (int q = 0; q < A.maxl / 8; ++q) reinterpret_cast<uint4 *>(rms)[q] = __ldg(rm4 + q);
-              int rn = 0;
-              for (int i = 0; i < nb; ++i) {
-                const int b = blist[i];
-                if (tzs[b]) pr[b] = rms[rn++];
-              }
+              R.mode = 4;
+              R.recid = el * CF::NDPE + lr;
             } else {
+              constexpr int TZS = tab_tzs(NB);
+              const uint4 *tz4 = reinterpret_cast<const uint4 *>(A.tabs.size + ((int64_t)s * NROWKEY + rk) * TZS);
+              uint4 *tmp4 = reinterpret_cast<uint4 *>(smem + CF::OFF_TMP + (warp * RG + lane) * CF::TMPB);
+              const uint8_t *tzs = reinterpret_cast<const uint8_t *>(tmp4);
+#pragma unroll
+              for (int q = 0; q < TZS / 16; ++q) tmp4[q] = __ldg(tz4 + q);
               int run = 0;
               for (int i = 0; i < nb; ++i) {
                 const int b = blist[i];
@@ -755,7 +746,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
       __syncwarp();
     }
   }
-  if (A.plan) return;
+  if (A.plan_mode) return;
   // ---- arrival on shared owned entities; the last element to arrive adds up their shared values
   __threadfence();
   __syncthreads();
@@ -777,36 +768,41 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
   const int nfin = s_fin_n;
   if (nfin > 0) {
     __threadfence();
-    // entity info of everything this element finalizes, fetched once: first row-info index,
-    // contributor record bases and the CSR offset of every row
-    __shared__ int s_fpre[28], s_frow0[27], s_fk[27], s_rpre[28];
-    __shared__ int s_fslot[27 * MAX_VALENCE];
-    constexpr int MAXFR = 512;  // finalized rows per element (<= 3 faces (p-1)^2 + 3 edges (p-1) + 1, with margin)
+    // Emit every row of the entities whose last contributor is this element: final position q of
+    // row r takes its column from the first contributor holding it and its value from the sum over
+    // all contributors holding it, in element order (setup merge plan: contributor m's stencil slot
+    // at q, or 255).
+    __shared__ int s_fk[27], s_fnr[27], s_fpre[28];
+    __shared__ int64_t s_fpb[27];
+    __shared__ int s_felem[27 * MAX_VALENCE];
+    constexpr int MAXFR = 256;  // rows whose offsets are staged (value rows hold >= 256 * 12 B)
     int64_t *s_rowoff = reinterpret_cast<int64_t *>(smem + CF::OFF_VB);  // value rows are free now
+    int *s_rowlen = reinterpret_cast<int *>(s_rowoff + MAXFR);
+    __shared__ int s_rpre[28];
     for (int i = tid; i < nfin; i += blockDim.x) {
       const Ose O = A.ose[s_fin[i]];
-      s_frow0[i] = A.ose_row0[s_fin[i]];
-      s_fk[i] = O.nrows;
-      for (int m = 0; m < O.k; ++m) s_fslot[i * MAX_VALENCE + m] = A.ose_slots[O.slot_off + m];
+      s_fk[i] = O.k;
+      s_fnr[i] = O.nrows;
+      s_fpb[i] = A.pbase[s_fin[i]];
+      for (int m = 0; m < O.k; ++m) s_felem[i * MAX_VALENCE + m] = A.ose_elem[O.slot_off + m];
     }
     __syncthreads();
     if (tid == 0) {
-      int acc2 = 0, accr = 0;
-      for (int i = 0; i < nfin; ++i) {
-        s_fpre[i] = acc2;
-        s_rpre[i] = accr;
-        acc2 += s_fk[i] * W;
-        accr += s_fk[i];
-      }
-      s_fpre[nfin] = acc2;
+      int accr = 0;
+      for (int i = 0; i < nfin; ++i) { s_rpre[i] = accr; s_fpre[i] = accr * W; accr += s_fnr[i]; }
       s_rpre[nfin] = accr;
+      s_fpre[nfin] = accr * W;
     }
     __syncthreads();
+    const int nfr = s_rpre[nfin];
     {
       int i = 0;
-      for (int rr2 = tid; rr2 < s_rpre[nfin] && rr2 < MAXFR; rr2 += blockDim.x) {
+      for (int rr2 = tid; rr2 < nfr && rr2 < MAXFR; rr2 += blockDim.x) {
         while (rr2 >= s_rpre[i + 1]) ++i;
-        s_rowoff[rr2] = A.row_ptr[(int64_t)A.ose[s_fin[i]].gid_base + (rr2 - s_rpre[i]) - A.row_begin];
+        const int64_t g = (int64_t)A.ose[s_fin[i]].gid_base + (rr2 - s_rpre[i]) - A.row_begin;
+        const int64_t a = A.row_ptr[g];
+        s_rowoff[rr2] = a;
+        s_rowlen[rr2] = (int)(A.row_ptr[g + 1] - a);
       }
     }
     __syncthreads();
@@ -815,22 +811,33 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
     for (int it = tid; it < total; it += blockDim.x) {
       while (it >= s_fpre[i + 1]) ++i;  // items ascend per thread: amortised O(1)
       const int rem = it - s_fpre[i];
-      const int r = rem / W, sidx = rem - r * W;
-      const int64_t ri = (int64_t)s_frow0[i] + r;
-      const int nsh = A.rinfo_nsh[ri];
-      const int q = A.rinfo_spos[ri * W + sidx];
-      const unsigned mask = A.rinfo_mask[ri * W + sidx];
-      if (sidx >= nsh) continue;
-      double part[MAX_VALENCE];
-#pragma unroll
-      for (int m = 0; m < MAX_VALENCE; ++m)
-        part[m] = (mask >> m) & 1u ? __ldcg(A.recd + ((int64_t)s_fslot[i * MAX_VALENCE + m] + r) * W + sidx) : 0.0;
-      double sum = 0.0;
-#pragma unroll
-      for (int m = 0; m < MAX_VALENCE; ++m)
-        if ((mask >> m) & 1u) sum += part[m];
+      const int r = rem / W, q = rem - r * W;
       const int rg2 = s_rpre[i] + r;
-      const int64_t ro = rg2 < MAXFR ? s_rowoff[rg2] : A.row_ptr[(int64_t)A.ose[s_fin[i]].gid_base + r - A.row_begin];
+      int64_t ro;
+      int len;
+      if (rg2 < MAXFR) { ro = s_rowoff[rg2]; len = s_rowlen[rg2]; }
+      else {
+        const int64_t g = (int64_t)A.ose[s_fin[i]].gid_base + r - A.row_begin;
+        ro = A.row_ptr[g];
+        len = (int)(A.row_ptr[g + 1] - ro);
+      }
+      if (q >= len) continue;
+      const int k = s_fk[i];
+      const int rstr = ((2 * k + W * k) + 1) & ~1;
+      const uint8_t *pr = A.plan + s_fpb[i] + (int64_t)r * rstr;
+      const uint16_t *lrow = reinterpret_cast<const uint16_t *>(pr);
+      const uint8_t *js = pr + 2 * k + q * k;
+      int gid = 0;
+      bool have = false;
+      double sum = 0.0;
+      for (int m = 0; m < k; ++m) {
+        const int jm = __ldg(js + m);
+        if (jm == 255) continue;
+        const int64_t rb = ((int64_t)s_felem[i * MAX_VALENCE + m] * CF::NDPE + __ldg(lrow + m)) * W + jm;
+        if (!have) { gid = __ldcg(A.ngid + rb); have = true; }
+        sum += __ldcg(A.nval + rb);
+      }
+      A.col[ro + q] = gid;
       A.val[ro + q] = sum;
     }
   }

@@ -79,11 +79,11 @@ struct SpaceDev {
   uint32_t *tslot = nullptr, *tpb = nullptr;
   uint8_t *tsize = nullptr, *tnpb = nullptr, *tlex = nullptr;
   int W = 0;
-  // setup merge plan of shared rows
-  uint16_t *rmap = nullptr, *rinfo_mask = nullptr;
-  double *recd = nullptr;
-  int32_t *ose_row0 = nullptr;
-  uint8_t *rinfo_nsh = nullptr, *rinfo_spos = nullptr, *is_defer = nullptr;
+  // shared rows: natural-order partial rows and the setup merge plan
+  double *nval = nullptr;
+  int32_t *ngid = nullptr, *ose_elem = nullptr;
+  int64_t *pbase = nullptr;
+  uint8_t *plan = nullptr, *is_defer = nullptr;
 };
 
 }  // namespace
@@ -238,14 +238,13 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.ose = S.ose;
   a.ose_slots = S.ose_slots;
   a.counters = S.counters;
-  a.rmap = S.rmap;
-  a.recd = S.recd;
-  a.ose_row0 = S.ose_row0;
-  a.rinfo_nsh = S.rinfo_nsh;
-  a.rinfo_spos = S.rinfo_spos;
-  a.rinfo_mask = S.rinfo_mask;
-  a.maxl = (S.maxl + 7) / 8 * 8;
-  a.plan = 0;
+  a.nval = S.nval;
+  a.ngid = S.ngid;
+  a.ose_elem = S.ose_elem;
+  a.pbase = S.pbase;
+  a.plan = S.plan;
+  a.maxl = S.maxl;
+  a.plan_mode = 0;
   a.alpha = alpha;
   a.beta = beta;
   a.err = c->err;
@@ -466,18 +465,24 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     SpaceDev &S = c->sp[s];
     if (!S.valid || S.n_ose == 0) continue;
     const SpacePlan &P = plan.sp[s];
-    std::vector<int32_t> row0(P.ose.size());
+    std::vector<int64_t> pb(P.ose.size());
     std::vector<uint8_t> isdef(P.ose.size(), 0);
-    int64_t nri = 0;
-    for (size_t i = 0; i < P.ose.size(); ++i) { row0[i] = (int32_t)nri; nri += P.ose[i].nrows; }
+    std::vector<int32_t> oel(P.ose_elem.size());
+    int64_t nbytes = 0;
+    for (size_t i = 0; i < P.ose.size(); ++i) {
+      pb[i] = nbytes;
+      const int k = P.ose[i].k;
+      nbytes += (int64_t)P.ose[i].nrows * (((2 * k + S.W * k) + 1) & ~1);
+    }
     for (int32_t d : P.defer) isdef[d] = 1;
-    if (dev_upload(c, &S.ose_row0, row0.data(), row0.size()) != cudaSuccess ||
+    for (size_t i = 0; i < oel.size(); ++i) oel[i] = (int32_t)(P.ose_elem[i] - plan.elem_begin);
+    const int ndpe_asm = S.ndpe;
+    if (dev_upload(c, &S.pbase, pb.data(), pb.size()) != cudaSuccess ||
         dev_upload(c, &S.is_defer, isdef.data(), isdef.size()) != cudaSuccess ||
-        dev_alloc(c, &S.rinfo_nsh, (size_t)nri) != cudaSuccess ||
-        dev_alloc(c, &S.rinfo_spos, (size_t)nri * S.W) != cudaSuccess ||
-        dev_alloc(c, &S.rinfo_mask, (size_t)nri * S.W) != cudaSuccess ||
-        dev_alloc(c, &S.rmap, (size_t)S.n_records * ((S.maxl + 7) / 8 * 8)) != cudaSuccess ||
-        dev_alloc(c, &S.recd, (size_t)S.n_records * S.W) != cudaSuccess)
+        dev_upload(c, &S.ose_elem, oel.data(), oel.size()) != cudaSuccess ||
+        dev_alloc(c, &S.plan, (size_t)std::max<int64_t>(nbytes, 16)) != cudaSuccess ||
+        dev_alloc(c, &S.nval, (size_t)c->nel_local * ndpe_asm * S.W) != cudaSuccess ||
+        dev_alloc(c, &S.ngid, (size_t)c->nel_local * ndpe_asm * S.W) != cudaSuccess)
       return bail(LOR_ERR_OUT_OF_MEMORY, "plan");
     AsmArgs a{};
     a.nel_local = c->nel_local;
@@ -494,8 +499,8 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     a.ose = S.ose;
     a.ose_slots = S.ose_slots;
     a.counters = S.counters;
-    a.maxl = (S.maxl + 7) / 8 * 8;
-    a.plan = 1;
+    a.maxl = S.maxl;
+    a.plan_mode = 1;
     a.alpha = 1.0;
     a.beta = 1.0;
     a.err = c->err;
@@ -507,13 +512,9 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     pa.is_defer = S.is_defer;
     pa.scratch = S.scratch;
     pa.rstride = S.rstride;
-    pa.maxl = (S.maxl + 7) / 8 * 8;
     pa.W = S.W;
-    pa.rmap = S.rmap;
-    pa.ose_row0 = S.ose_row0;
-    pa.rinfo_nsh = S.rinfo_nsh;
-    pa.rinfo_spos = S.rinfo_spos;
-    pa.rinfo_mask = S.rinfo_mask;
+    pa.pbase = S.pbase;
+    pa.plan = S.plan;
     if (launch_plan_merge(pa, S.n_ose, c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "plan merge");
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "plan sync");
     int herr[4] = {0, 0, 0, 0};

@@ -285,61 +285,54 @@ __global__ void __launch_bounds__(128) k_finalize_list(FinArgs F) {
 
 // ================================================================================ setup merge plan
 // One CTA per owned shared entity whose contributors are all local; one thread per row.  Reads the
-// partial-row records written by k_assemble in plan mode (sorted entries tagged with their block
-// base), merges the block runs of the k contributors by base (the final row order) and records,
-// for every run of every contributor, its offset in the final row and -- if the block is held by
-// two or more contributors -- in the row's list of shared values, plus per row the final position
-// and contributor mask of every shared value.  Topological: computed once in lor_setup.
+// partial-row records written by k_assemble in plan mode (each contributor's row sorted by column,
+// entries tagged with their block base and stencil slot; header = length, local row), merges the
+// block runs of the k contributors by base (= the final row order) and records, for every final
+// position q and contributor m, m's stencil slot at q (255 = m does not hold q), plus m's local row.
+// Topological: computed once in lor_setup; at run time the last contributor gathers with it.
 __global__ void k_plan_merge(PlanArgs A) {
   const int oi = blockIdx.x;
   if (oi >= A.n || A.is_defer[oi]) return;
   const Ose O = A.ose[oi];
-  const int k = O.k;
+  const int k = O.k, W = A.W;
+  const int rstr = ((2 * k + W * k) + 1) & ~1;
   for (int r = threadIdx.x; r < O.nrows; r += blockDim.x) {
+    uint8_t *pr = A.plan + A.pbase[oi] + (int64_t)r * rstr;
+    uint16_t *lrow = reinterpret_cast<uint16_t *>(pr);
+    uint8_t *js = pr + 2 * k;
+    for (int i = 0; i < W * k; ++i) js[i] = 255;
     int64_t rid[MAX_VALENCE];
-    int len[MAX_VALENCE], ptr[MAX_VALENCE], run[MAX_VALENCE];
+    int len[MAX_VALENCE], ptr[MAX_VALENCE];
     for (int m = 0; m < k; ++m) {
-      rid[m] = (int64_t)A.ose_slots[O.slot_off + m] + r;
-      len[m] = A.scratch[rid[m] * A.rstride + A.rstride - 1].col;
+      rid[m] = ((int64_t)A.ose_slots[O.slot_off + m] + r) * A.rstride;
+      const RecEntry h = A.scratch[rid[m] + A.rstride - 1];
+      len[m] = h.col;
+      lrow[m] = (uint16_t)h.bbase;
       ptr[m] = 0;
-      run[m] = 0;
     }
-    const int64_t ri = (int64_t)A.ose_row0[oi] + r;
-    int P = 0, nsh = 0;
+    int P = 0;
     while (true) {
       int minb = 0x7fffffff;
       for (int m = 0; m < k; ++m)
         if (ptr[m] < len[m]) {
-          const int b = A.scratch[rid[m] * A.rstride + ptr[m]].bbase;
+          const int b = A.scratch[rid[m] + ptr[m]].bbase;
           minb = b < minb ? b : minb;
         }
       if (minb == 0x7fffffff) break;
-      unsigned mask = 0;
       int size = 0;
       for (int m = 0; m < k; ++m) {
-        if (ptr[m] >= len[m] || A.scratch[rid[m] * A.rstride + ptr[m]].bbase != minb) continue;
+        if (ptr[m] >= len[m] || A.scratch[rid[m] + ptr[m]].bbase != minb) continue;
         int e = ptr[m];
-        while (e < len[m] && A.scratch[rid[m] * A.rstride + e].bbase == minb) ++e;
-        size = e - ptr[m];
-        mask |= 1u << m;
-      }
-      const bool sh = __popc(mask) >= 2;
-      for (int m = 0; m < k; ++m) {
-        if (!(mask & (1u << m))) continue;
-        A.rmap[rid[m] * A.maxl + run[m]] = (uint16_t)(P | ((sh ? nsh : 255) << 8));
-        ++run[m];
-        ptr[m] += size;
-      }
-      if (sh) {
-        for (int o = 0; o < size; ++o) {
-          A.rinfo_spos[ri * A.W + nsh + o] = (uint8_t)(P + o);
-          A.rinfo_mask[ri * A.W + nsh + o] = (uint16_t)mask;
+        while (e < len[m] && A.scratch[rid[m] + e].bbase == minb) {
+          const int q = P + (e - ptr[m]);
+          if (q < W) js[q * k + m] = (uint8_t)(int)A.scratch[rid[m] + e].val;
+          ++e;
         }
-        nsh += size;
+        size = e - ptr[m];
+        ptr[m] = e;
       }
       P += size;
     }
-    A.rinfo_nsh[ri] = (uint8_t)nsh;
   }
 }
 

@@ -54,31 +54,29 @@ struct AsmArgs {
   const Ose *ose;
   const int32_t *ose_slots;
   int32_t *counters;
-  // setup-time merge plan of shared rows whose contributors are all local
-  const uint16_t *rmap;          // [n_records][maxl]: per block run of the record: P0u | P0s << 8 (255 = exclusive);
-                                 // row stride maxl is a multiple of 8 (16-byte rows)
-  double *recd;                  // [n_records][W] compact shared values
-  const int32_t *ose_row0;       // [n_ose] first row-info index of the OSE
-  const uint8_t *rinfo_nsh;      // [n_rowinfo] number of shared positions of the row
-  const uint8_t *rinfo_spos;     // [n_rowinfo][W] final positions of the shared entries
-  const uint16_t *rinfo_mask;    // [n_rowinfo][W] contributor bit mask of each shared entry
+  // shared rows whose contributors are all local: every contributor
+  // writes its partial row in natural stencil-slot order; the last one to arrive emits the row
+  double *nval;                  // [nel_local][NDPE][W] partial values (orientation signs applied)
+  int32_t *ngid;                 // [nel_local][NDPE][W] their global column ids
+  const int32_t *ose_elem;       // per OSE slot (ose_slots order): local index of the contributing element
+  const int64_t *pbase;          // [n_ose] byte offset of the OSE's merge-plan rows
+  const uint8_t *plan;           // per OSE row: k x uint16 contributor local rows, then W x k slot bytes
   int maxl;
-  int plan;                      // 1: setup plan pass (write records of every shared row, no CSR output)
+  int plan_mode;                 // 1: setup plan pass (partial-row records of every shared row, no CSR output)
   double alpha, beta;
   int *err;                      // [0] code, [1] element, [2] cell
 };
 
 struct PlanArgs {
-  int n;                         // number of local OSEs (not deferred)
+  int n;                         // number of OSEs
   const Ose *ose;
   const int32_t *ose_slots;
   const uint8_t *is_defer;       // [n_ose]
-  const RecEntry *scratch;
-  int rstride, maxl, W;
-  uint16_t *rmap;
-  const int32_t *ose_row0;
-  uint8_t *rinfo_nsh, *rinfo_spos;
-  uint16_t *rinfo_mask;
+  const RecEntry *scratch;       // plan-mode records: entries (col, block base, slot index as double),
+                                 // header (len, local row)
+  int rstride, W;
+  const int64_t *pbase;
+  uint8_t *plan;
 };
 
 struct FinArgs {

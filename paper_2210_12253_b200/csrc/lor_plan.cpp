@@ -354,6 +354,7 @@ void HostPlan::build(const PlanInput &in) {
           else { sl.rel = recv_cnt[q]; recv_cnt[q] += nd[t]; remote = true; }
           slots.push_back(sl);
           S.ose_slots.push_back(0);
+          S.ose_elem.push_back((int32_t)e);
         }
         if (remote) S.defer.push_back((int32_t)oi);
         ose_of[t][id] = oi;

@@ -25,6 +25,7 @@ struct SpacePlan {
   std::vector<ElemSpace> esp;             // per local element
   std::vector<Ose> ose;                   // owned shared entities
   std::vector<int32_t> ose_slots;         // record base per slot
+  std::vector<int32_t> ose_elem;          // global element id per slot
   std::vector<int32_t> defer;             // OSE indices finalized after the exchange
   int64_t n_records = 0;                  // scratch records (MAXL entries each)
   std::vector<int64_t> recv_begin, recv_count, send_begin, send_count;  // per peer, in records
