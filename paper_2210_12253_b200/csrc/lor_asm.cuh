@@ -14,6 +14,24 @@ namespace lorb {
 __host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b * ipow_c(b, e - 1); }
 
 // ------------------------------------------------------------------------ small helpers
+// L2 eviction priorities: the CSR output is written once and never re-read by this kernel
+// (evict_first); partial rows wait in L2 for the last contributor of their entity (evict_last).
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_hint(int32_t *a, int32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(double *a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void report_error(int *err, int code, int64_t e, int cell) {
   if (atomicCAS(err, 0, code) == 0) {
     err[1] = (int)e;
@@ -87,6 +105,11 @@ __device__ __forceinline__ int row_key(int p, int s, const int x[3]) {
 __device__ __forceinline__ int join_cls(int cr, int cc) { return (cr == cc && cr != 1) ? cr : 1; }
 
 // ================================================================================ k_assemble
+// natural-order partial-row records: row strides padded to whole 32-byte sectors and written
+// completely (invalid slots as 0 / -1), so a record sector is never partially valid in L2
+__host__ __device__ constexpr int rec_w8(int W) { return (W + 3) / 4 * 4; }   // doubles per row
+__host__ __device__ constexpr int rec_w4(int W) { return (W + 7) / 8 * 8; }   // int32 per row
+
 template <int DIM, int SP, int P, int KZ>
 struct AsmCfg {
   using T_ = Tr<DIM, SP>;
@@ -459,6 +482,28 @@ __device__ __forceinline__ void emit_row(const AsmArgs &A, const RowRec &R, cons
   const int64_t key = (int64_t)R.s * NROWKEY + R.rk;
   int32_t *colr = A.col + R.out;
   double *valr = A.val + R.out;
+  if (R.mode == 4) {  // natural-order partial row: no position work, dense sector-aligned record
+    constexpr int W8 = rec_w8(W), W4 = rec_w4(W);
+    const uint64_t pl = l2_policy_last();
+#pragma unroll
+    for (int j0 = 0; j0 < W4; j0 += 32) {
+      const int j = j0 + lane;
+      double v = 0.0;
+      int gid = -1;
+      if (j < W) {
+        const uint32_t w = wpre[j0 / 32];
+        if ((w & 127) != 127) {
+          const int s2 = (w >> 24) & 3;
+          const int l = R.lb[s2] + dlt[R.s * W + j];
+          gid = gmap[l];
+          v = (bsg[l] & 128) ? -vrow[j] : vrow[j];
+        }
+      }
+      if (j < W8) st_hint(A.nval + R.recid * W8 + j, v, pl);
+      if (j < W4) st_hint(A.ngid + R.recid * W4 + j, gid, pl);
+    }
+    return;
+  }
 #pragma unroll
   for (int j0 = 0; j0 < W; j0 += 32) {
     const int j = j0 + lane;
@@ -471,16 +516,14 @@ __device__ __forceinline__ void emit_row(const AsmArgs &A, const RowRec &R, cons
         const int gid = gmap[l];
         const int bs = bsg[l];
         const int b = bs & 127;
-        if (R.mode == 4) {  // natural-order partial row: no position work
-          A.nval[R.recid * W + j] = (bs & 128) ? -vrow[j] : vrow[j];
-          A.ngid[R.recid * W + j] = gid;
-        } else {
+        {
           const int lex = __ldg(A.tabs.lex + ((key * W + j) << 3) + T.orient[b - 27 * s2]);
           const int pos = (int)(p0r[b] & 255u) + lex;
           const double v = (bs & 128) ? -vrow[j] : vrow[j];
           if (R.mode == 1) {
-            colr[pos] = gid;
-            valr[pos] = v;
+            const uint64_t pf = l2_policy_first();
+            st_hint(colr + pos, gid, pf);
+            st_hint(valr + pos, v, pf);
           } else {
             double2 *dst = reinterpret_cast<double2 *>(A.scratch) + R.out;
             dst[pos] = make_double2(__longlong_as_double(((long long)(unsigned)blk[b].base << 32) | (unsigned)gid),
@@ -518,8 +561,8 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
   RowRec *rr = reinterpret_cast<RowRec *>(smem + CF::OFF_RM) + warp * RG;
   uint16_t *p0r = reinterpret_cast<uint16_t *>(smem + CF::OFF_P0) + warp * RG * NBP;
   int8_t *dlt = reinterpret_cast<int8_t *>(smem + CF::OFF_DL);
-  const int64_t el = blockIdx.x;  // local element index
-  if (el >= A.nel_local) return;
+  if ((int64_t)blockIdx.x >= A.nel_local) return;
+  const int64_t el = A.order ? A.order[blockIdx.x] : blockIdx.x;  // local element (locality-preserving order)
   {
     const int4 *src = reinterpret_cast<const int4 *>(A.topo + el);
     int4 *dst = reinterpret_cast<int4 *>(&T);
@@ -833,12 +876,13 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
       for (int m = 0; m < k; ++m) {
         const int jm = __ldg(js + m);
         if (jm == 255) continue;
-        const int64_t rb = ((int64_t)s_felem[i * MAX_VALENCE + m] * CF::NDPE + __ldg(lrow + m)) * W + jm;
-        if (!have) { gid = __ldcg(A.ngid + rb); have = true; }
-        sum += __ldcg(A.nval + rb);
+        const int64_t rr3 = (int64_t)s_felem[i * MAX_VALENCE + m] * CF::NDPE + __ldg(lrow + m);
+        if (!have) { gid = __ldcg(A.ngid + rr3 * rec_w4(W) + jm); have = true; }
+        sum += __ldcg(A.nval + rr3 * rec_w8(W) + jm);
       }
-      A.col[ro + q] = gid;
-      A.val[ro + q] = sum;
+      const uint64_t pf = l2_policy_first();
+      st_hint(A.col + ro + q, gid, pf);
+      st_hint(A.val + ro + q, sum, pf);
     }
   }
 }

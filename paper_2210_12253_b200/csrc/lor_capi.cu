@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -93,6 +94,7 @@ struct lor_ctx_s {
   int64_t nel = 0, elem_begin = 0, nel_local = 0, ntopo = 0;
   cudaStream_t stream = nullptr;
   ElemTopo *topo = nullptr;
+  int32_t *order = nullptr;  // CTA -> local element, Morton order of element centroids
   double *X = nullptr;
   int64_t xstride = 0;
   SpaceDev sp[3];
@@ -221,6 +223,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   if (st) return st;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   AsmArgs a;
+  a.order = c->order;
   a.nel_local = c->nel_local;
   a.elem_begin = c->elem_begin;
   a.topo = c->topo;
@@ -376,6 +379,39 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     }
     std::vector<double> padded((size_t)(plan.nel_local * c->xstride), 0.0);
     for (int64_t e = 0; e < plan.nel_local; ++e) memcpy(&padded[e * c->xstride], src + e * raw, sizeof(double) * raw);
+    // locality-preserving processing order: Morton code of element centroids (neighbours of an
+    // element are processed close in time, so partial rows are merged while still in L2)
+    {
+      const int64_t n = plan.nel_local;
+      std::vector<double> cen((size_t)n * 3, 0.0);
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      for (int64_t e = 0; e < n; ++e)
+        for (int d = 0; d < A.dim; ++d) {
+          double sum = 0.0;
+          for (int l = 0; l < np; ++l) sum += src[e * raw + (int64_t)d * np + l];
+          const double v = sum / np;
+          cen[e * 3 + d] = v;
+          lo[d] = std::min(lo[d], v);
+          hi[d] = std::max(hi[d], v);
+        }
+      std::vector<std::pair<uint64_t, int32_t>> key((size_t)n);
+      for (int64_t e = 0; e < n; ++e) {
+        uint64_t code = 0;
+        uint32_t qd[3] = {0, 0, 0};
+        for (int d = 0; d < A.dim; ++d) {
+          const double t = hi[d] > lo[d] ? (cen[e * 3 + d] - lo[d]) / (hi[d] - lo[d]) : 0.0;
+          qd[d] = (uint32_t)std::min(1023.0, std::max(0.0, t * 1023.0 + 0.5));
+        }
+        for (int bit = 9; bit >= 0; --bit)
+          for (int d = A.dim - 1; d >= 0; --d) code = (code << 1) | ((qd[d] >> bit) & 1u);
+        key[e] = {code, (int32_t)e};
+      }
+      std::stable_sort(key.begin(), key.end(),
+                       [](const std::pair<uint64_t, int32_t> &a, const std::pair<uint64_t, int32_t> &b) { return a.first < b.first; });
+      std::vector<int32_t> ord((size_t)n);
+      for (int64_t e = 0; e < n; ++e) ord[e] = key[e].second;
+      if (dev_upload(c, &c->order, ord.data(), ord.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "order");
+    }
     if (dev_upload(c, &c->X, padded.data(), padded.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "X");
   }
   if (dev_upload(c, &c->topo, plan.topo.data(), plan.topo.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "topo");
@@ -481,10 +517,11 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
         dev_upload(c, &S.is_defer, isdef.data(), isdef.size()) != cudaSuccess ||
         dev_upload(c, &S.ose_elem, oel.data(), oel.size()) != cudaSuccess ||
         dev_alloc(c, &S.plan, (size_t)std::max<int64_t>(nbytes, 16)) != cudaSuccess ||
-        dev_alloc(c, &S.nval, (size_t)c->nel_local * ndpe_asm * S.W) != cudaSuccess ||
-        dev_alloc(c, &S.ngid, (size_t)c->nel_local * ndpe_asm * S.W) != cudaSuccess)
+        dev_alloc(c, &S.nval, (size_t)c->nel_local * ndpe_asm * ((S.W + 3) / 4 * 4)) != cudaSuccess ||
+        dev_alloc(c, &S.ngid, (size_t)c->nel_local * ndpe_asm * ((S.W + 7) / 8 * 8)) != cudaSuccess)
       return bail(LOR_ERR_OUT_OF_MEMORY, "plan");
     AsmArgs a{};
+    a.order = c->order;
     a.nel_local = c->nel_local;
     a.elem_begin = c->elem_begin;
     a.topo = c->topo;

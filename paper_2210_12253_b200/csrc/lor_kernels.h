@@ -39,6 +39,7 @@ struct CountArgs {
 
 struct AsmArgs {
   int64_t nel_local, elem_begin;
+  const int32_t *order;          // CTA -> local element (Morton order of element centroids), or NULL
   const ElemTopo *topo;
   const ElemSpace *esp;
   const double *X;               // local E-vector, element stride xstride doubles
