@@ -154,7 +154,8 @@ lor_status lor_assemble_finish(lor_ctx ctx, lor_space space, lor_csr *out);
 lor_status lor_plan_dry_run(const lor_setup_args *args, int64_t *info, int64_t *send_counts, int64_t *recv_counts);
 
 /* Diagnostics: copy internal setup tables of `space` to host memory (what = 0: row-class slot
- * table uint32[S][729][W]; 1: block-size table uint8[S][729][3*27 or 27]).  Returns bytes copied
+ * table uint32[S][729][W]; 1: block-size table uint8[S][729][3*27 or 27]; 2: per-CTA phase clocks
+ * uint64[n_elem_local][16] of the last element pass, only if LOR_PHASE_TIMING=1 at setup).  Returns bytes copied
  * (0 on error / cap too small). */
 int64_t lor_debug_dump(lor_ctx ctx, int what, lor_space space, void *host_out, int64_t cap_bytes);
 

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "lor_cells.cuh"
 #include "lor_device.cuh"
 #include "lor_kernels.h"
@@ -15,6 +17,8 @@ __host__ __device__ constexpr int ipow_c(int b, int e) { return e == 0 ? 1 : b *
 
 // ------------------------------------------------------------------------ small helpers
 // L2 eviction priorities: the CSR output is written once and never re-read by this kernel
+// (the hinted stores carry no "memory" clobber: nothing in the issuing thread reads them back, and
+// leaving it off lets the compiler hoist the shared-memory loads of later slots above them)
 // (evict_first); partial rows wait in L2 for the last contributor of their entity (evict_last).
 __device__ __forceinline__ uint64_t l2_policy_first() {
   uint64_t p;
@@ -27,11 +31,53 @@ __device__ __forceinline__ uint64_t l2_policy_last() {
   return p;
 }
 __device__ __forceinline__ void st_hint(int32_t *a, int32_t v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol));
 }
 __device__ __forceinline__ void st_hint(double *a, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol));
 }
+// streaming reads (coordinates, merge plan, row offsets): read once per call, so they must not
+// push the waiting partial rows out of L2
+__device__ __forceinline__ uint4 ld_stream(const uint4 *a, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2 *a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_stream(const int64_t *a, uint64_t pol) {
+  int64_t v;
+  asm volatile("ld.global.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint2(double *a, double v0, double v1, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v0), "d"(v1), "l"(pol));
+}
+// debug: per-CTA phase clocks (A.tstamp, LOR_PHASE_TIMING=1)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid_() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define LOR_TSTAMP(cond, k)                                                                \
+  do {                                                                                     \
+    if (A.tstamp && (cond)) A.tstamp[(int64_t)blockIdx.x * 16 + (k)] = clock64();        \
+  } while (0)
+#define LOR_STAMP(k)                                                                       \
+  do {                                                                                     \
+    if (A.tstamp && threadIdx.x == 0) A.tstamp[(int64_t)blockIdx.x * 16 + (k)] = clock64(); \
+  } while (0)
+
 __device__ __forceinline__ void report_error(int *err, int code, int64_t e, int cell) {
   if (atomicCAS(err, 0, code) == 0) {
     err[1] = (int)e;
@@ -105,10 +151,17 @@ __device__ __forceinline__ int row_key(int p, int s, const int x[3]) {
 __device__ __forceinline__ int join_cls(int cr, int cc) { return (cr == cc && cr != 1) ? cr : 1; }
 
 // ================================================================================ k_assemble
-// natural-order partial-row records: row strides padded to whole 32-byte sectors and written
-// completely (invalid slots as 0 / -1), so a record sector is never partially valid in L2
-__host__ __device__ constexpr int rec_w8(int W) { return (W + 3) / 4 * 4; }   // doubles per row
-__host__ __device__ constexpr int rec_w4(int W) { return (W + 7) / 8 * 8; }   // int32 per row
+// natural-order partial-row records (values only; columns and column signs of shared rows are
+// topological and live in the setup merge plan): row strides padded to whole 128-byte lines, so a
+// record line can be dropped from L2 with discard.global.L2 once the finalizer has consumed it
+// (no write-back to HBM)
+__host__ __device__ constexpr int rec_w8(int W) { return (W + 15) / 16 * 16; }  // doubles per row
+
+// H1 stencil slot j <-> neighbour offset (dx, dy, dz) in {-1,0,1}^d, x fastest (st_slot order)
+template <int DIM>
+__host__ __device__ constexpr int h1_off(int j, int a) { return a == 0 ? j % 3 - 1 : (a == 1 ? (j / 3) % 3 - 1 : (DIM == 3 ? j / 9 - 1 : 0)); }
+template <int DIM, int P>
+__host__ __device__ constexpr int h1_dl(int j) { return h1_off<DIM>(j, 0) + (P + 1) * (h1_off<DIM>(j, 1) + (P + 1) * h1_off<DIM>(j, 2)); }
 
 template <int DIM, int SP, int P, int KZ>
 struct AsmCfg {
@@ -120,37 +173,28 @@ struct AsmCfg {
   static constexpr int CPL = P * P;                               // cells per layer (2D: all)
   static constexpr int NRING = DIM == 3 ? (KZ == P ? P : KZ + 1) : 1;
   static constexpr int NCELL = NRING * CPL;                       // cells resident in smem
+  static constexpr int NCP = NCELL | 1;                           // cell-matrix pitch (odd: the 8 corner
+                                                                  // lanes of a cell hit different banks)
   static constexpr int NW = 4;                                    // warps per CTA
-  static constexpr int RG = 16;                                   // rows per warp group
-  static constexpr int NBP = (NB + 7) / 8 * 8;                    // P0 entries per row (uint16)
-  // shared memory layout (bytes)
+  static constexpr int NT = NW * 32;
+  static constexpr int TZS = tab_tzs(NB);                         // block-size table row (bytes)
+  static constexpr int TSB = TZS + (NB + 15) / 16 * 16;           // per-thread row scratch: sizes/positions | P0
+  // shared memory layout (bytes); everything from OFF_X on is reused by the finalizer
   static constexpr int OFF_BLK = 0;
   static constexpr int OFF_OS = OFF_BLK + NB * (int)sizeof(Blk);            // ordsig[NB] uint16
   static constexpr int OFF_BL = OFF_OS + NB * 2;                           // blist[NB] uint8
   static constexpr int OFF_GM = (OFF_BL + NB + 15) / 16 * 16;              // gmap[NDPE] int32
   static constexpr int OFF_BS = OFF_GM + NDPE * 4;                         // bsg[NDPE] uint8
-  static constexpr int OFF_X = (OFF_BS + NDPE + 15) / 16 * 16;
+  static constexpr int OFF_DL = (OFF_BS + NDPE + 15) / 16 * 16;            // dl[S][W] int16: local offset | s2 << 8
+  static constexpr int OFF_X = (OFF_DL + S * W * 2 + 15) / 16 * 16;
   static constexpr int OFF_CM = (OFF_X + DIM * NPTS * 8 + 15) / 16 * 16;
-  static constexpr int OFF_VB = (OFF_CM + NENT * NCELL * 8 + 15) / 16 * 16;  // per warp: RG rows x W values
-  static constexpr int OFF_RM = (OFF_VB + NW * RG * W * 8 + 15) / 16 * 16;   // per warp: RG row records
-  static constexpr int OFF_P0 = OFF_RM + NW * RG * 32;                     // per warp: RG x P0[NBP] uint16
-  static constexpr int RMS = (MAXL + 7) / 8 * 8;                  // merge-plan row (uint16 entries)
-  static constexpr int TMPB = tab_tzs(NB) + RMS * 2;              // per-row staging of table rows
-  static constexpr int OFF_TMP = (OFF_P0 + NW * RG * NBP * 2 + 15) / 16 * 16;
-  static constexpr int OFF_DL = OFF_TMP + NW * RG * TMPB;                  // dl[S][W] int8 (slot -> local offset)
-  static constexpr int SMEM = (OFF_DL + S * W + 15) / 16 * 16;
+  static constexpr int OFF_TS = (OFF_CM + NENT * NCP * 8 + 15) / 16 * 16;    // row scratch [TSB][NT] bytes
+  static constexpr int MAXR = DIM == 3 ? S * (P + 1) * (P + 1) * (KZ + 1) : (P + 1) * (P + 1);  // rows per chunk
+  static constexpr int OFF_RL = OFF_TS + NT * TSB;                         // row order list uint16[MAXR]
+  static constexpr int SMEM = (OFF_RL + 2 * MAXR + 15) / 16 * 16;
+  static_assert(TZS >= W, "slot positions overwrite the block-size bytes");
 };
 
-// per-row record kept by the row's thread for the warp-wide emission
-struct __align__(16) RowRec {
-  int64_t out;     // mode 1, 3: CSR offset of the row; mode 2: scratch entry offset of the record
-  int64_t recid;   // mode 4: natural record row; mode 2: record length (header)
-  int32_t lb[3];   // local index of the row position in each column sub-lattice's layout
-  uint16_t rk;     // row key
-  uint8_t mode;    // 0 skip, 1 own row, 2 partial-row record (sorted, merged at run time), 4 natural-order partial row
-  uint8_t s;       // sub-lattice
-};
-static_assert(sizeof(RowRec) == 32, "RowRec");
 
 // per-row value accumulation: acc[slot] = sum over cells containing the row of the cell matrix row
 template <int DIM, int SP, int P, int RS, int NC>
@@ -297,15 +341,18 @@ __device__ __forceinline__ void cells_h1_corner(const double *__restrict__ X, do
     if (act) {
       const int ci = (((cz % NRING_) * P) + cy) * P + cx;
       double *o = cm + ci;
-      o[tri(8, q, q) * NC] = diag;
+      // packed upper-triangle index of (i, j), i <= j < 8: i*8 - i(i-1)/2 + (j - i) = i(15-i)/2 + j
+      const int rq = (q * (15 - q)) >> 1;
+      o[(rq + q) * NC] = diag;
 #pragma unroll
       for (int d = 0; d < 3; ++d)
-        if (!((q >> d) & 1)) o[tri(8, q, q ^ (1 << d)) * NC] = edge[d];
+        if (!((q >> d) & 1)) o[(rq + (q | (1 << d))) * NC] = edge[d];
       // face diagonal of (d,d') is written by the lower of its two corners q, q^d^d'
-      if (q < (q ^ 3)) o[tri(8, q ^ 1, q ^ 2) * NC] = fdg[0];
-      if (q < (q ^ 5)) o[tri(8, q ^ 1, q ^ 4) * NC] = fdg[1];
-      if (q < (q ^ 6)) o[tri(8, q ^ 2, q ^ 4) * NC] = fdg[2];
-      if (q < 4) o[tri(8, q, q ^ 7) * NC] = 0.0;
+      auto tp = [](int a, int b) { const int i = a < b ? a : b, j = a < b ? b : a; return ((i * (15 - i)) >> 1) + j; };
+      if (q < (q ^ 3)) o[tp(q ^ 1, q ^ 2) * NC] = fdg[0];
+      if (q < (q ^ 5)) o[tp(q ^ 1, q ^ 4) * NC] = fdg[1];
+      if (q < (q ^ 6)) o[tp(q ^ 2, q ^ 4) * NC] = fdg[2];
+      if (q < 4) o[(rq + (q ^ 7)) * NC] = 0.0;
     }
   }
 }
@@ -467,81 +514,10 @@ static __device__ __noinline__ void finalize_ose(const Ose O, const int32_t *__r
   }
 }
 
-// Warp-wide emission of one row (lanes = stencil slots): each lane places its column at
-// P0(block) + rank inside the block's sub-box (setup table per orientation code of the block's
-// entity), so the row comes out in ascending global column order and the warp's stores cover a
-// contiguous range (coalesced).  P0 per block was prepared by the row's thread (p0r).
-template <int DIM, int SP, int P>
-__device__ __forceinline__ void emit_row(const AsmArgs &A, const RowRec &R, const uint32_t *wpre,
-                                         const double *__restrict__ vrow,
-                                         const uint16_t *__restrict__ p0r, const Blk *__restrict__ blk,
-                                         const ElemTopo &T, const int32_t *__restrict__ gmap,
-                                         const uint8_t *__restrict__ bsg, const int8_t *__restrict__ dlt, int lane) {
-  using C = Tr<DIM, SP>;
-  constexpr int W = C::W;
-  const int64_t key = (int64_t)R.s * NROWKEY + R.rk;
-  int32_t *colr = A.col + R.out;
-  double *valr = A.val + R.out;
-  if (R.mode == 4) {  // natural-order partial row: no position work, dense sector-aligned record
-    constexpr int W8 = rec_w8(W), W4 = rec_w4(W);
-    const uint64_t pl = l2_policy_last();
-#pragma unroll
-    for (int j0 = 0; j0 < W4; j0 += 32) {
-      const int j = j0 + lane;
-      double v = 0.0;
-      int gid = -1;
-      if (j < W) {
-        const uint32_t w = wpre[j0 / 32];
-        if ((w & 127) != 127) {
-          const int s2 = (w >> 24) & 3;
-          const int l = R.lb[s2] + dlt[R.s * W + j];
-          gid = gmap[l];
-          v = (bsg[l] & 128) ? -vrow[j] : vrow[j];
-        }
-      }
-      if (j < W8) st_hint(A.nval + R.recid * W8 + j, v, pl);
-      if (j < W4) st_hint(A.ngid + R.recid * W4 + j, gid, pl);
-    }
-    return;
-  }
-#pragma unroll
-  for (int j0 = 0; j0 < W; j0 += 32) {
-    const int j = j0 + lane;
-    if (j < W) {
-      const uint32_t w = wpre[j0 / 32];
-      const int bw = w & 127;
-      if (bw != 127) {
-        const int s2 = (w >> 24) & 3;
-        const int l = R.lb[s2] + dlt[R.s * W + j];
-        const int gid = gmap[l];
-        const int bs = bsg[l];
-        const int b = bs & 127;
-        {
-          const int lex = __ldg(A.tabs.lex + ((key * W + j) << 3) + T.orient[b - 27 * s2]);
-          const int pos = (int)(p0r[b] & 255u) + lex;
-          const double v = (bs & 128) ? -vrow[j] : vrow[j];
-          if (R.mode == 1) {
-            const uint64_t pf = l2_policy_first();
-            st_hint(colr + pos, gid, pf);
-            st_hint(valr + pos, v, pf);
-          } else {
-            double2 *dst = reinterpret_cast<double2 *>(A.scratch) + R.out;
-            dst[pos] = make_double2(__longlong_as_double(((long long)(unsigned)blk[b].base << 32) | (unsigned)gid),
-                                    A.plan_mode ? (double)j : v);
-          }
-        }
-      }
-    }
-  }
-  if (R.mode == 2 && lane == 0)  // record header: length, local row
-    reinterpret_cast<double2 *>(A.scratch)[R.out + A.rstride - 1] = make_double2(
-        __longlong_as_double(((long long)(unsigned)R.lb[R.s] << 32) | (long long)(unsigned)R.recid), 0.0);
-}
-
-template <int DIM, int SP, int P, int QUAD, int KZ>
-__global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
+template <int DIM, int SP, int P, int QUAD, int KZ, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
   using CF = AsmCfg<DIM, SP, P, KZ>;
-  constexpr int S = CF::S, W = CF::W, NB = CF::NB, NC = CF::NCELL;
+  constexpr int S = CF::S, W = CF::W, NB = CF::NB, NC = CF::NCP;
   extern __shared__ __align__(16) unsigned char smem[];
   Blk *blk = reinterpret_cast<Blk *>(smem + CF::OFF_BLK);
   uint16_t *ordsig = reinterpret_cast<uint16_t *>(smem + CF::OFF_OS);
@@ -556,13 +532,11 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
   __shared__ int s_fin[27];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int RG = CF::RG, NBP = CF::NBP;
-  double *vb = reinterpret_cast<double *>(smem + CF::OFF_VB) + warp * RG * W;
-  RowRec *rr = reinterpret_cast<RowRec *>(smem + CF::OFF_RM) + warp * RG;
-  uint16_t *p0r = reinterpret_cast<uint16_t *>(smem + CF::OFF_P0) + warp * RG * NBP;
-  int8_t *dlt = reinterpret_cast<int8_t *>(smem + CF::OFF_DL);
+  int16_t *dlt = reinterpret_cast<int16_t *>(smem + CF::OFF_DL);
   if ((int64_t)blockIdx.x >= A.nel_local) return;
   const int64_t el = A.order ? A.order[blockIdx.x] : blockIdx.x;  // local element (locality-preserving order)
+  LOR_STAMP(0);
+  if (A.tstamp && tid == 0) A.tstamp[(int64_t)blockIdx.x * 16 + 6] = gtimer();
   {
     const int4 *src = reinterpret_cast<const int4 *>(A.topo + el);
     int4 *dst = reinterpret_cast<int4 *>(&T);
@@ -573,7 +547,8 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
     const double2 *xs = reinterpret_cast<const double2 *>(A.X + el * A.xstride);
     double2 *xd = reinterpret_cast<double2 *>(X);
     constexpr int NX2 = (DIM * CF::NPTS) / 2;
-    for (int i = tid; i < NX2; i += blockDim.x) xd[i] = __ldg(xs + i);
+    const uint64_t pfx = l2_policy_first();
+    for (int i = tid; i < NX2; i += blockDim.x) xd[i] = ld_stream(xs + i, pfx);
     if ((DIM * CF::NPTS) & 1) {
       if (tid == 0) X[DIM * CF::NPTS - 1] = __ldg(A.X + el * A.xstride + DIM * CF::NPTS - 1);
     }
@@ -622,7 +597,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
     const int nx = st_hi<SP>(s, s2, 0) - st_lo<SP>(s, s2, 0) + 1, ny = st_hi<SP>(s, s2, 1) - st_lo<SP>(s, s2, 1) + 1;
     const int dx = st_lo<SP>(s, s2, 0) + jj % nx, dy = st_lo<SP>(s, s2, 1) + (jj / nx) % ny;
     const int dz = (DIM == 3) ? st_lo<SP>(s, s2, 2) + jj / (nx * ny) : 0;
-    dlt[i] = (int8_t)(dx + ext_of<SP>(P, s2, 0) * (dy + ext_of<SP>(P, s2, 1) * dz));
+    dlt[i] = (int16_t)((uint8_t)(int8_t)(dx + ext_of<SP>(P, s2, 0) * (dy + ext_of<SP>(P, s2, 1) * dz)) | (s2 << 8));
   }
   // ---- element restriction in shared memory: global id and block/sign of every local dof
   for (int l = tid; l < CF::NDPE; l += blockDim.x) {
@@ -635,6 +610,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
   }
   __syncthreads();
   const int nb = s_nb;
+  LOR_STAMP(1);
 
   // ---- z-chunks of cell layers
   constexpr int NCHUNK = (DIM == 3) ? (P + KZ - 1) / KZ : 1;
@@ -656,6 +632,7 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
     }
     __syncthreads();
     if (s_bad && tid == 0) report_error(A.err, 2, A.elem_begin + el, s_bad - 1);
+    if (ch == 0) LOR_STAMP(2);
     // rows of this chunk: per sub-lattice s the z range [k0, kend(s))
     int nrows = 0, nrow_s0 = 0, nrow_s1 = 0;
 #pragma unroll
@@ -671,128 +648,191 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
       if (s == 1) nrow_s1 = n;
       nrows += n;
     }
-    // groups of RG rows per warp: the row's thread accumulates its values and prepares P0 of its
-    // blocks (all global loads of the row issued here, in parallel across rows), then the warp
-    // emits the rows one at a time, lanes = stencil slots
-    for (int g0 = warp * RG; g0 < nrows; g0 += CF::NW * RG) {
-      const int r = g0 + lane;
-      if (lane < RG) {
-        RowRec R;
-        R.mode = 0;
-        R.out = 0;
-        R.recid = 0;
-        R.rk = 0;
-        R.s = 0;
-        R.lb[0] = R.lb[1] = R.lb[2] = 0;
-        if (r < nrows) {
-          int s = 0, rq = r;
-          if (S > 1 && rq >= nrow_s0) { rq -= nrow_s0; s = 1; if (rq >= nrow_s1) { rq -= nrow_s1; s = 2; } }
-          const int ex = ext_of<SP>(P, s, 0), ey = ext_of<SP>(P, s, 1);
-          int x[3];
-          x[0] = rq % ex;
-          x[1] = (rq / ex) % ey;
-          x[2] = (DIM == 3) ? k0 + rq / (ex * ey) : 0;
-          const int tr = row_tau<DIM, SP>(P, s, x);
-          const uint8_t fl = T.flags[tr], sf = E.sflags[tr];
-          const bool owned = fl & TF_OWNED;
-          const bool shared = sf & SF_SHARED;
-          const bool local_plan = shared && owned && !(sf & SF_DEFER) && !A.plan_mode;  // mode 3
-          const bool rec = shared && (owned || (sf & SF_SEND)) && !local_plan;      // mode 2
-          if ((owned && !A.plan_mode) || rec || local_plan) {
-            R.s = (uint8_t)s;
-            const int rk = row_key<DIM, SP>(P, s, x);
-            R.rk = (uint16_t)rk;
+    // one thread per row: values from the cell matrices in shared memory; a shared row goes out
+    // as a natural-order partial row (record), an own row straight into its CSR row at the
+    // positions P0(block) + rank in the block's sub-box (ascending global column order)
+    // per-thread row scratch, transposed ([byte][thread]) so lanes never share a bank:
+    // bytes [0, TZS) block sizes, then slot positions; [TZS, TSB) P0 per block
+    unsigned char *ts = smem + CF::OFF_TS + tid;
+    auto decode_row = [&](int r, int &s, int *x) {
+      s = 0;
+      int rq = r;
+      if (S > 1 && rq >= nrow_s0) { rq -= nrow_s0; s = 1; if (rq >= nrow_s1) { rq -= nrow_s1; s = 2; } }
+      const int ex = ext_of<SP>(P, s, 0), ey = ext_of<SP>(P, s, 1);
+      x[0] = rq % ex;
+      x[1] = (rq / ex) % ey;
+      x[2] = (DIM == 3) ? k0 + rq / (ex * ey) : 0;
+      return row_tau<DIM, SP>(P, s, x);
+    };
+    // row order: partial rows first, own rows (the heavier path: positions + CSR stores) last, so
+    // they fill as few warps as possible instead of diverging inside every warp
+    __shared__ int s_nsh, s_nown;
+    uint16_t *rlist = reinterpret_cast<uint16_t *>(smem + CF::OFF_RL);
+    if (tid == 0) { s_nsh = 0; s_nown = 0; }
+    __syncthreads();
+    for (int r = tid; r < nrows; r += CF::NT) {
+      int s, x[3];
+      const int tr = decode_row(r, s, x);
+      const bool owned = T.flags[tr] & TF_OWNED;
+      const uint8_t sf = E.sflags[tr];
+      const bool shared = sf & SF_SHARED;
+      if (owned && !shared && !A.plan_mode) rlist[CF::MAXR - 1 - atomicAdd(&s_nown, 1)] = (uint16_t)r;
+      else if (shared && (owned || (sf & SF_SEND))) rlist[atomicAdd(&s_nsh, 1)] = (uint16_t)r;
+    }
+    __syncthreads();
+    const int nsh = s_nsh, nact = s_nsh + s_nown;
+    for (int ii = tid; ii < nact; ii += CF::NT) {
+      const int r = ii < nsh ? rlist[ii] : rlist[CF::MAXR - 1 - (ii - nsh)];
+      int s, x[3];
+      const int tr = decode_row(r, s, x);
+      const uint8_t fl = T.flags[tr], sf = E.sflags[tr];
+      const bool owned = fl & TF_OWNED;
+      const bool shared = sf & SF_SHARED;
+      const bool natural = shared && owned && !(sf & SF_DEFER) && !A.plan_mode;   // merged in-kernel
+      const bool rec = shared && (owned || (sf & SF_SEND)) && !natural;           // sorted record
+      const int rk = row_key<DIM, SP>(P, s, x);
+      int lb[3];
 #pragma unroll
-            for (int s2 = 0; s2 < S; ++s2) {
-              const int OFFS = (SP == SP_H1) ? 0 : s2 * (SP == SP_ND ? P * (P + 1) * (P + 1) : (P + 1) * P * P);
-              R.lb[s2] = OFFS + x[0] + ext_of<SP>(P, s2, 0) * (x[1] + ext_of<SP>(P, s2, 1) * x[2]);
+      for (int s2 = 0; s2 < S; ++s2) {
+        const int OFFS = (SP == SP_H1) ? 0 : s2 * (SP == SP_ND ? P * (P + 1) * (P + 1) : (P + 1) * P * P);
+        lb[s2] = OFFS + x[0] + ext_of<SP>(P, s2, 0) * (x[1] + ext_of<SP>(P, s2, 1) * x[2]);
+      }
+      const int lr = lb[s];
+      const int gid = gmap[lr];
+      const double sig_row = (bsg[lr] & 128) ? -1.0 : 1.0;
+      int64_t out = 0;
+      int rowlen = 0;
+      if (!natural) {
+        if (rec) {
+          const int c0 = cls_of(tr, 0), c1 = cls_of(tr, 1), c2 = DIM == 3 ? cls_of(tr, 2) : 1;
+          const int nI = (c0 == 1) + (c1 == 1) + (DIM == 3 ? (c2 == 1) : 0);
+          const int type = (nI == 0) ? 0 : (nI == DIM ? 3 : (DIM == 3 ? nI : 1));
+          out = ((int64_t)E.rec[tr] + (gid - A.base[type][T.ent[tr]])) * A.rstride;
+        } else {
+          out = ld_stream(A.row_ptr + (gid - A.row_begin), l2_policy_first());
+        }
+        // P0 of every block of the row (ascending block base order), then the final position of
+        // every stencil slot: P0 of its block + rank in the block's sub-box (per orientation code)
+        const int64_t key = (int64_t)s * NROWKEY + rk;
+        const uint4 *tz4 = reinterpret_cast<const uint4 *>(A.tabs.size + key * CF::TZS);
+        uint32_t wv[SP == SP_H1 ? 1 : W];  // slot words (H1: validity and offsets are closed-form)
+        if constexpr (SP != SP_H1) {
+#pragma unroll
+          for (int j = 0; j < W; ++j) wv[j] = __ldg(A.tabs.slot + key * W + j);
+        }
+#pragma unroll
+        for (int q = 0; q < CF::TZS / 16; ++q) {
+          const uint4 t = __ldg(tz4 + q);
+          const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int c = 0; c < 16; ++c) ts[(16 * q + c) * CF::NT] = (unsigned char)(w4[c >> 2] >> (8 * (c & 3)));
+        }
+        unsigned char *p0 = ts + CF::TZS * CF::NT;
+        if (NB <= 32) {  // all block sizes read before the first P0 store (no load-after-store chain)
+          unsigned char sz[NB <= 32 ? NB : 1];
+#pragma unroll
+          for (int i = 0; i < (NB <= 32 ? NB : 1); ++i) sz[i] = i < nb ? ts[blist[i] * CF::NT] : 0;
+#pragma unroll
+          for (int i = 0; i < (NB <= 32 ? NB : 1); ++i)
+            if (i < nb) {
+              p0[blist[i] * CF::NT] = (unsigned char)rowlen;
+              rowlen += sz[i];
             }
-            const int lr = R.lb[s];
-            const int gid = gmap[lr];
-            const double sig_row = (bsg[lr] & 128) ? -1.0 : 1.0;
-            int t_in = 0;
-            if (shared) {
-              const int c0 = cls_of(tr, 0), c1 = cls_of(tr, 1), c2 = DIM == 3 ? cls_of(tr, 2) : 1;
-              const int nI = (c0 == 1) + (c1 == 1) + (DIM == 3 ? (c2 == 1) : 0);
-              const int type = (nI == 0) ? 0 : (nI == DIM ? 3 : (DIM == 3 ? nI : 1));
-              t_in = gid - A.base[type][T.ent[tr]];
-            }
-            const int64_t recid = shared ? (int64_t)E.rec[tr] + t_in : 0;
-            // P0 of the row's blocks: the row's block-size table row (and for planned shared rows
-            // its merge-plan row) are fetched with 16-byte loads into the (still free) value row
-            uint16_t *pr = p0r + lane * NBP;
-            if (local_plan) {
-              R.mode = 4;
-              R.recid = el * CF::NDPE + lr;
+        } else {
+          for (int i = 0; i < nb; ++i) {
+            const int b = blist[i];
+            p0[b * CF::NT] = (unsigned char)rowlen;
+            rowlen += ts[b * CF::NT];
+          }
+        }
+        // every slot's P0 and rank-table load issued before any position is stored
+        unsigned char pz[W];
+        unsigned char lx[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          pz[j] = 255;
+          lx[j] = 0;
+          bool valid;
+          int s2 = 0, l;
+          if constexpr (SP == SP_H1) {
+            valid = true;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) valid = valid && (unsigned)(x[a] + h1_off<DIM>(j, a)) <= (unsigned)P;
+            l = lb[0] + h1_dl<DIM, P>(j);
+          } else {
+            valid = (wv[j] & 127) != 127;
+            s2 = (wv[j] >> 24) & 3;
+            l = (s2 == 0 ? lb[0] : (s2 == 1 ? lb[S > 1 ? 1 : 0] : lb[S > 2 ? 2 : 0])) + (int)(int8_t)(dlt[s * W + j] & 255);
+          }
+          if (valid) {
+            const int b = bsg[l] & 127;
+            pz[j] = p0[b * CF::NT];
+            lx[j] = __ldg(A.tabs.lex + ((key * W + j) << 3) + T.orient[b - 27 * s2]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < W; ++j) ts[j * CF::NT] = pz[j] == 255 ? (unsigned char)255 : (unsigned char)(pz[j] + lx[j]);
+      }
+      double acc[W];
+      switch (s) {
+        case 0: row_values<DIM, SP, P, 0, NC>(cm, x, CF::NRING, acc); break;
+        case 1: if (S > 1) row_values<DIM, SP, P, (S > 1 ? 1 : 0), NC>(cm, x, CF::NRING, acc); break;
+        default: if (S > 2) row_values<DIM, SP, P, (S > 2 ? 2 : 0), NC>(cm, x, CF::NRING, acc); break;
+      }
+      if (natural) {  // natural-order partial row (slot order), column signs applied by the merge
+        const uint64_t pl = l2_policy_last();
+        double *dst = A.nval + (el * CF::NDPE + lr) * rec_w8(W);
+#pragma unroll
+        for (int j = 0; j + 1 < W; j += 2) st_hint2(dst + j, acc[j] * sig_row, acc[j + 1] * sig_row, pl);
+        if (W & 1) st_hint(dst + W - 1, acc[W - 1] * sig_row, pl);
+      } else if (!rec) {
+        const uint64_t pf = l2_policy_first();
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const int ps = ts[j * CF::NT];
+          if (ps != 255) {
+            int l;
+            if constexpr (SP == SP_H1) {
+              l = lb[0] + h1_dl<DIM, P>(j);
             } else {
-              constexpr int TZS = tab_tzs(NB);
-              const uint4 *tz4 = reinterpret_cast<const uint4 *>(A.tabs.size + ((int64_t)s * NROWKEY + rk) * TZS);
-              uint4 *tmp4 = reinterpret_cast<uint4 *>(smem + CF::OFF_TMP + (warp * RG + lane) * CF::TMPB);
-              const uint8_t *tzs = reinterpret_cast<const uint8_t *>(tmp4);
-#pragma unroll
-              for (int q = 0; q < TZS / 16; ++q) tmp4[q] = __ldg(tz4 + q);
-              int run = 0;
-              for (int i = 0; i < nb; ++i) {
-                const int b = blist[i];
-                pr[b] = (uint16_t)(run | 0xff00);
-                run += tzs[b];
-              }
-              if (!rec) {
-                R.mode = 1;
-                R.out = A.row_ptr[gid - A.row_begin];
-              } else {
-                R.mode = 2;
-                R.out = recid * A.rstride;
-                R.recid = run;
-              }
+              const int dd = dlt[s * W + j], s2 = (dd >> 8) & 3;
+              l = (s2 == 0 ? lb[0] : (s2 == 1 ? lb[S > 1 ? 1 : 0] : lb[S > 2 ? 2 : 0])) + (int)(int8_t)(dd & 255);
             }
-            double acc[W];
-            switch (s) {
-              case 0: row_values<DIM, SP, P, 0, NC>(cm, x, CF::NRING, acc); break;
-              case 1: if (S > 1) row_values<DIM, SP, P, (S > 1 ? 1 : 0), NC>(cm, x, CF::NRING, acc); break;
-              default: if (S > 2) row_values<DIM, SP, P, (S > 2 ? 2 : 0), NC>(cm, x, CF::NRING, acc); break;
-            }
-#pragma unroll
-            for (int j = 0; j < W; ++j) vb[lane * W + j] = acc[j] * sig_row;
+            const double v = acc[j] * ((bsg[l] & 128) ? -sig_row : sig_row);
+            st_hint(A.col + out + ps, gmap[l], pf);
+            st_hint(A.val + out + ps, v, pf);
           }
         }
-        rr[lane] = R;
-      }
-      __syncwarp();
-      const int nr = (nrows - g0 < RG) ? nrows - g0 : RG;
-      // slot words of the next row are fetched while the current row is emitted
-      uint32_t wcur[(W + 31) / 32], wnext[(W + 31) / 32];
-      {
-        const RowRec &R0 = rr[0];
-        const int64_t key0 = (int64_t)R0.s * NROWKEY + R0.rk;
+      } else {  // sorted record {column | block base << 32, value (plan pass: slot | 64 if flipped)}
+        double2 *dst = reinterpret_cast<double2 *>(A.scratch) + out;
 #pragma unroll
-        for (int h = 0; h < (W + 31) / 32; ++h) {
-          const int j = h * 32 + lane;
-          wcur[h] = (j < W) ? __ldg(A.tabs.slot + key0 * W + j) : 127u;
-        }
-      }
-      for (int i = 0; i < nr; ++i) {
-        if (i + 1 < nr) {
-          const RowRec &Rn = rr[i + 1];
-          const int64_t keyn = (int64_t)Rn.s * NROWKEY + Rn.rk;
-#pragma unroll
-          for (int h = 0; h < (W + 31) / 32; ++h) {
-            const int j = h * 32 + lane;
-            wnext[h] = (j < W) ? __ldg(A.tabs.slot + keyn * W + j) : 127u;
+        for (int j = 0; j < W; ++j) {
+          const int ps = ts[j * CF::NT];
+          if (ps != 255) {
+            int l;
+            if constexpr (SP == SP_H1) {
+              l = lb[0] + h1_dl<DIM, P>(j);
+            } else {
+              const int dd = dlt[s * W + j], s2 = (dd >> 8) & 3;
+              l = (s2 == 0 ? lb[0] : (s2 == 1 ? lb[S > 1 ? 1 : 0] : lb[S > 2 ? 2 : 0])) + (int)(int8_t)(dd & 255);
+            }
+            const int bs = bsg[l];
+            const double v = acc[j] * ((bs & 128) ? -sig_row : sig_row);
+            dst[ps] = make_double2(__longlong_as_double(((long long)(unsigned)blk[bs & 127].base << 32) | (unsigned)gmap[l]),
+                                   A.plan_mode ? (double)(j | ((bs & 128) ? 64 : 0)) : v);
           }
         }
-        const RowRec &Ri = rr[i];
-        if (Ri.mode) emit_row<DIM, SP, P>(A, Ri, wcur, vb + i * W, p0r + i * NBP, blk, T, gmap, bsg, dlt, lane);
-#pragma unroll
-        for (int h = 0; h < (W + 31) / 32; ++h) wcur[h] = wnext[h];
+        dst[A.rstride - 1] = make_double2(__longlong_as_double(((long long)(unsigned)lr << 32) | (long long)(unsigned)rowlen), 0.0);
       }
-      __syncwarp();
     }
   }
   if (A.plan_mode) return;
-  // ---- arrival on shared owned entities; the last element to arrive adds up their shared values
-  __threadfence();
+  LOR_STAMP(3);
+  // ---- arrival on shared owned entities; the last element to arrive adds up their shared values.
+  // The CTA barrier orders every thread's record stores before warp 0's gpu-scope fence, which is
+  // cumulative (PTX memory model), so only the arriving warp fences.
   __syncthreads();
+  if (warp == 0 && !(A.dbg & 1)) __threadfence();
   if (tid < CF::NSLOT) {
     const int tau = tid;
     const uint8_t sf = E.sflags[tau];
@@ -809,82 +849,208 @@ __global__ void __launch_bounds__(128, 4) k_assemble(AsmArgs A) {
   }
   __syncthreads();
   const int nfin = s_fin_n;
-  if (nfin > 0) {
-    __threadfence();
-    // Emit every row of the entities whose last contributor is this element: final position q of
-    // row r takes its column from the first contributor holding it and its value from the sum over
-    // all contributors holding it, in element order (setup merge plan: contributor m's stencil slot
-    // at q, or 255).
-    __shared__ int s_fk[27], s_fnr[27], s_fpre[28];
-    __shared__ int64_t s_fpb[27];
-    __shared__ int s_felem[27 * MAX_VALENCE];
-    constexpr int MAXFR = 256;  // rows whose offsets are staged (value rows hold >= 256 * 12 B)
-    int64_t *s_rowoff = reinterpret_cast<int64_t *>(smem + CF::OFF_VB);  // value rows are free now
-    int *s_rowlen = reinterpret_cast<int *>(s_rowoff + MAXFR);
-    __shared__ int s_rpre[28];
-    for (int i = tid; i < nfin; i += blockDim.x) {
-      const Ose O = A.ose[s_fin[i]];
-      s_fk[i] = O.k;
-      s_fnr[i] = O.nrows;
-      s_fpb[i] = A.pbase[s_fin[i]];
-      for (int m = 0; m < O.k; ++m) s_felem[i * MAX_VALENCE + m] = A.ose_elem[O.slot_off + m];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int accr = 0;
-      for (int i = 0; i < nfin; ++i) { s_rpre[i] = accr; s_fpre[i] = accr * W; accr += s_fnr[i]; }
-      s_rpre[nfin] = accr;
-      s_fpre[nfin] = accr * W;
-    }
-    __syncthreads();
-    const int nfr = s_rpre[nfin];
-    {
-      int i = 0;
-      for (int rr2 = tid; rr2 < nfr && rr2 < MAXFR; rr2 += blockDim.x) {
-        while (rr2 >= s_rpre[i + 1]) ++i;
-        const int64_t g = (int64_t)A.ose[s_fin[i]].gid_base + (rr2 - s_rpre[i]) - A.row_begin;
-        const int64_t a = A.row_ptr[g];
-        s_rowoff[rr2] = a;
-        s_rowlen[rr2] = (int)(A.row_ptr[g + 1] - a);
-      }
-    }
-    __syncthreads();
-    const int total = s_fpre[nfin];
-    int i = 0;
-    for (int it = tid; it < total; it += blockDim.x) {
-      while (it >= s_fpre[i + 1]) ++i;  // items ascend per thread: amortised O(1)
-      const int rem = it - s_fpre[i];
-      const int r = rem / W, q = rem - r * W;
-      const int rg2 = s_rpre[i] + r;
-      int64_t ro;
-      int len;
-      if (rg2 < MAXFR) { ro = s_rowoff[rg2]; len = s_rowlen[rg2]; }
-      else {
-        const int64_t g = (int64_t)A.ose[s_fin[i]].gid_base + r - A.row_begin;
-        ro = A.row_ptr[g];
-        len = (int)(A.row_ptr[g + 1] - ro);
-      }
-      if (q >= len) continue;
-      const int k = s_fk[i];
-      const int rstr = ((2 * k + W * k) + 1) & ~1;
-      const uint8_t *pr = A.plan + s_fpb[i] + (int64_t)r * rstr;
-      const uint16_t *lrow = reinterpret_cast<const uint16_t *>(pr);
-      const uint8_t *js = pr + 2 * k + q * k;
-      int gid = 0;
-      bool have = false;
-      double sum = 0.0;
-      for (int m = 0; m < k; ++m) {
-        const int jm = __ldg(js + m);
-        if (jm == 255) continue;
-        const int64_t rr3 = (int64_t)s_felem[i * MAX_VALENCE + m] * CF::NDPE + __ldg(lrow + m);
-        if (!have) { gid = __ldcg(A.ngid + rr3 * rec_w4(W) + jm); have = true; }
-        sum += __ldcg(A.nval + rr3 * rec_w8(W) + jm);
-      }
-      const uint64_t pf = l2_policy_first();
-      st_hint(A.col + ro + q, gid, pf);
-      st_hint(A.val + ro + q, sum, pf);
-    }
+  LOR_STAMP(4);
+  if (A.tstamp && tid == 0) A.tstamp[(int64_t)blockIdx.x * 16 + 7] = (unsigned long long)nfin << 32 | smid_();
+  if (nfin == 0) {
+    LOR_STAMP(5);
+    return;
   }
+  if (!(A.dbg & 1)) __threadfence();
+  // Emit every row of the entities whose last contributor is this element.  Their merge-plan rows
+  // and row offsets are staged in shared memory (the cell matrices and value rows are dead now),
+  // then one thread per final column position q: the column comes from the plan, the value is the
+  // sum over the contributors holding q in element order (column sign from the plan).  The
+  // consumed records are dead afterwards and are dropped from L2 without write-back.
+  constexpr int W8 = rec_w8(W), LT = W8 / 16;
+  __shared__ int s_fk[27], s_frp[28], s_fsp[28], s_fkp[28];
+  __shared__ int64_t s_fpb[27], s_fg0[27];
+  __shared__ int s_felem[27 * MAX_VALENCE];
+  for (int i = tid; i < nfin; i += blockDim.x) {
+    const int oi = s_fin[i];
+    const Ose O = A.ose[oi];
+    s_fk[i] = O.k;
+    s_frp[i + 1] = O.nrows;
+    s_fpb[i] = A.pbase[oi];
+    s_fg0[i] = (int64_t)O.gid_base - A.row_begin;
+    for (int m = 0; m < O.k; ++m) s_felem[i * MAX_VALENCE + m] = __ldg(A.ose_elem + O.slot_off + m);
+  }
+  __syncthreads();
+  LOR_STAMP(8);
+  if (tid == 0) {
+    int rows = 0, bytes = 0, kk = 0;
+    for (int i = 0; i < nfin; ++i) {
+      const int nr = s_frp[i + 1];
+      s_frp[i] = rows;
+      s_fsp[i] = bytes;
+      s_fkp[i] = kk;
+      rows += nr;
+      bytes += nr * plan_row_bytes(s_fk[i], W);
+      kk += nr * s_fk[i];
+    }
+    s_frp[nfin] = rows;
+    s_fsp[nfin] = bytes;
+    s_fkp[nfin] = kk;
+  }
+  __syncthreads();
+  // staged per row: its CSR offset and length, plan row, and the record row of every contributor
+  struct FRow {
+    int64_t ro;
+    int32_t pofs, rbo;
+    int16_t len;
+    uint8_t k, pad;
+    int32_t pad2;
+  };
+  unsigned char *fs = smem + CF::OFF_X;
+  constexpr int AVAIL = CF::SMEM - CF::OFF_X;
+  constexpr int ROWB = (int)sizeof(FRow) + 4 * MAX_VALENCE;  // per-row staging besides the plan row
+  const int NR = s_frp[nfin];
+  auto ent_of = [&](int R, int &i) { while (R >= s_frp[i + 1]) ++i; };
+  auto bofs = [&](int R) {  // plan bytes before row R (rows of all finalized entities concatenated)
+    int i = 0;
+    ent_of(R < NR ? R : NR - 1, i);
+    return s_fsp[i] + (R - s_frp[i]) * plan_row_bytes(s_fk[i], W);
+  };
+  int R0 = 0;
+  while (R0 < NR) {
+    // largest batch of rows whose plan rows + row data fit the staging area
+    const int b0 = bofs(R0);
+    int R1 = NR;
+    if (s_fsp[nfin] - b0 + ROWB * (NR - R0) + 16 > AVAIL) {
+      R1 = R0 + 1;
+      while (R1 < NR && bofs(R1 + 1) - b0 + ROWB * (R1 + 1 - R0) + 16 <= AVAIL) ++R1;
+    }
+    const int nbytes = bofs(R1) - b0;
+    FRow *srow = reinterpret_cast<FRow *>(fs);
+    int32_t *sbase = reinterpret_cast<int32_t *>(srow + (R1 - R0));
+    unsigned char *splan = reinterpret_cast<unsigned char *>(sbase + MAX_VALENCE * (R1 - R0));
+    splan += (16 - ((uintptr_t)splan & 15)) & 15;
+    {
+      // 16-byte copies, four in flight per thread
+      const int n16 = nbytes / 16;
+      for (int w0 = 0; w0 < n16; w0 += 4 * 128) {
+        uint4 t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int w = w0 + u * 128 + tid;
+          if (w < n16) {
+            const int byte = b0 + 16 * w;
+            int i = 0;
+            while (byte >= s_fsp[i + 1]) ++i;
+            t[u] = ld_stream(reinterpret_cast<const uint4 *>(A.plan + s_fpb[i] + (byte - s_fsp[i])), l2_policy_first());
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int w = w0 + u * 128 + tid;
+          if (w < n16) reinterpret_cast<uint4 *>(splan)[w] = t[u];
+        }
+      }
+      // one thread per row: offsets, and the contributors' record rows (read from the plan in HBM
+      // while the copy above is in flight)
+      int i = 0;
+      const int kb0 = [&] { int i0 = 0; ent_of(R0, i0); return s_fkp[i0] + (R0 - s_frp[i0]) * s_fk[i0]; }();
+      for (int R = R0 + tid; R < R1; R += blockDim.x) {
+        ent_of(R, i);
+        const int k = s_fk[i], r = R - s_frp[i];
+        const int64_t g = s_fg0[i] + r;
+        const uint64_t pf = l2_policy_first();
+        const int64_t a = ld_stream(A.row_ptr + g, pf);
+        const int64_t e = ld_stream(A.row_ptr + g + 1, pf);
+        FRow F;
+        F.ro = a;
+        F.len = (int16_t)(e - a);
+        F.k = (uint8_t)k;
+        F.pofs = s_fsp[i] + r * plan_row_bytes(k, W) - b0;
+        F.rbo = s_fkp[i] + r * k - kb0;
+        F.pad = 0;
+        F.pad2 = 0;
+        srow[R - R0] = F;
+        const uint16_t *lrow = reinterpret_cast<const uint16_t *>(A.plan + s_fpb[i] + (int64_t)r * plan_row_bytes(k, W));
+        for (int m = 0; m < k; ++m) sbase[F.rbo + m] = s_felem[i * MAX_VALENCE + m] * CF::NDPE + __ldg(lrow + m);
+      }
+    }
+    __syncthreads();
+    LOR_STAMP(9);
+    {
+      // four items per thread in flight, up to four holders each: all their record loads are
+      // issued before the first use (the rare fifth+ holder is added afterwards, in order)
+      const int nit = (R1 - R0) * W;
+      for (int it0 = 0; it0 < nit; it0 += 4 * CF::NT) {
+        if (it0 < 3 * 4 * CF::NT) LOR_STAMP(11 + it0 / (4 * CF::NT));
+        double xv[4][4];
+        int gid[4];
+        int64_t dsto[4];
+        unsigned rest[4];
+        const unsigned char *jsb[4];
+        const int32_t *rbb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int it = it0 + u * CF::NT + tid;
+          dsto[u] = -1;
+          gid[u] = 0;
+          rest[u] = 0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) xv[u][m] = 0.0;
+          if (it >= nit) continue;
+          const int Rl = it / W, q = it - Rl * W;
+          const FRow &F = srow[Rl];
+          if (q >= F.len) continue;
+          const int k = F.k, coff = plan_col_off(k, W);
+          const unsigned char *pr = splan + F.pofs;
+          unsigned hm = reinterpret_cast<const uint16_t *>(pr)[k + q];
+          gid[u] = reinterpret_cast<const int32_t *>(pr + coff)[q];
+          dsto[u] = F.ro + q;
+          const unsigned char *js = pr + coff + 4 * W + q * k;
+          const int32_t *rb = sbase + F.rbo;
+#pragma unroll
+          for (int m4 = 0; m4 < 4; ++m4) {
+            if (hm) {
+              const int m = __ffs(hm) - 1;
+              hm &= hm - 1;
+              const int jm = js[m];
+              const double x = A.nval[(int64_t)rb[m] * W8 + (jm & 63)];
+              xv[u][m4] = (jm & 64) ? -x : x;
+            }
+          }
+          rest[u] = hm;
+          jsb[u] = js;
+          rbb[u] = rb;
+        }
+        const uint64_t pf = l2_policy_first();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double sum = ((xv[u][0] + xv[u][1]) + xv[u][2]) + xv[u][3];
+          unsigned hm = rest[u];
+          while (hm) {
+            const int m = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const int jm = jsb[u][m];
+            const double x = A.nval[(int64_t)rbb[u][m] * W8 + (jm & 63)];
+            sum += (jm & 64) ? -x : x;
+          }
+          if (dsto[u] >= 0) {
+            st_hint(A.col + dsto[u], gid[u], pf);
+            st_hint(A.val + dsto[u], sum, pf);
+          }
+        }
+      }
+    }
+    LOR_STAMP(14);
+    __syncthreads();
+    LOR_STAMP(10);
+    // the consumed records are dead: drop their lines from L2 without write-back
+    for (int it = tid; it < (R1 - R0) * MAX_VALENCE; it += blockDim.x) {
+      const int Rl = it / MAX_VALENCE, m = it - Rl * MAX_VALENCE;
+      const FRow &F = srow[Rl];
+      if (m >= F.k) continue;
+      const char *rec = reinterpret_cast<const char *>(A.nval + (int64_t)sbase[F.rbo + m] * W8);
+#pragma unroll
+      for (int ln = 0; ln < LT; ++ln) asm volatile("discard.global.L2 [%0], 128;" ::"l"(rec + 128 * ln) : "memory");
+    }
+    __syncthreads();
+    R0 = R1;
+  }
+  LOR_STAMP(5);
 }
 
 template <int DIM, int SP, int P, int KZ>
@@ -893,14 +1059,20 @@ cudaError_t launch_asm_p(const AsmArgs &a, int quad, cudaStream_t st, int *smem_
   const int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
+  // dev experiment: LOR_MINB=8 selects the 8-CTA/SM register budget for the 3D H1 vertex kernel
+  static const int minb = getenv("LOR_MINB") ? atoi(getenv("LOR_MINB")) : 4;
+  // dev experiment: LOR_SMEM_PAD inflates the dynamic shared memory to cap CTAs per SM
+  static const int pad = getenv("LOR_SMEM_PAD") ? atoi(getenv("LOR_SMEM_PAD")) : 0;
+  auto run = [&](auto k) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + pad);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    k<<<(unsigned)a.nel_local, 128, smem + pad, st>>>(a);
+  };
   if (quad == 0) {
-    auto k = k_assemble<DIM, SP, P, 0, KZ>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<<<(unsigned)a.nel_local, 128, smem, st>>>(a);
+    if (DIM == 3 && SP == SP_H1 && minb == 8) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 8 : 4>);
+    else run(k_assemble<DIM, SP, P, 0, KZ, 4>);
   } else {
-    auto k = k_assemble<DIM, SP, P, 1, KZ>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<<<(unsigned)a.nel_local, 128, smem, st>>>(a);
+    run(k_assemble<DIM, SP, P, 1, KZ, 4>);
   }
   return cudaGetLastError();
 }

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -82,7 +83,7 @@ struct SpaceDev {
   int W = 0;
   // shared rows: natural-order partial rows and the setup merge plan
   double *nval = nullptr;
-  int32_t *ngid = nullptr, *ose_elem = nullptr;
+  int32_t *ose_elem = nullptr;
   int64_t *pbase = nullptr;
   uint8_t *plan = nullptr, *is_defer = nullptr;
 };
@@ -99,6 +100,7 @@ struct lor_ctx_s {
   int64_t xstride = 0;
   SpaceDev sp[3];
   int *err = nullptr;
+  unsigned long long *tstamp = nullptr;  // per-CTA phase clocks of the last element pass (debug)
   ncclComm_t comm = nullptr;
   int exchange_mode = 0;  // 0 NCCL, 1 manual
   std::string last_error;
@@ -242,7 +244,6 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.ose_slots = S.ose_slots;
   a.counters = S.counters;
   a.nval = S.nval;
-  a.ngid = S.ngid;
   a.ose_elem = S.ose_elem;
   a.pbase = S.pbase;
   a.plan = S.plan;
@@ -251,6 +252,8 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.alpha = alpha;
   a.beta = beta;
   a.err = c->err;
+  a.tstamp = c->tstamp;
+  a.dbg = getenv("LOR_DBG") ? atoi(getenv("LOR_DBG")) : 0;
   CUDA_TRY(c, launch_assemble(c->dim, s, c->p, (int)quad, a, c->stream, nullptr));
   if (c->nel_local > 0) c->launches++;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
@@ -381,7 +384,9 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     for (int64_t e = 0; e < plan.nel_local; ++e) memcpy(&padded[e * c->xstride], src + e * raw, sizeof(double) * raw);
     // locality-preserving processing order: Morton code of element centroids (neighbours of an
     // element are processed close in time, so partial rows are merged while still in L2)
-    {
+    const char *ord_env = getenv("LOR_ORDER");  // dev experiments: "natural", "sweep" (default Morton)
+    const bool sweep = ord_env && !strcmp(ord_env, "sweep");
+    if (!(ord_env && !strcmp(ord_env, "natural"))) {
       const int64_t n = plan.nel_local;
       std::vector<double> cen((size_t)n * 3, 0.0);
       double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -402,8 +407,12 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
           const double t = hi[d] > lo[d] ? (cen[e * 3 + d] - lo[d]) / (hi[d] - lo[d]) : 0.0;
           qd[d] = (uint32_t)std::min(1023.0, std::max(0.0, t * 1023.0 + 0.5));
         }
-        for (int bit = 9; bit >= 0; --bit)
-          for (int d = A.dim - 1; d >= 0; --d) code = (code << 1) | ((qd[d] >> bit) & 1u);
+        if (sweep) {  // plane sweep: z, then y, then x
+          for (int d = A.dim - 1; d >= 0; --d) code = (code << 10) | qd[d];
+        } else {
+          for (int bit = 9; bit >= 0; --bit)
+            for (int d = A.dim - 1; d >= 0; --d) code = (code << 1) | ((qd[d] >> bit) & 1u);
+        }
         key[e] = {code, (int32_t)e};
       }
       std::stable_sort(key.begin(), key.end(),
@@ -416,6 +425,9 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
   }
   if (dev_upload(c, &c->topo, plan.topo.data(), plan.topo.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "topo");
   if (dev_alloc(c, &c->err, 4) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "err");
+  if (getenv("LOR_PHASE_TIMING") && c->nel_local > 0 &&
+      dev_alloc(c, &c->tstamp, (size_t)c->nel_local * 16) != cudaSuccess)
+    return bail(LOR_ERR_OUT_OF_MEMORY, "tstamp");
   for (int i = 0; i < 8; ++i) cudaEventCreate(&c->ev[i]);
   int max_smem = 0;
   for (int s = 0; s < 3; ++s) {
@@ -508,7 +520,7 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     for (size_t i = 0; i < P.ose.size(); ++i) {
       pb[i] = nbytes;
       const int k = P.ose[i].k;
-      nbytes += (int64_t)P.ose[i].nrows * (((2 * k + S.W * k) + 1) & ~1);
+      nbytes += (int64_t)P.ose[i].nrows * plan_row_bytes(k, S.W);
     }
     for (int32_t d : P.defer) isdef[d] = 1;
     for (size_t i = 0; i < oel.size(); ++i) oel[i] = (int32_t)(P.ose_elem[i] - plan.elem_begin);
@@ -517,8 +529,7 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
         dev_upload(c, &S.is_defer, isdef.data(), isdef.size()) != cudaSuccess ||
         dev_upload(c, &S.ose_elem, oel.data(), oel.size()) != cudaSuccess ||
         dev_alloc(c, &S.plan, (size_t)std::max<int64_t>(nbytes, 16)) != cudaSuccess ||
-        dev_alloc(c, &S.nval, (size_t)c->nel_local * ndpe_asm * ((S.W + 3) / 4 * 4)) != cudaSuccess ||
-        dev_alloc(c, &S.ngid, (size_t)c->nel_local * ndpe_asm * ((S.W + 7) / 8 * 8)) != cudaSuccess)
+        dev_alloc(c, &S.nval, (size_t)c->nel_local * ndpe_asm * ((S.W + 15) / 16 * 16)) != cudaSuccess)
       return bail(LOR_ERR_OUT_OF_MEMORY, "plan");
     AsmArgs a{};
     a.order = c->order;
@@ -747,6 +758,7 @@ int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int
   const void *src = nullptr;
   if (what == 0) { bytes = tab_slot_entries(c->dim, space) * 4; src = S.tslot; }
   else if (what == 1) { bytes = tab_size_entries(c->dim, space); src = S.tsize; }
+  else if (what == 2 && c->tstamp) { bytes = c->nel_local * 16 * 8; src = c->tstamp; }
   else return 0;
   if (bytes > cap) return 0;
   cudaSetDevice(c->device);

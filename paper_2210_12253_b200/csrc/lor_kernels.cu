@@ -295,11 +295,14 @@ __global__ void k_plan_merge(PlanArgs A) {
   if (oi >= A.n || A.is_defer[oi]) return;
   const Ose O = A.ose[oi];
   const int k = O.k, W = A.W;
-  const int rstr = ((2 * k + W * k) + 1) & ~1;
+  const int rstr = plan_row_bytes(k, W);
   for (int r = threadIdx.x; r < O.nrows; r += blockDim.x) {
     uint8_t *pr = A.plan + A.pbase[oi] + (int64_t)r * rstr;
     uint16_t *lrow = reinterpret_cast<uint16_t *>(pr);
-    uint8_t *js = pr + 2 * k;
+    uint16_t *hm = lrow + k;
+    int32_t *cq = reinterpret_cast<int32_t *>(pr + plan_col_off(k, W));
+    uint8_t *js = pr + plan_col_off(k, W) + 4 * W;
+    for (int i = 0; i < W; ++i) { hm[i] = 0; cq[i] = -1; }
     for (int i = 0; i < W * k; ++i) js[i] = 255;
     int64_t rid[MAX_VALENCE];
     int len[MAX_VALENCE], ptr[MAX_VALENCE];
@@ -325,7 +328,12 @@ __global__ void k_plan_merge(PlanArgs A) {
         int e = ptr[m];
         while (e < len[m] && A.scratch[rid[m] + e].bbase == minb) {
           const int q = P + (e - ptr[m]);
-          if (q < W) js[q * k + m] = (uint8_t)(int)A.scratch[rid[m] + e].val;
+          if (q < W) {
+            const RecEntry &re = A.scratch[rid[m] + e];
+            js[q * k + m] = (uint8_t)(int)re.val;
+            if (!hm[q]) cq[q] = re.col;
+            hm[q] |= (uint16_t)(1u << m);
+          }
           ++e;
         }
         size = e - ptr[m];

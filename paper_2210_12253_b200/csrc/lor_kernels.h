@@ -17,6 +17,13 @@ namespace lorb {
 //   pb[NB], npb : compact list of present blocks: b' | tau_J << 7 | size << 12
 constexpr int NROWKEY = 729;
 // byte stride of a row of the block-size table (16-byte aligned rows for vector loads)
+// merge plan row of a shared entity with k contributors, per final column position q:
+// [k x u16 contributor-local row][W x u16 holder mask over contributors] (pad to 4 B)
+// [W x i32 global column][W x k u8: slot j of q in holder m's natural record | 64 if the column
+// dof is sign-flipped in m (255 none)] (pad to 16 B: plan rows are staged with 16-byte loads)
+__host__ __device__ constexpr int plan_col_off(int k, int W) { return (2 * k + 2 * W + 3) & ~3; }
+__host__ __device__ constexpr int plan_row_bytes(int k, int W) { return (plan_col_off(k, W) + 4 * W + W * k + 15) & ~15; }
+
 __host__ __device__ constexpr int tab_tzs(int nb) { return (nb + 15) / 16 * 16; }
 struct Tabs {
   const uint32_t *slot;
@@ -57,8 +64,7 @@ struct AsmArgs {
   int32_t *counters;
   // shared rows whose contributors are all local: every contributor
   // writes its partial row in natural stencil-slot order; the last one to arrive emits the row
-  double *nval;                  // [nel_local][NDPE][W] partial values (orientation signs applied)
-  int32_t *ngid;                 // [nel_local][NDPE][W] their global column ids
+  double *nval;                  // [nel_local][NDPE][rec_w8(W)] natural-order partial rows (row sign applied)
   const int32_t *ose_elem;       // per OSE slot (ose_slots order): local index of the contributing element
   const int64_t *pbase;          // [n_ose] byte offset of the OSE's merge-plan rows
   const uint8_t *plan;           // per OSE row: k x uint16 contributor local rows, then W x k slot bytes
@@ -66,6 +72,8 @@ struct AsmArgs {
   int plan_mode;                 // 1: setup plan pass (partial-row records of every shared row, no CSR output)
   double alpha, beta;
   int *err;                      // [0] code, [1] element, [2] cell
+  unsigned long long *tstamp;    // optional [grid][16] per-CTA phase clocks (LOR_PHASE_TIMING=1)
+  int dbg;                       // dev experiments (LOR_DBG bits; 0 in production)
 };
 
 struct PlanArgs {
