@@ -165,8 +165,9 @@ lor_status lor_nccl_get_unique_id(void *out128);
 /* Number of this library's kernels launched on the context since setup (instrumentation). */
 int64_t lor_kernel_launches(lor_ctx ctx);
 
-/* Per-phase device timing of the last assembly call in milliseconds (count, scan, element,
- * exchange+finalize); valid after lor_sync.  Returns number of phases written (<= 8). */
+/* Per-phase device timing of the last assembly call in milliseconds (count+scan, element pass
+ * k_assemble, merge pass k_merge_rows, exchange+finalize); valid after lor_sync.  Returns number of
+ * phases written (<= 8). */
 int lor_last_phase_ms(lor_ctx ctx, float *ms, int cap);
 
 #ifdef __cplusplus

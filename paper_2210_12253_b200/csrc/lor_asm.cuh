@@ -178,7 +178,7 @@ struct AsmCfg {
   static constexpr int NW = 4;                                    // warps per CTA
   static constexpr int NT = NW * 32;
   static constexpr int TZS = tab_tzs(NB);                         // block-size table row (bytes)
-  static constexpr int TSB = TZS + (NB + 15) / 16 * 16;           // per-thread row scratch: sizes/positions | P0
+  static constexpr int TSB = TZS + (NB + 15) / 16 * 16;           // per-thread row scratch: sizes -> positions | P0
   // shared memory layout (bytes); everything from OFF_X on is reused by the finalizer
   static constexpr int OFF_BLK = 0;
   static constexpr int OFF_OS = OFF_BLK + NB * (int)sizeof(Blk);            // ordsig[NB] uint16
@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
         } else {
           out = ld_stream(A.row_ptr + (gid - A.row_begin), l2_policy_first());
         }
+        LOR_TSTAMP(ii == nsh, 11);
         // P0 of every block of the row (ascending block base order), then the final position of
         // every stencil slot: P0 of its block + rank in the block's sub-box (per orientation code)
         const int64_t key = (int64_t)s * NROWKEY + rk;
@@ -772,6 +773,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
         }
 #pragma unroll
         for (int j = 0; j < W; ++j) ts[j * CF::NT] = pz[j] == 255 ? (unsigned char)255 : (unsigned char)(pz[j] + lx[j]);
+        LOR_TSTAMP(ii == nsh, 12);
       }
       double acc[W];
       switch (s) {
@@ -779,12 +781,12 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
         case 1: if (S > 1) row_values<DIM, SP, P, (S > 1 ? 1 : 0), NC>(cm, x, CF::NRING, acc); break;
         default: if (S > 2) row_values<DIM, SP, P, (S > 2 ? 2 : 0), NC>(cm, x, CF::NRING, acc); break;
       }
+      LOR_TSTAMP(ii == nsh, 13);
       if (natural) {  // natural-order partial row (slot order), column signs applied by the merge
-        const uint64_t pl = l2_policy_last();
-        double *dst = A.nval + (el * CF::NDPE + lr) * rec_w8(W);
+        double2 *dst = reinterpret_cast<double2 *>(A.nval + (el * CF::NDPE + lr) * rec_w8(W));
 #pragma unroll
-        for (int j = 0; j + 1 < W; j += 2) st_hint2(dst + j, acc[j] * sig_row, acc[j + 1] * sig_row, pl);
-        if (W & 1) st_hint(dst + W - 1, acc[W - 1] * sig_row, pl);
+        for (int j = 0; j + 1 < W; j += 2) dst[j / 2] = make_double2(acc[j] * sig_row, acc[j + 1] * sig_row);
+        if (W & 1) A.nval[(el * CF::NDPE + lr) * rec_w8(W) + W - 1] = acc[W - 1] * sig_row;
       } else if (!rec) {
         const uint64_t pf = l2_policy_first();
 #pragma unroll
@@ -803,6 +805,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
             st_hint(A.val + out + ps, v, pf);
           }
         }
+        LOR_TSTAMP(ii == nsh, 14);
       } else {  // sorted record {column | block base << 32, value (plan pass: slot | 64 if flipped)}
         double2 *dst = reinterpret_cast<double2 *>(A.scratch) + out;
 #pragma unroll
@@ -826,231 +829,12 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
       }
     }
   }
-  if (A.plan_mode) return;
-  LOR_STAMP(3);
-  // ---- arrival on shared owned entities; the last element to arrive adds up their shared values.
-  // The CTA barrier orders every thread's record stores before warp 0's gpu-scope fence, which is
-  // cumulative (PTX memory model), so only the arriving warp fences.
-  __syncthreads();
-  if (warp == 0 && !(A.dbg & 1)) __threadfence();
-  if (tid < CF::NSLOT) {
-    const int tau = tid;
-    const uint8_t sf = E.sflags[tau];
-    if ((sf & SF_SHARED) && !(sf & (SF_DEFER | SF_SEND)) && E.ose[tau] >= 0) {
-      const int oi = E.ose[tau];
-      const int kk = A.ose[oi].k;
-      const int old = atomicAdd(A.counters + oi, 1);
-      if (old == kk - 1) {
-        A.counters[oi] = 0;
-        const int pos = atomicAdd(&s_fin_n, 1);
-        s_fin[pos] = oi;
-      }
-    }
-  }
-  __syncthreads();
-  const int nfin = s_fin_n;
-  LOR_STAMP(4);
-  if (A.tstamp && tid == 0) A.tstamp[(int64_t)blockIdx.x * 16 + 7] = (unsigned long long)nfin << 32 | smid_();
-  if (nfin == 0) {
-    LOR_STAMP(5);
-    return;
-  }
-  if (!(A.dbg & 1)) __threadfence();
-  // Emit every row of the entities whose last contributor is this element.  Their merge-plan rows
-  // and row offsets are staged in shared memory (the cell matrices and value rows are dead now),
-  // then one thread per final column position q: the column comes from the plan, the value is the
-  // sum over the contributors holding q in element order (column sign from the plan).  The
-  // consumed records are dead afterwards and are dropped from L2 without write-back.
-  constexpr int W8 = rec_w8(W), LT = W8 / 16;
-  __shared__ int s_fk[27], s_frp[28], s_fsp[28], s_fkp[28];
-  __shared__ int64_t s_fpb[27], s_fg0[27];
-  __shared__ int s_felem[27 * MAX_VALENCE];
-  for (int i = tid; i < nfin; i += blockDim.x) {
-    const int oi = s_fin[i];
-    const Ose O = A.ose[oi];
-    s_fk[i] = O.k;
-    s_frp[i + 1] = O.nrows;
-    s_fpb[i] = A.pbase[oi];
-    s_fg0[i] = (int64_t)O.gid_base - A.row_begin;
-    for (int m = 0; m < O.k; ++m) s_felem[i * MAX_VALENCE + m] = __ldg(A.ose_elem + O.slot_off + m);
-  }
-  __syncthreads();
-  LOR_STAMP(8);
-  if (tid == 0) {
-    int rows = 0, bytes = 0, kk = 0;
-    for (int i = 0; i < nfin; ++i) {
-      const int nr = s_frp[i + 1];
-      s_frp[i] = rows;
-      s_fsp[i] = bytes;
-      s_fkp[i] = kk;
-      rows += nr;
-      bytes += nr * plan_row_bytes(s_fk[i], W);
-      kk += nr * s_fk[i];
-    }
-    s_frp[nfin] = rows;
-    s_fsp[nfin] = bytes;
-    s_fkp[nfin] = kk;
-  }
-  __syncthreads();
-  // staged per row: its CSR offset and length, plan row, and the record row of every contributor
-  struct FRow {
-    int64_t ro;
-    int32_t pofs, rbo;
-    int16_t len;
-    uint8_t k, pad;
-    int32_t pad2;
-  };
-  unsigned char *fs = smem + CF::OFF_X;
-  constexpr int AVAIL = CF::SMEM - CF::OFF_X;
-  constexpr int ROWB = (int)sizeof(FRow) + 4 * MAX_VALENCE;  // per-row staging besides the plan row
-  const int NR = s_frp[nfin];
-  auto ent_of = [&](int R, int &i) { while (R >= s_frp[i + 1]) ++i; };
-  auto bofs = [&](int R) {  // plan bytes before row R (rows of all finalized entities concatenated)
-    int i = 0;
-    ent_of(R < NR ? R : NR - 1, i);
-    return s_fsp[i] + (R - s_frp[i]) * plan_row_bytes(s_fk[i], W);
-  };
-  int R0 = 0;
-  while (R0 < NR) {
-    // largest batch of rows whose plan rows + row data fit the staging area
-    const int b0 = bofs(R0);
-    int R1 = NR;
-    if (s_fsp[nfin] - b0 + ROWB * (NR - R0) + 16 > AVAIL) {
-      R1 = R0 + 1;
-      while (R1 < NR && bofs(R1 + 1) - b0 + ROWB * (R1 + 1 - R0) + 16 <= AVAIL) ++R1;
-    }
-    const int nbytes = bofs(R1) - b0;
-    FRow *srow = reinterpret_cast<FRow *>(fs);
-    int32_t *sbase = reinterpret_cast<int32_t *>(srow + (R1 - R0));
-    unsigned char *splan = reinterpret_cast<unsigned char *>(sbase + MAX_VALENCE * (R1 - R0));
-    splan += (16 - ((uintptr_t)splan & 15)) & 15;
-    {
-      // 16-byte copies, four in flight per thread
-      const int n16 = nbytes / 16;
-      for (int w0 = 0; w0 < n16; w0 += 4 * 128) {
-        uint4 t[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int w = w0 + u * 128 + tid;
-          if (w < n16) {
-            const int byte = b0 + 16 * w;
-            int i = 0;
-            while (byte >= s_fsp[i + 1]) ++i;
-            t[u] = ld_stream(reinterpret_cast<const uint4 *>(A.plan + s_fpb[i] + (byte - s_fsp[i])), l2_policy_first());
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int w = w0 + u * 128 + tid;
-          if (w < n16) reinterpret_cast<uint4 *>(splan)[w] = t[u];
-        }
-      }
-      // one thread per row: offsets, and the contributors' record rows (read from the plan in HBM
-      // while the copy above is in flight)
-      int i = 0;
-      const int kb0 = [&] { int i0 = 0; ent_of(R0, i0); return s_fkp[i0] + (R0 - s_frp[i0]) * s_fk[i0]; }();
-      for (int R = R0 + tid; R < R1; R += blockDim.x) {
-        ent_of(R, i);
-        const int k = s_fk[i], r = R - s_frp[i];
-        const int64_t g = s_fg0[i] + r;
-        const uint64_t pf = l2_policy_first();
-        const int64_t a = ld_stream(A.row_ptr + g, pf);
-        const int64_t e = ld_stream(A.row_ptr + g + 1, pf);
-        FRow F;
-        F.ro = a;
-        F.len = (int16_t)(e - a);
-        F.k = (uint8_t)k;
-        F.pofs = s_fsp[i] + r * plan_row_bytes(k, W) - b0;
-        F.rbo = s_fkp[i] + r * k - kb0;
-        F.pad = 0;
-        F.pad2 = 0;
-        srow[R - R0] = F;
-        const uint16_t *lrow = reinterpret_cast<const uint16_t *>(A.plan + s_fpb[i] + (int64_t)r * plan_row_bytes(k, W));
-        for (int m = 0; m < k; ++m) sbase[F.rbo + m] = s_felem[i * MAX_VALENCE + m] * CF::NDPE + __ldg(lrow + m);
-      }
-    }
+  // shared rows are merged by the separate pass k_merge_rows (lor_kernels.cu)
+  if (A.tstamp) {
+    LOR_STAMP(3);  // thread 0 done
     __syncthreads();
-    LOR_STAMP(9);
-    {
-      // four items per thread in flight, up to four holders each: all their record loads are
-      // issued before the first use (the rare fifth+ holder is added afterwards, in order)
-      const int nit = (R1 - R0) * W;
-      for (int it0 = 0; it0 < nit; it0 += 4 * CF::NT) {
-        if (it0 < 3 * 4 * CF::NT) LOR_STAMP(11 + it0 / (4 * CF::NT));
-        double xv[4][4];
-        int gid[4];
-        int64_t dsto[4];
-        unsigned rest[4];
-        const unsigned char *jsb[4];
-        const int32_t *rbb[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int it = it0 + u * CF::NT + tid;
-          dsto[u] = -1;
-          gid[u] = 0;
-          rest[u] = 0;
-#pragma unroll
-          for (int m = 0; m < 4; ++m) xv[u][m] = 0.0;
-          if (it >= nit) continue;
-          const int Rl = it / W, q = it - Rl * W;
-          const FRow &F = srow[Rl];
-          if (q >= F.len) continue;
-          const int k = F.k, coff = plan_col_off(k, W);
-          const unsigned char *pr = splan + F.pofs;
-          unsigned hm = reinterpret_cast<const uint16_t *>(pr)[k + q];
-          gid[u] = reinterpret_cast<const int32_t *>(pr + coff)[q];
-          dsto[u] = F.ro + q;
-          const unsigned char *js = pr + coff + 4 * W + q * k;
-          const int32_t *rb = sbase + F.rbo;
-#pragma unroll
-          for (int m4 = 0; m4 < 4; ++m4) {
-            if (hm) {
-              const int m = __ffs(hm) - 1;
-              hm &= hm - 1;
-              const int jm = js[m];
-              const double x = A.nval[(int64_t)rb[m] * W8 + (jm & 63)];
-              xv[u][m4] = (jm & 64) ? -x : x;
-            }
-          }
-          rest[u] = hm;
-          jsb[u] = js;
-          rbb[u] = rb;
-        }
-        const uint64_t pf = l2_policy_first();
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          double sum = ((xv[u][0] + xv[u][1]) + xv[u][2]) + xv[u][3];
-          unsigned hm = rest[u];
-          while (hm) {
-            const int m = __ffs(hm) - 1;
-            hm &= hm - 1;
-            const int jm = jsb[u][m];
-            const double x = A.nval[(int64_t)rbb[u][m] * W8 + (jm & 63)];
-            sum += (jm & 64) ? -x : x;
-          }
-          if (dsto[u] >= 0) {
-            st_hint(A.col + dsto[u], gid[u], pf);
-            st_hint(A.val + dsto[u], sum, pf);
-          }
-        }
-      }
-    }
-    LOR_STAMP(14);
-    __syncthreads();
-    LOR_STAMP(10);
-    // the consumed records are dead: drop their lines from L2 without write-back
-    for (int it = tid; it < (R1 - R0) * MAX_VALENCE; it += blockDim.x) {
-      const int Rl = it / MAX_VALENCE, m = it - Rl * MAX_VALENCE;
-      const FRow &F = srow[Rl];
-      if (m >= F.k) continue;
-      const char *rec = reinterpret_cast<const char *>(A.nval + (int64_t)sbase[F.rbo + m] * W8);
-#pragma unroll
-      for (int ln = 0; ln < LT; ++ln) asm volatile("discard.global.L2 [%0], 128;" ::"l"(rec + 128 * ln) : "memory");
-    }
-    __syncthreads();
-    R0 = R1;
+    LOR_STAMP(4);  // CTA done
   }
-  LOR_STAMP(5);
 }
 
 template <int DIM, int SP, int P, int KZ>
@@ -1059,8 +843,8 @@ cudaError_t launch_asm_p(const AsmArgs &a, int quad, cudaStream_t st, int *smem_
   const int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
-  // dev experiment: LOR_MINB=8 selects the 8-CTA/SM register budget for the 3D H1 vertex kernel
-  static const int minb = getenv("LOR_MINB") ? atoi(getenv("LOR_MINB")) : 4;
+  // 3D H1 vertex rule: 6 CTAs/SM (80 registers) measured fastest at C2; LOR_MINB=4/5/8 for experiments
+  static const int minb = getenv("LOR_MINB") ? atoi(getenv("LOR_MINB")) : 6;
   // dev experiment: LOR_SMEM_PAD inflates the dynamic shared memory to cap CTAs per SM
   static const int pad = getenv("LOR_SMEM_PAD") ? atoi(getenv("LOR_SMEM_PAD")) : 0;
   auto run = [&](auto k) {
@@ -1070,6 +854,8 @@ cudaError_t launch_asm_p(const AsmArgs &a, int quad, cudaStream_t st, int *smem_
   };
   if (quad == 0) {
     if (DIM == 3 && SP == SP_H1 && minb == 8) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 8 : 4>);
+    else if (DIM == 3 && SP == SP_H1 && minb == 6) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 6 : 4>);
+    else if (DIM == 3 && SP == SP_H1 && minb == 5) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 5 : 4>);
     else run(k_assemble<DIM, SP, P, 0, KZ, 4>);
   } else {
     run(k_assemble<DIM, SP, P, 1, KZ, 4>);

@@ -71,6 +71,8 @@ struct SpaceDev {
   Ose *ose = nullptr;
   int32_t *ose_slots = nullptr, *counters = nullptr, *defer = nullptr;
   int n_ose = 0, n_defer = 0;
+  MergeRow *mrows = nullptr;  // merge-pass rows
+  int64_t n_mrows = 0;
   RecEntry *scratch = nullptr;
   int64_t n_records = 0;
   int32_t *cnt = nullptr;
@@ -256,6 +258,21 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.dbg = getenv("LOR_DBG") ? atoi(getenv("LOR_DBG")) : 0;
   CUDA_TRY(c, launch_assemble(c->dim, s, c->p, (int)quad, a, c->stream, nullptr));
   if (c->nel_local > 0) c->launches++;
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  if (S.n_mrows > 0) {  // shared rows whose contributors are all local: merge pass
+    MergeArgs m{};
+    m.n = S.n_mrows;
+    m.W = S.W;
+    m.W8 = (S.W + 15) / 16 * 16;
+    m.rows = S.mrows;
+    m.plan = S.plan;
+    m.nval = S.nval;
+    m.row_ptr = out->row_ptr;
+    m.col = out->col;
+    m.val = out->val;
+    CUDA_TRY(c, launch_merge_rows(m, c->stream));
+    c->launches++;
+  }
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   if (c->nranks > 1) {
     if (c->exchange_mode == 1) {
@@ -524,6 +541,15 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     }
     for (int32_t d : P.defer) isdef[d] = 1;
     for (size_t i = 0; i < oel.size(); ++i) oel[i] = (int32_t)(P.ose_elem[i] - plan.elem_begin);
+    std::vector<MergeRow> mr;
+    for (size_t i = 0; i < P.ose.size(); ++i) {
+      if (isdef[i]) continue;
+      const int k = P.ose[i].k;
+      for (int r = 0; r < P.ose[i].nrows; ++r)
+        mr.push_back(MergeRow{pb[i] + (int64_t)r * plan_row_bytes(k, S.W), (int32_t)(P.ose[i].gid_base + r - S.row_begin), k});
+    }
+    S.n_mrows = (int64_t)mr.size();
+    if (dev_upload(c, &S.mrows, mr.data(), mr.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "mrows");
     const int ndpe_asm = S.ndpe;
     if (dev_upload(c, &S.pbase, pb.data(), pb.size()) != cudaSuccess ||
         dev_upload(c, &S.is_defer, isdef.data(), isdef.size()) != cudaSuccess ||
@@ -563,6 +589,8 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     pa.W = S.W;
     pa.pbase = S.pbase;
     pa.plan = S.plan;
+    pa.ose_elem = S.ose_elem;
+    pa.ndpe = S.ndpe;
     if (launch_plan_merge(pa, S.n_ose, c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "plan merge");
     if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "plan sync");
     int herr[4] = {0, 0, 0, 0};

@@ -298,8 +298,8 @@ __global__ void k_plan_merge(PlanArgs A) {
   const int rstr = plan_row_bytes(k, W);
   for (int r = threadIdx.x; r < O.nrows; r += blockDim.x) {
     uint8_t *pr = A.plan + A.pbase[oi] + (int64_t)r * rstr;
-    uint16_t *lrow = reinterpret_cast<uint16_t *>(pr);
-    uint16_t *hm = lrow + k;
+    int32_t *rrow = reinterpret_cast<int32_t *>(pr);
+    uint16_t *hm = reinterpret_cast<uint16_t *>(pr + 4 * k);
     int32_t *cq = reinterpret_cast<int32_t *>(pr + plan_col_off(k, W));
     uint8_t *js = pr + plan_col_off(k, W) + 4 * W;
     for (int i = 0; i < W; ++i) { hm[i] = 0; cq[i] = -1; }
@@ -310,7 +310,7 @@ __global__ void k_plan_merge(PlanArgs A) {
       rid[m] = ((int64_t)A.ose_slots[O.slot_off + m] + r) * A.rstride;
       const RecEntry h = A.scratch[rid[m] + A.rstride - 1];
       len[m] = h.col;
-      lrow[m] = (uint16_t)h.bbase;
+      rrow[m] = A.ose_elem[O.slot_off + m] * A.ndpe + h.bbase;
       ptr[m] = 0;
     }
     int P = 0;
@@ -342,6 +342,94 @@ __global__ void k_plan_merge(PlanArgs A) {
       P += size;
     }
   }
+}
+
+// Merge pass over all in-kernel-merged shared rows (every contributor local to this rank): one
+// warp per row, lane = final column position q.  The column comes from the setup merge plan, the
+// value is the sum over the contributors holding q, in element order, of their natural-order
+// partial rows written by k_assemble (column sign from the plan).
+constexpr int MERGE_RPW = 4;  // rows per warp, their loads interleaved (memory-level parallelism)
+
+__global__ void __launch_bounds__(256) k_merge_rows(MergeArgs A) {
+  constexpr int R = MERGE_RPW;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t i0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (i0 >= A.n) return;
+  const int W = A.W;
+  MergeRow d{0, 0, 0};
+  if (lane < R && i0 + lane < A.n) d = A.rows[i0 + lane];
+  const uint8_t *pr[R];
+  int k[R], len[R];
+  int64_t rb[R], ro[R];
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const int64_t po = __shfl_sync(FULL, d.plan_off, u);
+    const int g = __shfl_sync(FULL, d.g, u);
+    k[u] = __shfl_sync(FULL, d.k, u);
+    pr[u] = A.plan + po;
+    rb[u] = lane < k[u] ? (int64_t)__ldg(reinterpret_cast<const int32_t *>(pr[u]) + lane) * A.W8 : 0;
+    ro[u] = k[u] ? __ldg(A.row_ptr + g) : 0;
+    len[u] = k[u] ? (int)(__ldg(A.row_ptr + g + 1) - ro[u]) : 0;
+  }
+  for (int q0 = 0; q0 < W; q0 += 32) {
+    const int q = q0 + lane;
+    unsigned hm[R];
+    int gid[R];
+    const uint8_t *js[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const bool on = q < len[u];
+      const int coff = plan_col_off(k[u], W);
+      hm[u] = on ? __ldg(reinterpret_cast<const uint16_t *>(pr[u] + 4 * k[u]) + q) : 0u;
+      gid[u] = on ? __ldg(reinterpret_cast<const int32_t *>(pr[u] + coff) + q) : 0;
+      js[u] = pr[u] + coff + 4 * W + q * k[u];
+    }
+    double xv[R][4];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+#pragma unroll
+      for (int m4 = 0; m4 < 4; ++m4) {  // first four holders of every row: all loads in flight together
+        const bool has = hm[u] != 0;
+        const int m = has ? __ffs(hm[u]) - 1 : 0;
+        if (has) hm[u] &= hm[u] - 1;
+        const int64_t rr = __shfl_sync(FULL, rb[u], m);
+        double x = 0.0;
+        if (has) {
+          const int jm = __ldg(js[u] + m);
+          x = A.nval[rr + (jm & 63)];
+          x = (jm & 64) ? -x : x;
+        }
+        xv[u][m4] = x;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      double sum = ((xv[u][0] + xv[u][1]) + xv[u][2]) + xv[u][3];
+      while (__any_sync(FULL, hm[u] != 0)) {  // rare: more than four holders (vertex rows)
+        const bool has = hm[u] != 0;
+        const int m = has ? __ffs(hm[u]) - 1 : 0;
+        if (has) hm[u] &= hm[u] - 1;
+        const int64_t rr = __shfl_sync(FULL, rb[u], m);
+        if (has) {
+          const int jm = __ldg(js[u] + m);
+          const double x = A.nval[rr + (jm & 63)];
+          sum += (jm & 64) ? -x : x;
+        }
+      }
+      if (q < len[u]) {
+        __stcs(A.col + ro[u] + q, gid[u]);
+        __stcs(A.val + ro[u] + q, sum);
+      }
+    }
+  }
+}
+
+cudaError_t launch_merge_rows(const MergeArgs &a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  const int64_t warps = (a.n + MERGE_RPW - 1) / MERGE_RPW;
+  k_merge_rows<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_plan_merge(const PlanArgs &a, int n_ose, cudaStream_t st) {

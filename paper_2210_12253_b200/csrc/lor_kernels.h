@@ -18,11 +18,19 @@ namespace lorb {
 constexpr int NROWKEY = 729;
 // byte stride of a row of the block-size table (16-byte aligned rows for vector loads)
 // merge plan row of a shared entity with k contributors, per final column position q:
-// [k x u16 contributor-local row][W x u16 holder mask over contributors] (pad to 4 B)
-// [W x i32 global column][W x k u8: slot j of q in holder m's natural record | 64 if the column
-// dof is sign-flipped in m (255 none)] (pad to 16 B: plan rows are staged with 16-byte loads)
-__host__ __device__ constexpr int plan_col_off(int k, int W) { return (2 * k + 2 * W + 3) & ~3; }
+// [k x i32 record row of contributor m (local element * ndpe + its local row)]
+// [W x u16 holder mask over contributors] (pad to 4 B) [W x i32 global column]
+// [W x k u8: slot j of q in holder m's natural record | 64 if the column dof is sign-flipped in m
+// (255 none)] (pad to 16 B)
+__host__ __device__ constexpr int plan_col_off(int k, int W) { return (4 * k + 2 * W + 3) & ~3; }
 __host__ __device__ constexpr int plan_row_bytes(int k, int W) { return (plan_col_off(k, W) + 4 * W + W * k + 15) & ~15; }
+
+// one shared (merged) row for the merge pass
+struct MergeRow {
+  int64_t plan_off;              // byte offset of the row's plan row
+  int32_t g;                     // local row index
+  int32_t k;                     // contributors
+};
 
 __host__ __device__ constexpr int tab_tzs(int nb) { return (nb + 15) / 16 * 16; }
 struct Tabs {
@@ -85,7 +93,21 @@ struct PlanArgs {
                                  // header (len, local row)
   int rstride, W;
   const int64_t *pbase;
+  const int32_t *ose_elem;       // local element of every contributor
+  int ndpe;
   uint8_t *plan;
+};
+
+// merge pass of the natural-order partial rows of shared rows: one warp per row
+struct MergeArgs {
+  int64_t n;                     // merged rows
+  int W, W8;
+  const MergeRow *rows;
+  const uint8_t *plan;
+  const double *nval;
+  const int64_t *row_ptr;
+  int32_t *col;
+  double *val;
 };
 
 struct FinArgs {
@@ -135,6 +157,7 @@ int64_t scan_status_words(int64_t n);
 cudaError_t launch_assemble(int dim, int space, int p, int quad, const AsmArgs &a, cudaStream_t st, int *smem_out);
 cudaError_t launch_finalize_list(const FinArgs &f, cudaStream_t st);
 cudaError_t launch_plan_merge(const PlanArgs &a, int n_ose, cudaStream_t st);
+cudaError_t launch_merge_rows(const MergeArgs &a, cudaStream_t st);
 cudaError_t launch_discrete(int which, const DiscArgs &a, cudaStream_t st);
 cudaError_t launch_rowptr_stride(int64_t *row_ptr, int64_t n, int w, cudaStream_t st);
 cudaError_t launch_dofmap(int dim, int space, const DofmapArgs &a, cudaStream_t st);
