@@ -239,7 +239,7 @@ def main():
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(args.config, {}).get("k_assemble_dram_bytes")
+                traffic = json.load(f).get(args.config, {}).get("fill_dram_bytes")
         except Exception:
             traffic = None
 
