@@ -282,11 +282,10 @@ __device__ __forceinline__ void row_values(const double *__restrict__ cm, const 
 //   (q,q^d)     = -s_d (Q_q s)_d - s'_d (Q_{q^d} s')_d
 //   (q^d,q^d')  = s_d s_d' Q_q[d][d'] + (same at corner q^d^d')        (face diagonal)
 //   body diagonal = 0
-template <int P, int NC>
+template <int P, int NC, int NRING_>
 __device__ __forceinline__ void cells_h1_corner(const double *__restrict__ X, double *__restrict__ cm, int k0, int ncell,
                                                 double alpha, double beta, int &bad) {
   constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1;
-  constexpr int NRING_ = P;  // only used with KZ == P for H1 (whole element)
   const int lane = threadIdx.x & 31;
   const int items = ncell * 8;
   const int ceil32 = (items + 31) / 32 * 32;
@@ -528,7 +527,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
   double *cm = reinterpret_cast<double *>(smem + CF::OFF_CM);
   __shared__ ElemTopo T;
   __shared__ ElemSpace E;
-  __shared__ int s_nb, s_fin_n, s_bad;
+  __shared__ int s_nb, s_fin_n, s_bad, s_ownacc;
   __shared__ int s_fin[27];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -552,7 +551,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
     if ((DIM * CF::NPTS) & 1) {
       if (tid == 0) X[DIM * CF::NPTS - 1] = __ldg(A.X + el * A.xstride + DIM * CF::NPTS - 1);
     }
-    if (tid == 0) { s_fin_n = 0; s_bad = 0; }
+    if (tid == 0) { s_fin_n = 0; s_bad = 0; s_ownacc = 0; }
   }
   __syncthreads();
   // ---- element block table, canonical axis order/directions, ascending-base order
@@ -562,7 +561,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
     if (DIM == 2 && tau >= 9) {
       B.size = 0; B.g0 = 0; B.base = 0; B.sigma = 1; B.ord = 0; B.str[0] = B.str[1] = B.str[2] = 0;
     } else {
-      block_affine<DIM, SP>(P, s, tau, T, A.base, B);
+      block_affine_eb<DIM, SP>(P, s, tau, T, E.ebase[tau], B);
     }
     blk[tid] = B;
     ordsig[tid] = (uint16_t)(B.ord | ((B.str[0] < 0) << 6) | ((B.str[1] < 0) << 7) | ((B.str[2] < 0) << 8));
@@ -619,9 +618,9 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
     const int k1 = (DIM == 3) ? ((k0 + KZ < P) ? k0 + KZ : P) : P;
     const int ncell = (DIM == 3) ? (k1 - k0) * P * P : P * P;
     if (ch > 0) __syncthreads();  // previous chunk's rows done before its ring slots are reused
-    if (DIM == 3 && SP == SP_H1 && QUAD == 0 && KZ == P) {
+    if (DIM == 3 && SP == SP_H1 && QUAD == 0) {
       int bad = 0;
-      cells_h1_corner<P, NC>(X, cm, k0, ncell, A.alpha, A.beta, bad);
+      cells_h1_corner<P, NC, CF::NRING>(X, cm, k0, ncell, A.alpha, A.beta, bad);
       if (bad) s_bad = bad;
     } else {
       for (int c = tid; c < ncell; c += blockDim.x) {
@@ -666,21 +665,41 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
     };
     // row order: partial rows first, own rows (the heavier path: positions + CSR stores) last, so
     // they fill as few warps as possible instead of diverging inside every warp
-    __shared__ int s_nsh, s_nown;
+    // Own rows are listed in row order (block-wide ballot scan), so an own row's ordinal in its
+    // element (the index of its setup position-table row) is deterministic.
+    __shared__ int s_nsh, s_nown, s_wc[CF::NW];
     uint16_t *rlist = reinterpret_cast<uint16_t *>(smem + CF::OFF_RL);
     if (tid == 0) { s_nsh = 0; s_nown = 0; }
     __syncthreads();
-    for (int r = tid; r < nrows; r += CF::NT) {
-      int s, x[3];
-      const int tr = decode_row(r, s, x);
-      const bool owned = T.flags[tr] & TF_OWNED;
-      const uint8_t sf = E.sflags[tr];
-      const bool shared = sf & SF_SHARED;
-      if (owned && !shared && !A.plan_mode) rlist[CF::MAXR - 1 - atomicAdd(&s_nown, 1)] = (uint16_t)r;
-      else if (shared && (owned || (sf & SF_SEND))) rlist[atomicAdd(&s_nsh, 1)] = (uint16_t)r;
+    for (int r0 = 0; r0 < nrows; r0 += CF::NT) {
+      const int r = r0 + tid;
+      bool own = false;
+      if (r < nrows) {
+        int s, x[3];
+        const int tr = decode_row(r, s, x);
+        const bool owned = T.flags[tr] & TF_OWNED;
+        const uint8_t sf = E.sflags[tr];
+        const bool shared = sf & SF_SHARED;
+        own = owned && !shared;
+        if (!own && shared && (owned || (sf & SF_SEND)) && A.plan_mode != 2) rlist[atomicAdd(&s_nsh, 1)] = (uint16_t)r;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, own);
+      if (lane == 0) s_wc[warp] = __popc(bal);
+      __syncthreads();
+      int wb = s_nown;
+      for (int w2 = 0; w2 < warp; ++w2) wb += s_wc[w2];
+      if (own) rlist[CF::MAXR - 1 - (wb + __popc(bal & ((1u << lane) - 1u)))] = (uint16_t)r;
+      __syncthreads();
+      if (tid == 0) {
+        int t = 0;
+        for (int w2 = 0; w2 < CF::NW; ++w2) t += s_wc[w2];
+        s_nown += t;
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    const int nsh = s_nsh, nact = s_nsh + s_nown;
+    const int nown = s_nown;
+    const int nsh = s_nsh, nact = s_nsh + (A.plan_mode == 1 ? 0 : nown);
+    const int own0 = s_ownacc;  // own rows of earlier chunks of this element
     for (int ii = tid; ii < nact; ii += CF::NT) {
       const int r = ii < nsh ? rlist[ii] : rlist[CF::MAXR - 1 - (ii - nsh)];
       int s, x[3];
@@ -702,14 +721,27 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
       const double sig_row = (bsg[lr] & 128) ? -1.0 : 1.0;
       int64_t out = 0;
       int rowlen = 0;
-      if (!natural) {
+      uint32_t posw[(W + 3) / 4];  // final position of every stencil slot in the CSR row, 4 per word (255: none)
+      auto pos_of = [&](int j) -> int { return (int)((posw[j >> 2] >> (8 * (j & 3))) & 255u); };
+      const int64_t own_ord = ii >= nsh ? A.ownbase[el] + own0 + (ii - nsh) : 0;
+      if (!natural && !rec && A.plan_mode == 0) {
+        // own row: its slot positions are topological and come from the setup position table
+        out = ld_stream(A.row_ptr + (gid - A.row_begin), l2_policy_first());
+        const uint4 *op = reinterpret_cast<const uint4 *>(A.ownpos + own_ord * own_w(W));
+#pragma unroll
+        for (int q = 0; q < own_w(W) / 16; ++q) {
+          const uint4 t = ld_stream(op + q, l2_policy_first());
+          const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (4 * q + c < (W + 3) / 4) posw[4 * q + c] = w4[c];
+        }
+      } else if (!natural) {
         if (rec) {
           const int c0 = cls_of(tr, 0), c1 = cls_of(tr, 1), c2 = DIM == 3 ? cls_of(tr, 2) : 1;
           const int nI = (c0 == 1) + (c1 == 1) + (DIM == 3 ? (c2 == 1) : 0);
           const int type = (nI == 0) ? 0 : (nI == DIM ? 3 : (DIM == 3 ? nI : 1));
           out = ((int64_t)E.rec[tr] + (gid - A.base[type][T.ent[tr]])) * A.rstride;
-        } else {
-          out = ld_stream(A.row_ptr + (gid - A.row_begin), l2_policy_first());
         }
         LOR_TSTAMP(ii == nsh, 11);
         // P0 of every block of the row (ascending block base order), then the final position of
@@ -772,7 +804,25 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
           }
         }
 #pragma unroll
-        for (int j = 0; j < W; ++j) ts[j * CF::NT] = pz[j] == 255 ? (unsigned char)255 : (unsigned char)(pz[j] + lx[j]);
+        for (int i = 0; i < (W + 3) / 4; ++i) {
+          uint32_t v = 0;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int j = 4 * i + c;
+            const uint32_t b = j < W ? (pz[j] == 255 ? 255u : (uint32_t)(unsigned char)(pz[j] + lx[j])) : 255u;
+            v |= b << (8 * c);
+          }
+          posw[i] = v;
+        }
+        if (A.plan_mode == 2) {  // setup own-row position pass: store the row's positions, no values
+          uint32_t w[own_w(W) / 4];
+#pragma unroll
+          for (int i = 0; i < own_w(W) / 4; ++i) w[i] = i < (W + 3) / 4 ? posw[i] : 0xffffffffu;
+          uint4 *op = reinterpret_cast<uint4 *>(A.ownpos + own_ord * own_w(W));
+#pragma unroll
+          for (int q = 0; q < own_w(W) / 16; ++q) op[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+          continue;
+        }
         LOR_TSTAMP(ii == nsh, 12);
       }
       double acc[W];
@@ -791,7 +841,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
         const uint64_t pf = l2_policy_first();
 #pragma unroll
         for (int j = 0; j < W; ++j) {
-          const int ps = ts[j * CF::NT];
+          const int ps = pos_of(j);
           if (ps != 255) {
             int l;
             if constexpr (SP == SP_H1) {
@@ -805,12 +855,11 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
             st_hint(A.val + out + ps, v, pf);
           }
         }
-        LOR_TSTAMP(ii == nsh, 14);
       } else {  // sorted record {column | block base << 32, value (plan pass: slot | 64 if flipped)}
         double2 *dst = reinterpret_cast<double2 *>(A.scratch) + out;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
-          const int ps = ts[j * CF::NT];
+          const int ps = pos_of(j);
           if (ps != 255) {
             int l;
             if constexpr (SP == SP_H1) {
@@ -828,6 +877,8 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
         dst[A.rstride - 1] = make_double2(__longlong_as_double(((long long)(unsigned)lr << 32) | (long long)(unsigned)rowlen), 0.0);
       }
     }
+    __syncthreads();  // every thread has read s_ownacc
+    if (tid == 0) s_ownacc += nown;
   }
   // shared rows are merged by the separate pass k_merge_rows (lor_kernels.cu)
   if (A.tstamp) {
@@ -843,8 +894,8 @@ cudaError_t launch_asm_p(const AsmArgs &a, int quad, cudaStream_t st, int *smem_
   const int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
-  // 3D H1 vertex rule: 6 CTAs/SM (80 registers) measured fastest at C2; LOR_MINB=4/5/8 for experiments
-  static const int minb = getenv("LOR_MINB") ? atoi(getenv("LOR_MINB")) : 6;
+  // 3D H1 vertex rule: 5 CTAs/SM (96 registers) measured fastest at C2; LOR_MINB=4/6/8 for experiments
+  static const int minb = getenv("LOR_MINB") ? atoi(getenv("LOR_MINB")) : 5;
   // dev experiment: LOR_SMEM_PAD inflates the dynamic shared memory to cap CTAs per SM
   static const int pad = getenv("LOR_SMEM_PAD") ? atoi(getenv("LOR_SMEM_PAD")) : 0;
   auto run = [&](auto k) {
@@ -855,8 +906,8 @@ cudaError_t launch_asm_p(const AsmArgs &a, int quad, cudaStream_t st, int *smem_
   if (quad == 0) {
     if (DIM == 3 && SP == SP_H1 && minb == 8) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 8 : 4>);
     else if (DIM == 3 && SP == SP_H1 && minb == 6) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 6 : 4>);
-    else if (DIM == 3 && SP == SP_H1 && minb == 5) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 5 : 4>);
-    else run(k_assemble<DIM, SP, P, 0, KZ, 4>);
+    else if (DIM == 3 && SP == SP_H1 && minb == 4) run(k_assemble<DIM, SP, P, 0, KZ, 4>);
+    else run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 5 : 4>);
   } else {
     run(k_assemble<DIM, SP, P, 1, KZ, 4>);
   }

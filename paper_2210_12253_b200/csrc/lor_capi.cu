@@ -72,6 +72,9 @@ struct SpaceDev {
   int32_t *ose_slots = nullptr, *counters = nullptr, *defer = nullptr;
   int n_ose = 0, n_defer = 0;
   MergeRow *mrows = nullptr;  // merge-pass rows
+  int64_t *ownbase = nullptr;  // own-row position table: first row per element
+  uint8_t *ownpos = nullptr;
+  int64_t n_own = 0;
   int64_t n_mrows = 0;
   RecEntry *scratch = nullptr;
   int64_t n_records = 0;
@@ -114,6 +117,23 @@ struct lor_ctx_s {
 };
 
 namespace {
+
+// local rows of space `space` on entity slot tau (axis classes 0 min, 1 interior, 2 max)
+int64_t class_rows(int dim, int space, int p, int tau) {
+  const int cls[3] = {tau % 3, (tau / 3) % 3, tau / 9};
+  const int S = space == 0 ? 1 : 3;
+  int64_t tot = 0;
+  for (int s2 = 0; s2 < S; ++s2) {
+    int64_t n = 1;
+    for (int a = 0; a < 3; ++a) {
+      if (a >= dim) { n *= cls[a] == 0 ? 1 : 0; continue; }
+      const bool vk = space == 0 ? true : (space == 1 ? a != s2 : a == s2);
+      n *= vk ? (cls[a] == 1 ? p - 1 : 1) : (cls[a] == 1 ? p : 0);
+    }
+    tot += n;
+  }
+  return tot;
+}
 
 lor_status fail(lor_ctx c, lor_status st, const std::string &msg) {
   if (c) c->last_error = msg;
@@ -255,6 +275,8 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.beta = beta;
   a.err = c->err;
   a.tstamp = c->tstamp;
+  a.ownbase = S.ownbase;
+  a.ownpos = S.ownpos;
   a.dbg = getenv("LOR_DBG") ? atoi(getenv("LOR_DBG")) : 0;
   CUDA_TRY(c, launch_assemble(c->dim, s, c->p, (int)quad, a, c->stream, nullptr));
   if (c->nel_local > 0) c->launches++;
@@ -596,6 +618,43 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     int herr[4] = {0, 0, 0, 0};
     cudaMemcpy(herr, c->err, sizeof(herr), cudaMemcpyDeviceToHost);
     if (herr[0]) { cudaMemset(c->err, 0, sizeof(herr)); }  // geometry errors are reported by assembly calls
+  }
+  // own-row position tables (topological): rows of entities owned by one element alone get the
+  // final CSR position of every stencil slot once here, by a position pass of the element kernel
+  for (int s = 0; s < 3; ++s) {
+    SpaceDev &S = c->sp[s];
+    const SpacePlan &P = plan.sp[s];
+    if (!S.valid || c->nel_local == 0) continue;
+    std::vector<int64_t> ob((size_t)c->nel_local);
+    int64_t tot = 0;
+    for (int64_t e = 0; e < c->nel_local; ++e) {
+      ob[e] = tot;
+      for (int tau = 0; tau < 27; ++tau)
+        if ((plan.topo[e].flags[tau] & TF_OWNED) && !(P.esp[e].sflags[tau] & SF_SHARED))
+          tot += class_rows(A.dim, s, A.p, tau);
+    }
+    S.n_own = tot;
+    if (dev_upload(c, &S.ownbase, ob.data(), ob.size()) != cudaSuccess ||
+        dev_alloc(c, &S.ownpos, (size_t)std::max<int64_t>(tot, 1) * own_w(S.W)) != cudaSuccess)
+      return bail(LOR_ERR_OUT_OF_MEMORY, "own-row positions");
+    AsmArgs a{};
+    a.order = c->order;
+    a.nel_local = c->nel_local;
+    a.elem_begin = c->elem_begin;
+    a.topo = c->topo;
+    a.esp = S.esp;
+    a.X = c->X;
+    a.xstride = c->xstride;
+    for (int t = 0; t < 4; ++t) a.base[t] = S.base[t];
+    a.tabs = Tabs{S.tslot, S.tsize, S.tpb, S.tnpb, S.tlex};
+    a.row_begin = S.row_begin;
+    a.alpha = 1.0;
+    a.beta = 1.0;
+    a.err = c->err;
+    a.plan_mode = 2;
+    a.ownbase = S.ownbase;
+    a.ownpos = S.ownpos;
+    if (launch_assemble(A.dim, s, A.p, 0, a, c->stream, nullptr) != cudaSuccess) return bail(LOR_ERR_CUDA, "own-row positions");
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(LOR_ERR_CUDA, "setup sync");
   *out = c;

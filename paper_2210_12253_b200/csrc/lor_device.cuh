@@ -101,8 +101,9 @@ __device__ __forceinline__ int coord_cls(bool vk, int x, int p) { return vk ? (x
 
 // Block affine map from App. A.  T: the element's topology record,
 // base[t]: global id of the first dof of entity t of each type for this space.
+// eb: global id of the first dof of the entity at slot tau (base[type][T.ent[tau]])
 template <int DIM, int SP>
-__device__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int32_t *const *base, Blk &B) {
+__device__ void block_affine_eb(int p, int s, int tau, const ElemTopo &T, int eb, Blk &B) {
   int c[3] = {cls_of(tau, 0), cls_of(tau, 1), DIM == 3 ? cls_of(tau, 2) : 1};
   B.g0 = 0;
   B.str[0] = B.str[1] = B.str[2] = 0;
@@ -125,11 +126,11 @@ __device__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int
   const int o = T.orient[tau];
   if (SP == SP_H1) {
     if (nI == 0) {
-      B.g0 = base[0][ent];
+      B.g0 = eb;
     } else if (nI == 1) {  // edge along the interior axis d
       int d = (c[0] == 1) ? 0 : (c[1] == 1 ? 1 : 2);
       bool rev = o & 1;
-      B.g0 = base[1][ent] + (rev ? p - 1 : -1);
+      B.g0 = eb + (rev ? p - 1 : -1);
       B.str[d] = rev ? -1 : 1;
     } else if (DIM == 3 && nI == 2) {  // face with normal n
       int n = (c[0] != 1) ? 0 : (c[1] != 1 ? 1 : 2);
@@ -138,19 +139,19 @@ __device__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int
       int ax1 = swp ? v : u, ax2 = swp ? u : v;
       B.str[ax1] = s1n ? -1 : 1;
       B.str[ax2] = s2n ? -(p - 1) : (p - 1);
-      B.g0 = base[2][ent] + (s1n ? p - 1 : -1) + (p - 1) * (s2n ? p - 1 : -1);
+      B.g0 = eb + (s1n ? p - 1 : -1) + (p - 1) * (s2n ? p - 1 : -1);
     } else {  // interior, lexicographic
       B.str[0] = 1;
       B.str[1] = p - 1;
       B.str[2] = DIM == 3 ? (p - 1) * (p - 1) : 0;
-      B.g0 = base[3][ent] - 1 - (p - 1) - (DIM == 3 ? (p - 1) * (p - 1) : 0);
+      B.g0 = eb - 1 - (p - 1) - (DIM == 3 ? (p - 1) * (p - 1) : 0);
     }
   } else if (SP == SP_ND) {
     int u = (s == 0) ? 1 : 0, v = (s == 2) ? 1 : 2;  // axes other than the edge direction
     bool bu = c[u] != 1, bv = c[v] != 1;
     if (bu && bv) {  // coarse edge along s
       bool rev = o & 1;
-      B.g0 = base[1][ent] + (rev ? p - 1 : 0);
+      B.g0 = eb + (rev ? p - 1 : 0);
       B.str[s] = rev ? -1 : 1;
       B.sigma = rev ? -1 : 1;
     } else if (bu || bv) {  // coarse face with normal n (the boundary axis), s in-face
@@ -158,7 +159,7 @@ __device__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int
       int fu = (n == 0) ? 1 : 0, fv = (n == 2) ? 1 : 2;
       int swp = o & 1, s1n = (o >> 1) & 1, s2n = (o >> 2) & 1;
       int ax1 = swp ? fv : fu, ax2 = swp ? fu : fv;
-      int fb = base[2][ent];
+      int fb = eb;
       if (s == ax1) {  // axis1-parallel: base + i1c + p (i2 - 1)
         B.str[s] = s1n ? -1 : 1;
         B.str[ax2] = s2n ? -p : p;
@@ -176,7 +177,7 @@ __device__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int
       B.str[0] = 1;
       B.str[1] = rg[0];
       B.str[2] = rg[0] * rg[1];
-      int g = base[3][ent] + s * p * (p - 1) * (p - 1);
+      int g = eb + s * p * (p - 1) * (p - 1);
       for (int a = 0; a < 3; ++a)
         if (a != s) g -= B.str[a];
       B.g0 = g;
@@ -188,7 +189,7 @@ __device__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int
       int ax1 = swp ? v : u, ax2 = swp ? u : v;
       B.str[ax1] = s1n ? -1 : 1;
       B.str[ax2] = s2n ? -p : p;
-      B.g0 = base[2][ent] + (s1n ? p - 1 : 0) + (s2n ? p * (p - 1) : 0);
+      B.g0 = eb + (s1n ? p - 1 : 0) + (s2n ? p * (p - 1) : 0);
       const int eps = (s == 1) ? -1 : 1;
       B.sigma = (int8_t)((s1n ? -1 : 1) * (s2n ? -1 : 1) * (swp ? -1 : 1) * eps);
     } else {  // interior block s: x-fastest over (vertex-1 along s: p-1; cells elsewhere: p)
@@ -197,7 +198,7 @@ __device__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int
       B.str[0] = 1;
       B.str[1] = rg[0];
       B.str[2] = rg[0] * rg[1];
-      B.g0 = base[3][ent] + s * p * p * (p - 1) - B.str[s];
+      B.g0 = eb + s * p * p * (p - 1) - B.str[s];
     }
   }
   // min gid over the box and the axis order by |stride| (length-1 axes sort first, any order)
@@ -219,6 +220,14 @@ __device__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int
   for (int i = 1; i < 3; ++i)
     for (int j = i; j > 0 && key[ord[j]] < key[ord[j - 1]]; --j) { int t = ord[j]; ord[j] = ord[j - 1]; ord[j - 1] = t; }
   B.ord = (uint8_t)(ord[0] | (ord[1] << 2) | (ord[2] << 4));
+}
+
+template <int DIM, int SP>
+__device__ __forceinline__ void block_affine(int p, int s, int tau, const ElemTopo &T, const int32_t *const *base, Blk &B) {
+  const int c0 = cls_of(tau, 0), c1 = cls_of(tau, 1), c2 = DIM == 3 ? cls_of(tau, 2) : 1;
+  const int nI = (c0 == 1) + (c1 == 1) + (DIM == 3 ? (c2 == 1) : 0);
+  const int type = (nI == 0) ? 0 : (nI == DIM ? 3 : (DIM == 3 ? nI : 1));
+  block_affine_eb<DIM, SP>(p, s, tau, T, base[type][T.ent[tau]], B);
 }
 
 // ------------------------------------------------------------------------- row geometry

@@ -50,9 +50,11 @@ struct __align__(16) ElemSpace {
   int32_t rec[27];     // record base (16-byte-entry records of MAXL entries) of this element's partial
                        // rows of the entity, -1 if the entity's rows are written directly
   int32_t ose[27];     // index into the OSE table (owned shared entities), -1 otherwise
+  int32_t ebase[27];   // global id of the first dof of the entity at each slot (this space)
   uint8_t sflags[27];  // SF_*
-  uint8_t pad[5];
+  uint8_t pad[1];
 };
+static_assert(sizeof(ElemSpace) % 16 == 0, "layout");
 
 // Owned shared entity (per space)
 struct __align__(16) Ose {

@@ -32,6 +32,9 @@ struct MergeRow {
   int32_t k;                     // contributors
 };
 
+// own-row position table row (bytes): whole 16-byte vectors
+__host__ __device__ constexpr int own_w(int W) { return (W + 15) / 16 * 16; }
+
 __host__ __device__ constexpr int tab_tzs(int nb) { return (nb + 15) / 16 * 16; }
 struct Tabs {
   const uint32_t *slot;
@@ -77,7 +80,12 @@ struct AsmArgs {
   const int64_t *pbase;          // [n_ose] byte offset of the OSE's merge-plan rows
   const uint8_t *plan;           // per OSE row: k x uint16 contributor local rows, then W x k slot bytes
   int maxl;
-  int plan_mode;                 // 1: setup plan pass (partial-row records of every shared row, no CSR output)
+  int plan_mode;                 // 1: setup plan pass (partial-row records of every shared row, no CSR
+                                 //    output)
+                                 // 2: setup own-row position pass (final position of every stencil slot of
+                                 //    every own row -> ownpos)
+  const int64_t *ownbase;        // [nel_local] first own-row ordinal of the element
+  uint8_t *ownpos;               // [own rows][own_w(W)] slot -> position in the CSR row (255: not a column)
   double alpha, beta;
   int *err;                      // [0] code, [1] element, [2] cell
   unsigned long long *tstamp;    // optional [grid][16] per-CTA phase clocks (LOR_PHASE_TIMING=1)

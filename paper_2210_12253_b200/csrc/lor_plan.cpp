@@ -400,12 +400,13 @@ void HostPlan::build(const PlanInput &in) {
     for (int64_t i = 0; i < nel_local; ++i) {
       int64_t e = elem_begin + i;
       ElemSpace &R = S.esp[i];
-      for (int tau = 0; tau < 27; ++tau) { R.rec[tau] = -1; R.ose[tau] = -1; R.sflags[tau] = 0; }
+      for (int tau = 0; tau < 27; ++tau) { R.rec[tau] = -1; R.ose[tau] = -1; R.ebase[tau] = -1; R.sflags[tau] = 0; }
       for (int tau = 0; tau < nslot; ++tau) {
         int type;
         int64_t id;
         uint8_t orient;
         slot_info(e, tau, type, id, orient);
+        R.ebase[tau] = S.base[type].empty() ? -1 : S.base[type][id];
         if (type == 3 || nd[type] == 0) continue;
         int64_t k0 = inc_off[type][id], k1 = inc_off[type][id + 1];
         if (k1 - k0 < 2) continue;  // exclusive rows: written directly
