@@ -170,6 +170,13 @@ int64_t lor_kernel_launches(lor_ctx ctx);
  * phases written (<= 8). */
 int lor_last_phase_ms(lor_ctx ctx, float *ms, int cap);
 
+/* Which value-fill path lor_assemble_<space> takes with the vertex rule: 1 = extended-frame
+ * single pass (every element writes the complete rows it owns, recomputing the
+ * neighbour cells that touch them; 3D H1, one rank, meshes whose elements all have a regular
+ * 3x3x3 coarse neighbourhood -- checked at setup), 0 = element pass + merge pass of partial rows.
+ * LOR_XFRAME=0 in the environment at setup forces 0.  Returns -1 for an invalid context/space. */
+int lor_fill_path(lor_ctx ctx, lor_space space);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,7 +101,9 @@ def build(force: bool = False, verbose: bool = True) -> str:
     units = _gen_units(plist)
     jobs = [(os.path.join(CSRC, "lor_kernels.cu"), os.path.join(BUILD, "lor_kernels.o")),
             (os.path.join(CSRC, "lor_capi.cu"), os.path.join(BUILD, "lor_capi.o")),
-            (os.path.join(CSRC, "lor_plan.cpp"), os.path.join(BUILD, "lor_plan.o"))]
+            (os.path.join(CSRC, "lor_plan.cpp"), os.path.join(BUILD, "lor_plan.o")),
+            (os.path.join(CSRC, "lor_xframe.cpp"), os.path.join(BUILD, "lor_xframe.o")),
+            (os.path.join(CSRC, "lor_xh1.cu"), os.path.join(BUILD, "lor_xh1.o"))]
     jobs += [(u, u[:-3] + ".o") for u in units]
     # largest first (ND / high p) for better packing
     jobs.sort(key=lambda j: (("_3_1_" in j[0]) * 10 + ("_3_0_" in j[0]) * 5 + int(j[0][-4]) if "asm_" in j[0] else 100),

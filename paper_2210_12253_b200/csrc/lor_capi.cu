@@ -16,6 +16,7 @@
 #include "lor_internal.h"
 #include "lor_kernels.h"
 #include "lor_plan.h"
+#include "lor_xframe.h"
 
 // ---- minimal NCCL ABI (loaded with dlopen only when nranks > 1) ----------------------------------
 typedef struct ncclComm *ncclComm_t;
@@ -91,6 +92,12 @@ struct SpaceDev {
   int32_t *ose_elem = nullptr;
   int64_t *pbase = nullptr;
   uint8_t *plan = nullptr, *is_defer = nullptr;
+  // extended-frame fill path (lor_xframe.h; H1, 3D, one rank, regular neighbourhoods)
+  bool xok = false;
+  XElem *xe = nullptr;
+  XBox *xbox = nullptr;
+  uint8_t *xpos = nullptr;
+  int xc[3] = {0, 0, 0};
 };
 
 }  // namespace
@@ -246,6 +253,33 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   lor_status st = run_count_scan(c, s, out->row_ptr);
   if (st) return st;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  if (S.xok && quad == LOR_QUAD_VERTEX) {  // extended-frame path: every owned row in one pass
+    XFillArgs x{};
+    x.nel_local = c->nel_local;
+    x.elem_begin = c->elem_begin;
+    x.order = c->order;
+    x.xe = S.xe;
+    x.box = S.xbox;
+    x.pos = S.xpos;
+    x.X = c->X;
+    x.xstride = c->xstride;
+    x.row_begin = S.row_begin;
+    x.row_ptr = out->row_ptr;
+    x.col = out->col;
+    x.val = out->val;
+    x.alpha = alpha;
+    x.beta = beta;
+    x.ncx = S.xc[0];
+    x.ncy = S.xc[1];
+    x.ncz = S.xc[2];
+    x.err = c->err;
+    CUDA_TRY(c, launch_xh1_fill(c->p, x, c->stream, nullptr));
+    if (c->nel_local > 0) c->launches++;
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    return LOR_OK;
+  }
   AsmArgs a;
   a.order = c->order;
   a.nel_local = c->nel_local;
@@ -656,6 +690,41 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     a.ownpos = S.ownpos;
     if (launch_assemble(A.dim, s, A.p, 0, a, c->stream, nullptr) != cudaSuccess) return bail(LOR_ERR_CUDA, "own-row positions");
   }
+  // extended-frame H1 path: regular-neighbourhood check, element records, box and position tables
+  if (A.dim == 3 && c->sp[SP_H1].valid && c->nel_local > 0 && !(getenv("LOR_XFRAME") && !atoi(getenv("LOR_XFRAME")))) {
+    SpaceDev &S = c->sp[SP_H1];
+    std::vector<XElem> xe;
+    std::string why;
+    if (xframe_build(plan, A.elem_vert, xe, S.xc, &why)) {
+      if (dev_upload(c, &S.xe, xe.data(), xe.size()) != cudaSuccess ||
+          dev_alloc(c, &S.xbox, (size_t)c->nel_local * 125) != cudaSuccess ||
+          dev_alloc(c, &S.xpos, (size_t)std::max<int64_t>(S.n_local, 1) * XPOS_W) != cudaSuccess)
+        return bail(LOR_ERR_OUT_OF_MEMORY, "xframe");
+      if (cudaMemset(S.xpos, 0xff, (size_t)std::max<int64_t>(S.n_local, 1) * XPOS_W) != cudaSuccess)
+        return bail(LOR_ERR_CUDA, "xframe");
+      // S.cnt still holds the H1 row counts of the setup count pass
+      XSetupArgs xa{};
+      xa.nel_local = c->nel_local;
+      xa.xe = S.xe;
+      xa.topo = c->topo;
+      fill_base(S, xa.base);
+      xa.row_begin = S.row_begin;
+      xa.cnt = S.cnt;
+      xa.box = S.xbox;
+      xa.pos = S.xpos;
+      xa.err = c->err;
+      if (cudaMemset(c->err, 0, 4 * sizeof(int)) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe");
+      if (launch_xh1_setup(A.p, xa, c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe setup");
+      if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe sync");
+      int herr[4] = {0, 0, 0, 0};
+      cudaMemcpy(herr, c->err, sizeof(herr), cudaMemcpyDeviceToHost);
+      cudaMemset(c->err, 0, sizeof(herr));
+      S.xok = herr[0] == 0;
+      if (!S.xok) fprintf(stderr, "lor_setup: extended-frame tables inconsistent, using the element + merge passes\n");
+    } else if (getenv("LOR_XFRAME_VERBOSE")) {
+      fprintf(stderr, "lor_setup: extended-frame path off: %s\n", why.c_str());
+    }
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(LOR_ERR_CUDA, "setup sync");
   *out = c;
   return LOR_OK;
@@ -852,6 +921,11 @@ int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int
   cudaStreamSynchronize(c->stream);
   if (cudaMemcpy(host_out, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return bytes;
+}
+
+int lor_fill_path(lor_ctx c, lor_space space) {
+  if (!c || space < 0 || space > 2 || !c->sp[space].valid) return -1;
+  return c->sp[space].xok ? 1 : 0;
 }
 
 int lor_last_phase_ms(lor_ctx c, float *ms, int cap) {

@@ -1,0 +1,90 @@
+// lor_xframe.h -- the extended-frame ("owner computes") H1 fill path (DESIGN.md §4 "k_xh1").
+//
+// Every element writes the complete CSR rows of the dofs it owns (the minimal element containing
+// the dof's coarse entity), shared rows included: the LOR cells of the neighbouring
+// macro elements that touch those rows are recomputed in the owner's own lattice frame extended by
+// one cell layer on every side ("extended frame", lattice coordinates y in [-1, p+1]^3).  No
+// partial rows, no merge pass, no value atomics.
+//
+// The extended frame needs a regular neighbourhood: the (up to) 26 elements around an element
+// form a 3x3x3 block of hexes (any local orientations, any element numbering).  lor_setup checks
+// this per mesh (xframe_build) and otherwise keeps the general element pass + merge pass.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "lor_internal.h"
+
+namespace lorb {
+
+// neighbour delta index: (dx+1) + 3 (dy+1) + 9 (dz+1); 13 = the element itself
+struct XNbr {
+  int32_t el;     // local element index, -1: no element there
+  uint32_t code;  // bits 0-5: ax[a] (2 bits per neighbour-local axis a: the extended-frame axis it
+                  // runs along); bits 6-8: sn[a] (1 = runs along -ax[a]); bits 9-14: o[k] + 1
+                  // (2 bits per extended axis k: coarse position of the neighbour's local corner 0)
+                  // => local lattice coordinate L_a = sn_a * (y[ax_a] - p * o[ax_a])
+};
+
+struct __align__(16) XElem {
+  uint32_t own;      // bit tau: this element writes the rows of entity slot tau (TF_MIN & TF_OWNED)
+  int8_t clo[3];     // cell box [clo, chi] per axis in extended-frame cell coordinates
+  int8_t chi[3];
+  uint8_t pad[6];
+  XNbr nbr[27];
+  uint8_t pad2[8];
+};
+static_assert(sizeof(XElem) == 240, "layout");
+
+// extended-frame box table entry: points y with per-axis class (-1 | 0 | [1,p-1] | p | p+1) share
+// one coarse entity of one element, so gid = g0 + sum_k s[k] y[k] (App. A numbering is affine)
+struct XBox {
+  int32_t g0;
+  int8_t s[3];
+  uint8_t valid;
+};
+static_assert(sizeof(XBox) == 8, "layout");
+
+constexpr int XPOS_W = 32;  // position-table row: final CSR position of each of the 27 stencil slots
+
+struct XSetupArgs {
+  int64_t nel_local;
+  const XElem *xe;
+  const ElemTopo *topo;
+  const int32_t *base[4];
+  int64_t row_begin;
+  const int32_t *cnt;  // row lengths from k_count (consistency check)
+  XBox *box;           // [nel_local][125]
+  uint8_t *pos;        // [n_local][XPOS_W]
+  int *err;            // set to 1 on any inconsistency
+};
+
+struct XFillArgs {
+  int64_t nel_local, elem_begin;
+  const int32_t *order;
+  const XElem *xe;
+  const XBox *box;
+  const uint8_t *pos;
+  const double *X;
+  int64_t xstride;
+  int64_t row_begin;
+  const int64_t *row_ptr;
+  int32_t *col;
+  double *val;
+  double alpha, beta;
+  int ncx, ncy, ncz;  // max cell-box extents over the elements (shared-memory sizing)
+  int *err;
+};
+
+// host: regular-neighbourhood check and per-element extended-frame records (nranks == 1)
+struct HostPlan;
+bool xframe_build(const HostPlan &plan, const int64_t *elem_vert, std::vector<XElem> &out, int cmax[3],
+                  std::string *why);
+
+cudaError_t launch_xh1_setup(int p, const XSetupArgs &a, cudaStream_t st);
+cudaError_t launch_xh1_fill(int p, const XFillArgs &a, cudaStream_t st, int *smem_out);
+
+}  // namespace lorb

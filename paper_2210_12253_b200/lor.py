@@ -73,6 +73,7 @@ def lib():
         L.lor_debug_dump.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
         L.lor_update_coordinates.argtypes = [C.c_void_p, C.c_void_p]
         L.lor_last_phase_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int]
+        L.lor_fill_path.argtypes = [C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -171,6 +172,10 @@ class LOR:
 
     def launches(self) -> int:
         return int(lib().lor_kernel_launches(self.h))
+
+    def fill_path(self, space="h1") -> int:
+        """1: extended-frame single-pass fill, 0: element pass + merge pass (lor_fill_path)."""
+        return int(lib().lor_fill_path(self.h, SPACES[space]))
 
     def phase_ms(self):
         buf = (C.c_float * 8)()
