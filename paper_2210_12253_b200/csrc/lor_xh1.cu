@@ -162,36 +162,145 @@ __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
 }
 
 // ============================================================================== fill kernel
-struct XLayout {
-  int npb;   // points in the (max) point box
-  int ncp;   // cell-matrix pitch (odd)
-  int nr;    // ring layers
-  int off_xg, off_cm, bytes;
+// Compile-time geometry of the shared-memory boxes.  NB = cell-box extent per axis the kernel is
+// built for: P+1 (every element of the mesh has a box of at most P+1 cells per axis: elements
+// owning entities on one side per axis -- lexicographic and orientation-scrambled structured
+// meshes) or P+2 (general).  All box-local index arithmetic then has constant strides.
+template <int P, int NB>
+struct XCfg {
+  static constexpr int PB = NB + 1;                 // points per axis of the point box
+  static constexpr int NPB = PB * PB * PB;
+  static constexpr int LAY = NB * NB;               // cells per layer
+  static constexpr int CE = 32;                     // stored entries per cell (36 packed minus the
+                                                    // four body diagonals, exactly 0 under the vertex rule)
+  static constexpr int CP = 33;                     // cell pitch (doubles): odd, conflict-free row gathers
+  static constexpr bool ONE = NB * LAY * CP * 8 <= 36 * 1024;  // all cells resident: one chunk
+  static constexpr int KZ = ONE ? P + 1 : 1;       // row layers per chunk
+  static constexpr int NR = ONE ? NB : 2;          // resident cell layers (ring)
+  static constexpr int NP1 = P + 1;
+  static constexpr int MAXROW = KZ * NP1 * NP1;     // rows per chunk (<= 125 for P <= 4, (P+1)^2 else)
+  static constexpr int OFF_XG = 3 * NPB * 8;
+  static constexpr int OFF_CM = (OFF_XG + NPB * 4 + 15) / 16 * 16;
+  static constexpr int OFF_RL = OFF_CM + NR * LAY * CP * 8;              // owned-row list uint16[NP1^3]
+  static constexpr int OFF_MT = (OFF_RL + 2 * NP1 * NP1 * NP1 + 15) / 16 * 16;  // per chunk row: out int64
+  static constexpr int OFF_PX = OFF_MT + 8 * MAXROW;                      // px int16 | len << 16 (int32)
+  static constexpr int SMEM = OFF_PX + 4 * MAXROW;
+  // staging of a chunk's rows for the coalesced write-out: values in final position order and the
+  // stencil slot of each position, placed over cell storage no longer needed (one chunk: all of it;
+  // ring: the slot the next chunk overwrites first)
+  static constexpr int STAGE = MAXROW * 27 * 9;
+  static_assert(STAGE <= (ONE ? NR * LAY * CP * 8 : LAY * CP * 8), "stage does not fit");
+  static_assert(MAXROW <= 128, "one row per thread per chunk");
 };
 
-__host__ __device__ inline XLayout xh1_layout(int ncx, int ncy, int ncz, int kz) {
-  XLayout L;
-  L.npb = (ncx + 1) * (ncy + 1) * (ncz + 1);
-  L.nr = kz + 1 < ncz ? kz + 1 : ncz;
-  L.ncp = (L.nr * ncx * ncy) | 1;
-  L.off_xg = 3 * L.npb * 8;
-  L.off_cm = (L.off_xg + L.npb * 4 + 15) / 16 * 16;
-  L.bytes = L.off_cm + 36 * L.ncp * 8;
-  return L;
+// packed index of the cell-matrix entry (a, b), a <= b, with the four body diagonals removed
+__host__ __device__ constexpr int cidx(int a, int b) {
+  const int i = a < b ? a : b, j = a < b ? b : a;
+  const int t = i * 8 - i * (i - 1) / 2 + (j - i);  // tri(8, i, j)
+  // body diagonals (q, q^7), q < 4, sit at tri indices 7, 13, 18, 22
+  return t - (t > 7) - (t > 13) - (t > 18) - (t > 22);
+}
+__host__ __device__ constexpr bool body_diag(int a, int b) { return (a ^ b) == 7; }
+
+// 1/x for x > 0: float seed + two Newton steps (relative error ~1e-28 before rounding)
+__device__ __forceinline__ double rcp_pos(double x) {
+  double r = (double)__frcp_rn((float)x);
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
-template <int P>
-__global__ void __launch_bounds__(128, 3) k_xh1_fill(XFillArgs A, int kz) {
-  constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1;
+// One LOR cell under the vertex rule (reading P-1), computed by one thread with the corner loop
+// unrolled: at corner q the Jacobian columns are the cell edge vectors through q, Q = w a
+// adj adj^T / det, and the corner adds (same terms as lor_cells.cuh)
+//   (q,q) += s^T Q s + w b det,  (q^d,q^d) += Q_dd,  (q,q^d) += -s_d (Q s)_d,
+//   (q^d,q^d') += s_d s_d' Q_dd'   (s = reference gradient signs of N_q, compile-time).
+// 32 entries (cidx order) stored at o[0..31]; returns false if det J <= 0 at a corner.
+// does corner q of a cell add to the entry (a, b) (see cell_h1v)?
+__host__ __device__ constexpr bool corner_touches(int q, int a, int b) {
+  if (a > b) { const int t = a; a = b; b = t; }
+  if (a == b) return a == q || (a ^ q) == 1 || (a ^ q) == 2 || (a ^ q) == 4;       // diagonal
+  const int x = a ^ b;
+  if (x == 1 || x == 2 || x == 4) return q == a || q == b;                         // edge
+  if (x == 7) return false;                                                        // body diagonal
+  return (q ^ a) != 0 && (q ^ b) != 0 && ((q ^ a) | (q ^ b)) == x;                 // face diagonal
+}
+__host__ __device__ constexpr bool first_touch(int q, int a, int b) {
+  for (int k = 0; k < q; ++k)
+    if (corner_touches(k, a, b)) return false;
+  return true;
+}
+
+template <int NPB, int PB>
+__device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, double a8, double b8, double *__restrict__ o) {
+  auto X = [&](int v, int k) -> double { return XE[k * NPB + pb + (v & 1) + PB * (((v >> 1) & 1) + PB * ((v >> 2) & 1))]; };
+  // accumulate in the cell's (thread-private) shared-memory row: the first corner touching an
+  // entry stores, later ones add (compile-time after unrolling)
+  auto put = [&](int q, int ea, int eb, double v) {
+    double &dst = o[cidx(ea, eb)];
+    if (first_touch(q, ea, eb)) dst = v;
+    else dst += v;
+  };
+  bool ok = true;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    // corners are evaluated one after the other (the fence keeps the compiler from hoisting every
+    // corner's loads and arithmetic at once: ~200 registers otherwise); the corner re-reads its
+    // four points from shared memory
+    asm volatile("" ::: "memory");
+    double j[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) j[d][k] = X(q | (1 << d), k) - X(q & ~(1 << d), k);
+    double r[3][3];
+    cross3x(j[1], j[2], r[0]);
+    cross3x(j[2], j[0], r[1]);
+    cross3x(j[0], j[1], r[2]);
+    const double det = dot3x(j[0], r[0]);
+    ok = ok && det > 0.0;
+    const double sa = a8 * ((fabs(det) > 1e-30) ? rcp_pos(det) : 1.0 / det);
+    double Q[3][3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int e = d; e < 3; ++e) Q[d][e] = Q[e][d] = sa * dot3x(r[d], r[e]);
+    const double s0 = (q & 1) ? 1.0 : -1.0, s1 = ((q >> 1) & 1) ? 1.0 : -1.0, s2 = ((q >> 2) & 1) ? 1.0 : -1.0;
+    double Qs[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) Qs[d] = s0 * Q[d][0] + s1 * Q[d][1] + s2 * Q[d][2];
+    put(q, q, q, s0 * Qs[0] + s1 * Qs[1] + s2 * Qs[2] + b8 * det);
+    put(q, q ^ 1, q ^ 1, Q[0][0]);
+    put(q, q ^ 2, q ^ 2, Q[1][1]);
+    put(q, q ^ 4, q ^ 4, Q[2][2]);
+    put(q, q, q ^ 1, -s0 * Qs[0]);
+    put(q, q, q ^ 2, -s1 * Qs[1]);
+    put(q, q, q ^ 4, -s2 * Qs[2]);
+    put(q, q ^ 1, q ^ 2, s0 * s1 * Q[0][1]);
+    put(q, q ^ 1, q ^ 4, s0 * s2 * Q[0][2]);
+    put(q, q ^ 2, q ^ 4, s1 * s2 * Q[1][2]);
+  }
+  return ok;
+}
+
+template <int P, int NB, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
+  using CF = XCfg<P, NB>;
+  constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1, PB = CF::PB, NPB = CF::NPB, LAY = CF::LAY, CP = CF::CP;
+  constexpr int NR = CF::NR;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ XElem H;
   __shared__ XBox B[125];
-  __shared__ int s_bad;
-  const XLayout LY = xh1_layout(A.ncx, A.ncy, A.ncz, kz);
+  __shared__ int s_bad, s_wc[4], s_nrow;
+  __shared__ int s_lz[NP1 + 1];  // owned-row list offset per lattice layer z
   double *XE = reinterpret_cast<double *>(smem);
-  int32_t *XG = reinterpret_cast<int32_t *>(smem + LY.off_xg);
-  double *cm = reinterpret_cast<double *>(smem + LY.off_cm);
-  const int tid = threadIdx.x;
+  int32_t *XG = reinterpret_cast<int32_t *>(smem + CF::OFF_XG);
+  double *cm = reinterpret_cast<double *>(smem + CF::OFF_CM);
+  uint16_t *rlist = reinterpret_cast<uint16_t *>(smem + CF::OFF_RL);
+  int64_t *m_out = reinterpret_cast<int64_t *>(smem + CF::OFF_MT);
+  int32_t *m_px = reinterpret_cast<int32_t *>(smem + CF::OFF_PX);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if ((int64_t)blockIdx.x >= A.nel_local) return;
   const int64_t el = A.order ? A.order[blockIdx.x] : blockIdx.x;
   {
@@ -201,16 +310,14 @@ __global__ void __launch_bounds__(128, 3) k_xh1_fill(XFillArgs A, int kz) {
     const uint2 *bs = reinterpret_cast<const uint2 *>(A.box + el * 125);
     uint2 *bd = reinterpret_cast<uint2 *>(B);
     for (int i = tid; i < 125; i += blockDim.x) bd[i] = __ldg(bs + i);
-    if (tid == 0) s_bad = 0;
+    if (tid == 0) { s_bad = 0; s_nrow = 0; }
   }
   __syncthreads();
   const int clo0 = H.clo[0], clo1 = H.clo[1], clo2 = H.clo[2];
-  const int nx = H.chi[0] - clo0 + 1, ny = H.chi[1] - clo1 + 1, nz = H.chi[2] - clo2 + 1;
-  const int npx = nx + 1, npy = ny + 1, npz = nz + 1;
-  const int npb = npx * npy * npz;
-  // point box origin = clo; index of point y: (y0-clo0) + npx ((y1-clo1) + npy (y2-clo2))
+  const int ex0 = H.chi[0] - clo0 + 1, ex1 = H.chi[1] - clo1 + 1, ex2 = H.chi[2] - clo2 + 1;  // <= NB
+  const int pbase = -(clo0 + PB * (clo1 + PB * clo2));  // box-local index of lattice point 0
   {
-    // own E-vector (contiguous, 16-byte vector loads) scattered into the point box
+    // own E-vector (contiguous, 16-byte loads) into the point box
     const double2 *xs = reinterpret_cast<const double2 *>(A.X + el * A.xstride);
     constexpr int NX2 = (3 * NPT + 1) / 2;
     for (int i = tid; i < NX2; i += blockDim.x) {
@@ -221,13 +328,16 @@ __global__ void __launch_bounds__(128, 3) k_xh1_fill(XFillArgs A, int kz) {
         if (q < 3 * NPT) {
           const int d = q / NPT, l = q - d * NPT;
           const int x0 = l % NP1, x1 = (l / NP1) % NP1, x2 = l / (NP1 * NP1);
-          XE[d * LY.npb + (x0 - clo0) + npx * ((x1 - clo1) + npy * (x2 - clo2))] = h ? v.y : v.x;
+          XE[d * NPB + pbase + x0 + PB * (x1 + PB * x2)] = h ? v.y : v.x;
         }
       }
     }
-    // neighbour points of the point box (read in the element's frame) and every point's gid
-    for (int i = tid; i < npb; i += blockDim.x) {
-      const int y[3] = {clo0 + i % npx, clo1 + (i / npx) % npy, clo2 + i / (npx * npy)};
+    // neighbour points of the element's point box [clo, chi+1] (read in the element's frame) and
+    // the global id of every point of the box
+    for (int i = tid; i < NPB; i += blockDim.x) {
+      const int u0 = i % PB, u1 = (i / PB) % PB, u2 = i / (PB * PB);
+      if (u0 > ex0 || u1 > ex1 || u2 > ex2) continue;
+      const int y[3] = {clo0 + u0, clo1 + u1, clo2 + u2};
       const XBox bx = B[ycls(y[0], P) + 5 * ycls(y[1], P) + 25 * ycls(y[2], P)];
       XG[i] = bx.g0 + bx.s[0] * y[0] + bx.s[1] * y[1] + bx.s[2] * y[2];
       const int ni = (ydelta(y[0], P) + 1) + 3 * (ydelta(y[1], P) + 1) + 9 * (ydelta(y[2], P) + 1);
@@ -237,149 +347,123 @@ __global__ void __launch_bounds__(128, 3) k_xh1_fill(XFillArgs A, int kz) {
       x_to_local(P, nb.code, y, L);
       const double *src = A.X + (int64_t)nb.el * A.xstride + L[0] + NP1 * (L[1] + NP1 * L[2]);
       XE[i] = __ldg(src);
-      XE[LY.npb + i] = __ldg(src + NPT);
-      XE[2 * LY.npb + i] = __ldg(src + 2 * NPT);
+      XE[NPB + i] = __ldg(src + NPT);
+      XE[2 * NPB + i] = __ldg(src + 2 * NPT);
     }
+    // owned rows in lattice order (z-major), compacted; s_lz[z] = first row of layer z
+    for (int l0 = 0; l0 < NPT; l0 += 128) {
+      const int l = l0 + tid;
+      bool own = false;
+      if (l < NPT) {
+        const int x0 = l % NP1, x1 = (l / NP1) % NP1, x2 = l / (NP1 * NP1);
+        own = (H.own >> (lcls(x0, P) + 3 * lcls(x1, P) + 9 * lcls(x2, P))) & 1;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, own);
+      if (lane == 0) s_wc[warp] = __popc(bal);
+      __syncthreads();
+      int off = s_nrow;
+      for (int w2 = 0; w2 < warp; ++w2) off += s_wc[w2];
+      off += __popc(bal & ((1u << lane) - 1u));
+      if (own) rlist[off] = (uint16_t)l;
+      if (l < NPT && (l % (NP1 * NP1)) == 0) s_lz[l / (NP1 * NP1)] = off;
+      __syncthreads();
+      if (tid == 0) s_nrow += s_wc[0] + s_wc[1] + s_wc[2] + s_wc[3];
+      __syncthreads();
+    }
+    if (tid == 0) s_lz[NP1] = s_nrow;
   }
   __syncthreads();
-  // owned-row box
-  int olo[3], ohi[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    bool c0 = false, c1 = false, c2 = false;
-    for (int tau = 0; tau < 27; ++tau) {
-      if (!((H.own >> tau) & 1)) continue;
-      const int c = a == 0 ? tau % 3 : (a == 1 ? (tau / 3) % 3 : tau / 9);
-      c0 |= c == 0;
-      c1 |= c == 1;
-      c2 |= c == 2;
-    }
-    olo[a] = c0 ? 0 : (c1 ? 1 : P);
-    ohi[a] = c2 ? P : (c1 ? P - 1 : 0);
-  }
-  const int NR = LY.nr, NCP = LY.ncp, lay = nx * ny;
+  // rows z in [zlo, zhi] (layers holding owned rows), in chunks of KZ layers
+  int zlo = 0, zhi = P;
+  while (zlo < P && s_lz[zlo + 1] == s_lz[zlo]) ++zlo;
+  while (zhi > zlo && s_lz[zhi + 1] == s_lz[zhi]) --zhi;
   const double alpha = A.alpha, beta = A.beta;
-  const int nchunk = (nz + kz - 1) / kz;
-  for (int ch = 0; ch < nchunk; ++ch) {
-    const int cz0 = clo2 + ch * kz;
-    const int cz1 = (cz0 + kz - 1 < H.chi[2]) ? cz0 + kz - 1 : H.chi[2];
-    if (ch > 0) __syncthreads();  // rows of the previous chunk done with the ring slots
-    // ---- cells of layers [cz0, cz1]: eight lanes per cell, one corner each
-    {
-      const int ncell = (cz1 - cz0 + 1) * lay;
-      const int items = ncell * 8;
-      const int ceil32 = (items + 31) / 32 * 32;
-      int bad = 0;
-      for (int it = tid; it < ceil32; it += blockDim.x) {
-        const bool act = it < items;
-        const int c = act ? it >> 3 : 0, q = it & 7;
-        const int ux = c % nx, uy = (c / nx) % ny, uz = c / lay;  // cell offsets in the box / chunk
-        const int cz = cz0 + uz;
-        const int pb = ux + npx * (uy + npy * (cz - clo2));
-        auto pt = [&](int v, int d) -> double {
-          return XE[d * LY.npb + pb + (v & 1) + npx * (((v >> 1) & 1) + npy * ((v >> 2) & 1))];
-        };
-        double j[3][3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const int hi = q | (1 << d), lo = q & ~(1 << d);
-#pragma unroll
-          for (int k = 0; k < 3; ++k) j[d][k] = pt(hi, k) - pt(lo, k);
-        }
-        double r[3][3];
-        cross3x(j[1], j[2], r[0]);
-        cross3x(j[2], j[0], r[1]);
-        cross3x(j[0], j[1], r[2]);
-        const double det = dot3x(j[0], r[0]);
-        const int cx = clo0 + ux, cy = clo1 + uy;
-        if (act && !(det > 0.0) && cx >= 0 && cx < P && cy >= 0 && cy < P && cz >= 0 && cz < P)
-          bad = 1 + cx + P * (cy + P * cz);
-        const double sa = 0.125 * alpha / det;
-        double Q[3][3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int e2 = d; e2 < 3; ++e2) Q[d][e2] = Q[e2][d] = sa * dot3x(r[d], r[e2]);
-        double sg[3], Qs[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) sg[d] = ((q >> d) & 1) ? 1.0 : -1.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) Qs[d] = Q[d][0] * sg[0] + Q[d][1] * sg[1] + Q[d][2] * sg[2];
-        double diag = sg[0] * Qs[0] + sg[1] * Qs[1] + sg[2] * Qs[2] + 0.125 * beta * det;
-        double edge[3], fdg[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          diag += __shfl_xor_sync(0xffffffffu, Q[d][d], 1 << d);
-          const double ev = -sg[d] * Qs[d];
-          edge[d] = ev + __shfl_xor_sync(0xffffffffu, ev, 1 << d);
-        }
-        {
-          const double f01 = sg[0] * sg[1] * Q[0][1], f02 = sg[0] * sg[2] * Q[0][2], f12 = sg[1] * sg[2] * Q[1][2];
-          fdg[0] = f01 + __shfl_xor_sync(0xffffffffu, f01, 3);
-          fdg[1] = f02 + __shfl_xor_sync(0xffffffffu, f02, 5);
-          fdg[2] = f12 + __shfl_xor_sync(0xffffffffu, f12, 6);
-        }
-        if (act) {
-          const int ci = ((cz - clo2) % NR) * lay + uy * nx + ux;
-          double *o = cm + ci;
-          const int rq = (q * (15 - q)) >> 1;
-          o[(rq + q) * NCP] = diag;
-#pragma unroll
-          for (int d = 0; d < 3; ++d)
-            if (!((q >> d) & 1)) o[(rq + (q | (1 << d))) * NCP] = edge[d];
-          auto tp = [](int a, int b) { const int i = a < b ? a : b, jj = a < b ? b : a; return ((i * (15 - i)) >> 1) + jj; };
-          if (q < (q ^ 3)) o[tp(q ^ 1, q ^ 2) * NCP] = fdg[0];
-          if (q < (q ^ 5)) o[tp(q ^ 1, q ^ 4) * NCP] = fdg[1];
-          if (q < (q ^ 6)) o[tp(q ^ 2, q ^ 4) * NCP] = fdg[2];
-          if (q < 4) o[(rq + (q ^ 7)) * NCP] = 0.0;
-        }
+  double *stage_v = cm;  // overwritten per chunk, see below
+  for (int z0 = zlo; z0 <= zhi; z0 += CF::KZ) {
+    const int z1 = (z0 + CF::KZ - 1 < zhi) ? z0 + CF::KZ - 1 : zhi;
+    // cell layers to compute now (lattice coordinates): [z0-1 (first chunk only), z1] within the box
+    int c0 = (z0 == zlo) ? z0 - 1 : z0;
+    int c1 = z1;
+    c0 = c0 < clo2 ? clo2 : c0;
+    c1 = c1 > clo2 + ex2 - 1 ? clo2 + ex2 - 1 : c1;
+    if (c1 >= c0) {
+      const int ncell = (c1 - c0 + 1) * LAY;
+      const double a8 = 0.125 * alpha, b8 = 0.125 * beta;
+      for (int c = tid; c < ncell; c += blockDim.x) {
+        const int ux = c % NB, uy = (c / NB) % NB, uz = c0 - clo2 + c / LAY;  // box-local cell
+        if (ux >= ex0 || uy >= ex1) continue;
+        const bool own = clo0 + ux >= 0 && clo0 + ux < P && clo1 + uy >= 0 && clo1 + uy < P && clo2 + uz >= 0 &&
+                         clo2 + uz < P;
+        if (!cell_h1v<NPB, PB>(XE, ux + PB * (uy + PB * uz), a8, b8, cm + ((uz % NR) * LAY + uy * NB + ux) * CP) && own)
+          s_bad = 1 + (clo0 + ux) + P * ((clo1 + uy) + P * (clo2 + uz));
       }
-      if (bad) s_bad = bad;
     }
     __syncthreads();
-    if (s_bad && tid == 0) xreport(A.err, 2, A.elem_begin + el, s_bad - 1);
-    // ---- rows of layers [cz0, cz1] (+ cz1 + 1 after the last cell layer), owned only
-    int rz0 = cz0, rz1 = (ch == nchunk - 1) ? cz1 + 1 : cz1;
-    rz0 = rz0 < olo[2] ? olo[2] : rz0;
-    rz1 = rz1 > ohi[2] ? ohi[2] : rz1;
-    const int rnx = ohi[0] - olo[0] + 1, rny = ohi[1] - olo[1] + 1;
-    const int nrow = (rz1 >= rz0) ? rnx * rny * (rz1 - rz0 + 1) : 0;
-    for (int ri = tid; ri < nrow; ri += blockDim.x) {
-      const int x[3] = {olo[0] + ri % rnx, olo[1] + (ri / rnx) % rny, rz0 + ri / (rnx * rny)};
-      const int tau = lcls(x[0], P) + 3 * lcls(x[1], P) + 9 * lcls(x[2], P);
-      if (!((H.own >> tau) & 1)) continue;
-      const int px = (x[0] - clo0) + npx * ((x[1] - clo1) + npy * (x[2] - clo2));
-      const int g = XG[px];
-      const int64_t r = (int64_t)g - A.row_begin;
-      const int64_t out = __ldg(A.row_ptr + r);
+    if (s_bad && tid == 0) { xreport(A.err, 2, A.elem_begin + el, s_bad - 1); s_bad = 0; }
+    // ---- rows of layers [z0, z1]: one thread per owned row, values from the <= 8 cells
+    const int rb = s_lz[z0], nrow = s_lz[z1 + 1] - rb;
+    double acc[27];
+    uint32_t pw[8];
+    int px = 0;
+    int64_t out = 0;
+    const bool hasrow = tid < nrow;
+    if (hasrow) {
+      const int l = rlist[rb + tid];
+      const int x0 = l % NP1, x1 = (l / NP1) % NP1, x2 = l / (NP1 * NP1);
+      px = pbase + x0 + PB * (x1 + PB * x2);
+      const int64_t r = (int64_t)XG[px] - A.row_begin;
+      out = __ldg(A.row_ptr + r);
       const uint4 *pp = reinterpret_cast<const uint4 *>(A.pos + r * XPOS_W);
-      const uint4 pa = __ldcs(pp), pbv = __ldcs(pp + 1);
-      const uint32_t pw[8] = {pa.x, pa.y, pa.z, pa.w, pbv.x, pbv.y, pbv.z, pbv.w};
-      double acc[27];
+      const uint4 pa = __ldcs(pp), pv = __ldcs(pp + 1);
+      pw[0] = pa.x; pw[1] = pa.y; pw[2] = pa.z; pw[3] = pa.w;
+      pw[4] = pv.x; pw[5] = pv.y; pw[6] = pv.z; pw[7] = pv.w;
 #pragma unroll
-      for (int j = 0; j < 27; ++j) acc[j] = 0.0;
+      for (int jj = 0; jj < 27; ++jj) acc[jj] = 0.0;
+      const int u0 = x0 - clo0, u1 = x1 - clo1, u2 = x2 - clo2;  // box-local lattice point
 #pragma unroll
       for (int o = 0; o < 8; ++o) {
         const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
-        const int cx = x[0] - ox, cy = x[1] - oy, cz = x[2] - oz;
-        if (cx < clo0 || cx > H.chi[0] || cy < clo1 || cy > H.chi[1] || cz < clo2 || cz > H.chi[2]) continue;
-        const int ci = ((cz - clo2) % NR) * lay + (cy - clo1) * nx + (cx - clo0);
+        const int cx = u0 - ox, cy = u1 - oy, cz = u2 - oz;
+        if (cx < 0 || cx >= ex0 || cy < 0 || cy >= ex1 || cz < 0 || cz >= ex2) continue;
+        const double *ce = cm + ((cz % NR) * LAY + cy * NB + cx) * CP;
 #pragma unroll
         for (int jc = 0; jc < 8; ++jc) {
+          if (body_diag(o, jc)) continue;
           const int dx = (jc & 1) - ox, dy = ((jc >> 1) & 1) - oy, dz = ((jc >> 2) & 1) - oz;
-          acc[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)] += cm[tri(8, o, jc) * NCP + ci];
+          acc[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)] += ce[cidx(o, jc)];
         }
-      }
-#pragma unroll
-      for (int j = 0; j < 27; ++j) {
-        const int ps = (int)((pw[j >> 2] >> (8 * (j & 3))) & 255u);
-        if (ps != 255) {
-          const int dj = (j % 3 - 1) + npx * (((j / 3) % 3 - 1) + npy * (j / 9 - 1));
-          __stcs(A.col + out + ps, XG[px + dj]);
-          __stcs(A.val + out + ps, acc[j]);
-        }
+        asm volatile("" ::: "memory");  // one cell's loads in flight at a time (register pressure)
       }
     }
+    __syncthreads();  // every row has read the cells: stage over the cell storage
+    // stage: ONE chunk -> all cells; ring -> the slot of layer z0-1 (next chunk's first write)
+    stage_v = CF::ONE ? cm : cm + (((z0 - 1 - clo2) % NR + NR) % NR) * LAY * CP;
+    int8_t *stage_j = reinterpret_cast<int8_t *>(stage_v + CF::MAXROW * 27);  // point offset of the column
+    if (hasrow) {
+      int len = 0;
+#pragma unroll
+      for (int jj = 0; jj < 27; ++jj) {
+        const int ps = (int)((pw[jj >> 2] >> (8 * (jj & 3))) & 255u);
+        if (ps != 255) {
+          stage_v[tid * 27 + ps] = acc[jj];
+          stage_j[tid * 27 + ps] = (int8_t)((jj % 3 - 1) + PB * ((jj / 3) % 3 - 1) + PB * PB * (jj / 9 - 1));
+          ++len;
+        }
+      }
+      m_out[tid] = out;
+      m_px[tid] = px | (len << 16);
+    }
+    __syncthreads();
+    // coalesced write-out: one warp per row, lane = final column position
+    for (int row = warp; row < nrow; row += 4) {
+      const int mp = m_px[row];
+      if (lane < (mp >> 16)) {
+        const int64_t o = m_out[row] + lane;
+        __stcs(A.col + o, XG[(mp & 0xffff) + (int)stage_j[row * 27 + lane]]);
+        __stcs(A.val + o, stage_v[row * 27 + lane]);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -391,18 +475,24 @@ static cudaError_t xh1_setup_p(const XSetupArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int P>
-static cudaError_t xh1_fill_p(const XFillArgs &a, cudaStream_t st, int *smem_out) {
-  // largest z-chunk whose shared memory keeps >= 3 CTAs per SM (<= 72 KB dynamic)
-  int kz = a.ncz;
-  while (kz > 1 && xh1_layout(a.ncx, a.ncy, a.ncz, kz).bytes > 72 * 1024) --kz;
-  const int smem = xh1_layout(a.ncx, a.ncy, a.ncz, kz).bytes;
+template <int P, int NB>
+static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_out) {
+  using CF = XCfg<P, NB>;
+  constexpr int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
-  cudaFuncSetAttribute(k_xh1_fill<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_xh1_fill<P>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  k_xh1_fill<P><<<(unsigned)a.nel_local, 128, smem, st>>>(a, kz);
+  constexpr int MINB = (smem <= 44 * 1024) ? 4 : 3;
+  auto k = k_xh1_fill<P, NB, MINB>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  k<<<(unsigned)a.nel_local, 128, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+template <int P>
+static cudaError_t xh1_fill_p(const XFillArgs &a, cudaStream_t st, int *smem_out) {
+  if (a.ncx <= P + 1 && a.ncy <= P + 1 && a.ncz <= P + 1) return xh1_fill_nb<P, P + 1>(a, st, smem_out);
+  return xh1_fill_nb<P, P + 2>(a, st, smem_out);
 }
 
 cudaError_t launch_xh1_setup(int p, const XSetupArgs &a, cudaStream_t st) {
