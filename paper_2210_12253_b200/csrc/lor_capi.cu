@@ -96,6 +96,8 @@ struct SpaceDev {
   bool xok = false;
   XElem *xe = nullptr;
   XBox *xbox = nullptr;
+  int32_t *xmap = nullptr;
+  int2 *xhalo = nullptr;
   uint8_t *xpos = nullptr;
   int xc[3] = {0, 0, 0};
 };
@@ -250,8 +252,14 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   CUDA_TRY(c, cudaSetDevice(c->device));
   c->nphase = 0;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
-  lor_status st = run_count_scan(c, s, out->row_ptr);
-  if (st) return st;
+  lor_status st = LOR_OK;
+  if (S.xok && quad == LOR_QUAD_VERTEX) {  // row counts from the extended-frame position table
+    CUDA_TRY(c, launch_scan(S.cnt, out->row_ptr, S.n_local, S.scan_status, S.tile_ctr, c->stream, S.xpos));
+    c->launches++;
+  } else {
+    st = run_count_scan(c, s, out->row_ptr);
+    if (st) return st;
+  }
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   if (S.xok && quad == LOR_QUAD_VERTEX) {  // extended-frame path: every owned row in one pass
     XFillArgs x{};
@@ -259,7 +267,8 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     x.elem_begin = c->elem_begin;
     x.order = c->order;
     x.xe = S.xe;
-    x.box = S.xbox;
+    x.xmap = S.xmap;
+    x.xhalo = S.xhalo;
     x.pos = S.xpos;
     x.X = c->X;
     x.xstride = c->xstride;
@@ -695,9 +704,13 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     SpaceDev &S = c->sp[SP_H1];
     std::vector<XElem> xe;
     std::string why;
-    if (xframe_build(plan, A.elem_vert, xe, S.xc, &why)) {
+    if (c->nel_local * c->xstride >= (int64_t(1) << 31)) {
+      why = "E-vector index exceeds int32";
+    } else if (xframe_build(plan, A.elem_vert, xe, S.xc, &why)) {
       if (dev_upload(c, &S.xe, xe.data(), xe.size()) != cudaSuccess ||
           dev_alloc(c, &S.xbox, (size_t)c->nel_local * 125) != cudaSuccess ||
+          dev_alloc(c, &S.xmap, (size_t)c->nel_local * xmap_points(A.p, S.xc)) != cudaSuccess ||
+          dev_alloc(c, &S.xhalo, (size_t)c->nel_local * (xmap_points(A.p, S.xc) - (int64_t)(A.p + 1) * (A.p + 1) * (A.p + 1))) != cudaSuccess ||
           dev_alloc(c, &S.xpos, (size_t)std::max<int64_t>(S.n_local, 1) * XPOS_W) != cudaSuccess)
         return bail(LOR_ERR_OUT_OF_MEMORY, "xframe");
       if (cudaMemset(S.xpos, 0xff, (size_t)std::max<int64_t>(S.n_local, 1) * XPOS_W) != cudaSuccess)
@@ -711,6 +724,10 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
       xa.row_begin = S.row_begin;
       xa.cnt = S.cnt;
       xa.box = S.xbox;
+      xa.nb = xfill_nb(A.p, S.xc);
+      xa.xmap = S.xmap;
+      xa.xhalo = S.xhalo;
+      xa.xstride = c->xstride;
       xa.pos = S.xpos;
       xa.err = c->err;
       if (cudaMemset(c->err, 0, 4 * sizeof(int)) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe");

@@ -191,6 +191,12 @@ bool xframe_build(const HostPlan &plan, const int64_t *EV, std::vector<XElem> &o
       X.clo[a] = (int8_t)((lo && ex[fm]) ? -1 : 0);
       X.chi[a] = (int8_t)((hi && ex[fp]) ? p : p - 1);
       cmax[a] = std::max(cmax[a], X.chi[a] - X.clo[a] + 1);
+      // owned-row bounding box along a (class 0 -> x = 0, 1 -> [1, p-1], 2 -> x = p)
+      bool c1 = false;
+      for (int tau = 0; tau < 27; ++tau)
+        if ((X.own >> tau) & 1) c1 = c1 || (a == 0 ? tau % 3 : a == 1 ? (tau / 3) % 3 : tau / 9) == 1;
+      X.olo[a] = (int8_t)(lo ? 0 : (c1 ? 1 : p));
+      X.ohi[a] = (int8_t)(hi ? p : (c1 ? p - 1 : 0));
     }
     for (int i = 0; i < 27; ++i) {
       X.nbr[i].el = -1;

@@ -33,7 +33,8 @@ struct __align__(16) XElem {
   uint32_t own;      // bit tau: this element writes the rows of entity slot tau (TF_MIN & TF_OWNED)
   int8_t clo[3];     // cell box [clo, chi] per axis in extended-frame cell coordinates
   int8_t chi[3];
-  uint8_t pad[6];
+  int8_t olo[3];     // bounding box [olo, ohi] of the owned rows (lattice coordinates)
+  int8_t ohi[3];
   XNbr nbr[27];
   uint8_t pad2[8];
 };
@@ -58,6 +59,13 @@ struct XSetupArgs {
   int64_t row_begin;
   const int32_t *cnt;  // row lengths from k_count (consistency check)
   XBox *box;           // [nel_local][125]
+  int nb;              // cell-box extent the fill kernel is built for (p+1 or p+2)
+  int32_t *xmap;       // [nel_local][(nb+1)^3] extended element restriction: global id of every point
+                       // of the element's point box [clo, clo+nb]^3 (-1 outside [clo, chi+1])
+  int2 *xhalo;         // [nel_local][(nb+1)^3 - (p+1)^3] coordinate gather list of the box points outside
+                       // the element: {E-vector index of the x component (-1: outside [clo, chi+1]),
+                       // point index in the box}
+  int64_t xstride;
   uint8_t *pos;        // [n_local][XPOS_W]
   int *err;            // set to 1 on any inconsistency
 };
@@ -66,7 +74,8 @@ struct XFillArgs {
   int64_t nel_local, elem_begin;
   const int32_t *order;
   const XElem *xe;
-  const XBox *box;
+  const int32_t *xmap;
+  const int2 *xhalo;
   const uint8_t *pos;
   const double *X;
   int64_t xstride;
@@ -83,6 +92,15 @@ struct XFillArgs {
 struct HostPlan;
 bool xframe_build(const HostPlan &plan, const int64_t *elem_vert, std::vector<XElem> &out, int cmax[3],
                   std::string *why);
+
+// cell-box extent the fill kernel is instantiated for, and points per element of the extended map
+inline int xfill_nb(int p, const int cmax[3]) {
+  return (cmax[0] <= p + 1 && cmax[1] <= p + 1 && cmax[2] <= p + 1) ? p + 1 : p + 2;
+}
+inline int64_t xmap_points(int p, const int cmax[3]) {
+  const int pb = xfill_nb(p, cmax) + 1;
+  return (int64_t)pb * pb * pb;
+}
 
 cudaError_t launch_xh1_setup(int p, const XSetupArgs &a, cudaStream_t st);
 cudaError_t launch_xh1_fill(int p, const XFillArgs &a, cudaStream_t st, int *smem_out);

@@ -118,6 +118,44 @@ __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
     okg = okg && bx.valid;
     return bx.g0 + bx.s[0] * y[0] + bx.s[1] * y[1] + bx.s[2] * y[2];
   };
+  {
+    const int pb = A.nb + 1, npb = pb * pb * pb;
+    for (int i = threadIdx.x; i < npb; i += blockDim.x) {
+      const int u[3] = {i % pb, (i / pb) % pb, i / (pb * pb)};
+      bool in = true;
+      for (int a = 0; a < 3; ++a) in = in && u[a] <= H.chi[a] - H.clo[a] + 1;
+      const int y[3] = {H.clo[0] + u[0], H.clo[1] + u[1], H.clo[2] + u[2]};
+      bool okg = true;
+      const int g = in ? gid(y, okg) : -1;
+      if (!okg) atomicExch(A.err, 1);
+      A.xmap[e * npb + i] = g;
+    }
+    // coordinate gather list of the box points that lie in neighbours (box lexicographic order)
+    if (threadIdx.x == 0) {
+      constexpr int NP1c = P + 1;
+      const int hc = npb - NP1c * NP1c * NP1c;
+      int k = 0;
+      for (int i = 0; i < npb; ++i) {
+        const int u[3] = {i % pb, (i / pb) % pb, i / (pb * pb)};
+        const int y[3] = {H.clo[0] + u[0], H.clo[1] + u[1], H.clo[2] + u[2]};
+        if (y[0] >= 0 && y[0] <= P && y[1] >= 0 && y[1] <= P && y[2] >= 0 && y[2] <= P) continue;
+        int2 ent = make_int2(-1, i);
+        bool in = true;
+        for (int a = 0; a < 3; ++a) in = in && u[a] <= H.chi[a] - H.clo[a] + 1;
+        if (in) {
+          const int ni = (ydelta(y[0], P) + 1) + 3 * (ydelta(y[1], P) + 1) + 9 * (ydelta(y[2], P) + 1);
+          const XNbr nb = H.nbr[ni];
+          int L[3];
+          x_to_local(P, nb.code, y, L);
+          if (nb.el < 0) atomicExch(A.err, 1);
+          ent.x = (int)((int64_t)nb.el * A.xstride + L[0] + NP1c * (L[1] + NP1c * L[2]));
+        }
+        if (k < hc) A.xhalo[e * hc + k] = ent;
+        ++k;
+      }
+      if (k != hc) atomicExch(A.err, 1);
+    }
+  }
   constexpr int NP1 = P + 1;
   for (int l = threadIdx.x; l < NP1 * NP1 * NP1; l += blockDim.x) {
     const int x[3] = {l % NP1, (l / NP1) % NP1, l / (NP1 * NP1)};
@@ -181,8 +219,7 @@ struct XCfg {
   static constexpr int MAXROW = KZ * NP1 * NP1;     // rows per chunk (<= 125 for P <= 4, (P+1)^2 else)
   static constexpr int OFF_XG = 3 * NPB * 8;
   static constexpr int OFF_CM = (OFF_XG + NPB * 4 + 15) / 16 * 16;
-  static constexpr int OFF_RL = OFF_CM + NR * LAY * CP * 8;              // owned-row list uint16[NP1^3]
-  static constexpr int OFF_MT = (OFF_RL + 2 * NP1 * NP1 * NP1 + 15) / 16 * 16;  // per chunk row: out int64
+  static constexpr int OFF_MT = OFF_CM + NR * LAY * CP * 8;              // per chunk row: out int64
   static constexpr int OFF_PX = OFF_MT + 8 * MAXROW;                      // px int16 | len << 16 (int32)
   static constexpr int SMEM = OFF_PX + 4 * MAXROW;
   // staging of a chunk's rows for the coalesced write-out: values in final position order and the
@@ -204,7 +241,9 @@ __host__ __device__ constexpr bool body_diag(int a, int b) { return (a ^ b) == 7
 
 // 1/x for x > 0: float seed + two Newton steps (relative error ~1e-28 before rounding)
 __device__ __forceinline__ double rcp_pos(double x) {
-  double r = (double)__frcp_rn((float)x);
+  float rf;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)x));
+  double r = (double)rf;
   double e = fma(-x, r, 1.0);
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
@@ -260,7 +299,7 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
     cross3x(j[0], j[1], r[2]);
     const double det = dot3x(j[0], r[0]);
     ok = ok && det > 0.0;
-    const double sa = a8 * ((fabs(det) > 1e-30) ? rcp_pos(det) : 1.0 / det);
+    const double sa = a8 * rcp_pos(det);  // |det| within float range (cell volumes > 1e-37)
     double Q[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -290,93 +329,56 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1, PB = CF::PB, NPB = CF::NPB, LAY = CF::LAY, CP = CF::CP;
   constexpr int NR = CF::NR;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ XElem H;
-  __shared__ XBox B[125];
-  __shared__ int s_bad, s_wc[4], s_nrow;
-  __shared__ int s_lz[NP1 + 1];  // owned-row list offset per lattice layer z
+  __shared__ int s_bad;
   double *XE = reinterpret_cast<double *>(smem);
   int32_t *XG = reinterpret_cast<int32_t *>(smem + CF::OFF_XG);
   double *cm = reinterpret_cast<double *>(smem + CF::OFF_CM);
-  uint16_t *rlist = reinterpret_cast<uint16_t *>(smem + CF::OFF_RL);
   int64_t *m_out = reinterpret_cast<int64_t *>(smem + CF::OFF_MT);
   int32_t *m_px = reinterpret_cast<int32_t *>(smem + CF::OFF_PX);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if ((int64_t)blockIdx.x >= A.nel_local) return;
   const int64_t el = A.order ? A.order[blockIdx.x] : blockIdx.x;
-  {
-    const int4 *src = reinterpret_cast<const int4 *>(A.xe + el);
-    int4 *dst = reinterpret_cast<int4 *>(&H);
-    for (int i = tid; i < (int)(sizeof(XElem) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
-    const uint2 *bs = reinterpret_cast<const uint2 *>(A.box + el * 125);
-    uint2 *bd = reinterpret_cast<uint2 *>(B);
-    for (int i = tid; i < 125; i += blockDim.x) bd[i] = __ldg(bs + i);
-    if (tid == 0) { s_bad = 0; s_nrow = 0; }
-  }
-  __syncthreads();
-  const int clo0 = H.clo[0], clo1 = H.clo[1], clo2 = H.clo[2];
-  const int ex0 = H.chi[0] - clo0 + 1, ex1 = H.chi[1] - clo1 + 1, ex2 = H.chi[2] - clo2 + 1;  // <= NB
+  // element header word {own, clo, chi, olo, ohi} read by every thread (broadcast); all loads of the
+  // prologue (extended restriction, own E-vector, neighbour points) are independent of each other
+  // and complete at one barrier
+  const int4 hw = __ldg(reinterpret_cast<const int4 *>(A.xe + el));
+  const int clo0 = (int8_t)(hw.y & 255), clo1 = (int8_t)((hw.y >> 8) & 255), clo2 = (int8_t)((hw.y >> 16) & 255);
+  const int ex0 = (int8_t)((hw.y >> 24) & 255) - clo0 + 1, ex1 = (int8_t)(hw.z & 255) - clo1 + 1,
+            ex2 = (int8_t)((hw.z >> 8) & 255) - clo2 + 1;  // cell-box extents (<= NB)
+  const int olo0 = (int8_t)((hw.z >> 16) & 255), olo1 = (int8_t)((hw.z >> 24) & 255), olo2 = (int8_t)(hw.w & 255);
+  const int ohi0 = (int8_t)((hw.w >> 8) & 255), ohi1 = (int8_t)((hw.w >> 16) & 255), ohi2 = (int8_t)((hw.w >> 24) & 255);
+  const uint32_t own = (uint32_t)hw.x;
   const int pbase = -(clo0 + PB * (clo1 + PB * clo2));  // box-local index of lattice point 0
   {
-    // own E-vector (contiguous, 16-byte loads) into the point box
-    const double2 *xs = reinterpret_cast<const double2 *>(A.X + el * A.xstride);
-    constexpr int NX2 = (3 * NPT + 1) / 2;
-    for (int i = tid; i < NX2; i += blockDim.x) {
-      const double2 v = __ldg(xs + i);
+    if (tid == 0) s_bad = 0;
+    // extended element restriction (setup): global id of every point of the box
+    const int32_t *xm = A.xmap + el * NPB;
+    for (int i = tid; i < NPB; i += blockDim.x) XG[i] = __ldg(xm + i);
+    // own E-vector, one lattice x-row per thread
+    const double *xs = A.X + el * A.xstride;
+    for (int rr = tid; rr < 3 * NP1 * NP1; rr += blockDim.x) {
+      const int d = rr / (NP1 * NP1), x12 = rr - d * NP1 * NP1, x1 = x12 % NP1, x2 = x12 / NP1;
+      const double *src = xs + d * NPT + x12 * NP1;
+      double *dst = XE + d * NPB + pbase + PB * (x1 + PB * x2);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = 2 * i + h;
-        if (q < 3 * NPT) {
-          const int d = q / NPT, l = q - d * NPT;
-          const int x0 = l % NP1, x1 = (l / NP1) % NP1, x2 = l / (NP1 * NP1);
-          XE[d * NPB + pbase + x0 + PB * (x1 + PB * x2)] = h ? v.y : v.x;
-        }
+      for (int i = 0; i < NP1; ++i) dst[i] = __ldg(src + i);
+    }
+    // neighbour points of the box (setup gather list)
+    constexpr int HC = NPB - NPT;
+    const int2 *hl = A.xhalo + el * HC;
+    for (int h = tid; h < HC; h += blockDim.x) {
+      const int2 hv = __ldg(hl + h);
+      if (hv.x >= 0) {
+        XE[hv.y] = __ldg(A.X + hv.x);
+        XE[NPB + hv.y] = __ldg(A.X + hv.x + NPT);
+        XE[2 * NPB + hv.y] = __ldg(A.X + hv.x + 2 * NPT);
       }
     }
-    // neighbour points of the element's point box [clo, chi+1] (read in the element's frame) and
-    // the global id of every point of the box
-    for (int i = tid; i < NPB; i += blockDim.x) {
-      const int u0 = i % PB, u1 = (i / PB) % PB, u2 = i / (PB * PB);
-      if (u0 > ex0 || u1 > ex1 || u2 > ex2) continue;
-      const int y[3] = {clo0 + u0, clo1 + u1, clo2 + u2};
-      const XBox bx = B[ycls(y[0], P) + 5 * ycls(y[1], P) + 25 * ycls(y[2], P)];
-      XG[i] = bx.g0 + bx.s[0] * y[0] + bx.s[1] * y[1] + bx.s[2] * y[2];
-      const int ni = (ydelta(y[0], P) + 1) + 3 * (ydelta(y[1], P) + 1) + 9 * (ydelta(y[2], P) + 1);
-      if (ni == 13) continue;
-      const XNbr nb = H.nbr[ni];
-      int L[3];
-      x_to_local(P, nb.code, y, L);
-      const double *src = A.X + (int64_t)nb.el * A.xstride + L[0] + NP1 * (L[1] + NP1 * L[2]);
-      XE[i] = __ldg(src);
-      XE[NPB + i] = __ldg(src + NPT);
-      XE[2 * NPB + i] = __ldg(src + 2 * NPT);
-    }
-    // owned rows in lattice order (z-major), compacted; s_lz[z] = first row of layer z
-    for (int l0 = 0; l0 < NPT; l0 += 128) {
-      const int l = l0 + tid;
-      bool own = false;
-      if (l < NPT) {
-        const int x0 = l % NP1, x1 = (l / NP1) % NP1, x2 = l / (NP1 * NP1);
-        own = (H.own >> (lcls(x0, P) + 3 * lcls(x1, P) + 9 * lcls(x2, P))) & 1;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, own);
-      if (lane == 0) s_wc[warp] = __popc(bal);
-      __syncthreads();
-      int off = s_nrow;
-      for (int w2 = 0; w2 < warp; ++w2) off += s_wc[w2];
-      off += __popc(bal & ((1u << lane) - 1u));
-      if (own) rlist[off] = (uint16_t)l;
-      if (l < NPT && (l % (NP1 * NP1)) == 0) s_lz[l / (NP1 * NP1)] = off;
-      __syncthreads();
-      if (tid == 0) s_nrow += s_wc[0] + s_wc[1] + s_wc[2] + s_wc[3];
-      __syncthreads();
-    }
-    if (tid == 0) s_lz[NP1] = s_nrow;
   }
   __syncthreads();
-  // rows z in [zlo, zhi] (layers holding owned rows), in chunks of KZ layers
-  int zlo = 0, zhi = P;
-  while (zlo < P && s_lz[zlo + 1] == s_lz[zlo]) ++zlo;
-  while (zhi > zlo && s_lz[zhi + 1] == s_lz[zhi]) --zhi;
+  // rows: the owned-row bounding box [olo, ohi], z-layers in chunks of KZ
+  const int zlo = olo2, zhi = ohi2;
+  const int rnx = ohi0 - olo0 + 1, rny = ohi1 - olo1 + 1;
   const double alpha = A.alpha, beta = A.beta;
   double *stage_v = cm;  // overwritten per chunk, see below
   for (int z0 = zlo; z0 <= zhi; z0 += CF::KZ) {
@@ -401,15 +403,21 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     __syncthreads();
     if (s_bad && tid == 0) { xreport(A.err, 2, A.elem_begin + el, s_bad - 1); s_bad = 0; }
     // ---- rows of layers [z0, z1]: one thread per owned row, values from the <= 8 cells
-    const int rb = s_lz[z0], nrow = s_lz[z1 + 1] - rb;
+    const int nrow = rnx * rny * (z1 - z0 + 1);
     double acc[27];
     uint32_t pw[8];
     int px = 0;
     int64_t out = 0;
-    const bool hasrow = tid < nrow;
+    bool hasrow = false;
+    int x0 = 0, x1 = 0, x2 = 0;
+    if (tid < nrow) {
+      const int t = tid / rnx;
+      x0 = olo0 + tid - t * rnx;
+      x1 = olo1 + t % rny;
+      x2 = z0 + t / rny;
+      hasrow = (own >> (lcls(x0, P) + 3 * lcls(x1, P) + 9 * lcls(x2, P))) & 1;
+    }
     if (hasrow) {
-      const int l = rlist[rb + tid];
-      const int x0 = l % NP1, x1 = (l / NP1) % NP1, x2 = l / (NP1 * NP1);
       px = pbase + x0 + PB * (x1 + PB * x2);
       const int64_t r = (int64_t)XG[px] - A.row_begin;
       out = __ldg(A.row_ptr + r);
@@ -452,6 +460,8 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       }
       m_out[tid] = out;
       m_px[tid] = px | (len << 16);
+    } else if (tid < nrow) {
+      m_px[tid] = 0;
     }
     __syncthreads();
     // coalesced write-out: one warp per row, lane = final column position
@@ -481,7 +491,7 @@ static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_ou
   constexpr int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
-  constexpr int MINB = (smem <= 44 * 1024) ? 4 : 3;
+  constexpr int MINB = (smem <= 44 * 1024) ? 5 : 3;
   auto k = k_xh1_fill<P, NB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
