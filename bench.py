@@ -289,7 +289,8 @@ def main():
                        "l2": "flushed (512 MiB write) before every timed step",
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
             "hbm_gbs": B["call"] / (t_ms * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "fill step a6 = k_assemble + k_merge_rows", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": ("fill step a6 = k_xh1_fill" if ctx.fill_path(space) == 1 else
+                                                    "fill step a6 = k_assemble + k_merge_rows"), "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": traffic, "algorithmic_bytes_per_launch": B["k_assemble"], "avg_launch_ms": asm_ms},
             "phases_ms": dict(zip(["count+scan", "k_assemble", "k_merge_rows", "exchange+finalize"], ph)),

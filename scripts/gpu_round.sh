@@ -12,5 +12,5 @@ for cfg in ${EXTRA_CFGS}; do
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>> gpurun_out/ncu.err; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_assemble|k_merge_rows" -s 3 -c 2 -f -o gpurun_out/prof_c2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_assemble|k_merge_rows|k_xh1_fill" -s 3 -c 2 -f -o gpurun_out/prof_c2 \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>> gpurun_out/ncu.err; echo "ncu full rc=$?"
