@@ -99,6 +99,7 @@ struct SpaceDev {
   int32_t *xmap = nullptr;
   int2 *xhalo = nullptr;
   uint8_t *xpos = nullptr;
+  uint32_t *xpiece = nullptr;
   int xc[3] = {0, 0, 0};
 };
 
@@ -270,6 +271,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     x.xmap = S.xmap;
     x.xhalo = S.xhalo;
     x.pos = S.xpos;
+    x.piece = S.xpiece;
     x.X = c->X;
     x.xstride = c->xstride;
     x.row_begin = S.row_begin;
@@ -713,6 +715,11 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
           dev_alloc(c, &S.xhalo, (size_t)c->nel_local * (xmap_points(A.p, S.xc) - (int64_t)(A.p + 1) * (A.p + 1) * (A.p + 1))) != cudaSuccess ||
           dev_alloc(c, &S.xpos, (size_t)std::max<int64_t>(S.n_local, 1) * XPOS_W) != cudaSuccess)
         return bail(LOR_ERR_OUT_OF_MEMORY, "xframe");
+      int kz = 0, maxrow = 0, maxp = 0, nchunk = 0;
+      xfill_geom(A.p, S.xc, &kz, &maxrow, &maxp, &nchunk);
+      const size_t npiece = (size_t)c->nel_local * nchunk * (1 + maxp);
+      if (nchunk <= 0 || dev_alloc(c, &S.xpiece, npiece) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "xframe");
+      if (cudaMemset(S.xpiece, 0, npiece * sizeof(uint32_t)) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe");
       if (cudaMemset(S.xpos, 0xff, (size_t)std::max<int64_t>(S.n_local, 1) * XPOS_W) != cudaSuccess)
         return bail(LOR_ERR_CUDA, "xframe");
       // S.cnt still holds the H1 row counts of the setup count pass
@@ -729,6 +736,11 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
       xa.xhalo = S.xhalo;
       xa.xstride = c->xstride;
       xa.pos = S.xpos;
+      xa.piece = S.xpiece;
+      xa.kz = kz;
+      xa.maxrow = maxrow;
+      xa.maxp = maxp;
+      xa.nchunk = nchunk;
       xa.err = c->err;
       if (cudaMemset(c->err, 0, 4 * sizeof(int)) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe");
       if (launch_xh1_setup(A.p, xa, c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe setup");

@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(128) k_count(CountArgs A) {
 constexpr int SCAN_T = 128, SCAN_I = 16, SCAN_TILE = SCAN_T * SCAN_I;
 constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
 
-// pos != NULL: row counts are the numbers of valid (!= 255) slot positions of the extended-frame
-// position table rows (lor_xframe.h, 32 bytes per row) instead of cnt[]
+// pos != NULL: row counts are the numbers of valid (!= 255) slot positions (bytes 0-27) of the
+// extended-frame position table rows (lor_xframe.h, 32 bytes per row) instead of cnt[]
 __global__ void __launch_bounds__(SCAN_T) k_scan(const int32_t *__restrict__ cnt, int64_t *__restrict__ row_ptr, int64_t n,
                                                  unsigned long long *status, unsigned int *tile_ctr,
                                                  const uint8_t *__restrict__ pos) {
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(const int32_t *__restrict__ cnt
         const uint4 a = __ldcs(pr), b = __ldcs(pr + 1);
         const unsigned w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int q = 0; q < 8; ++q) c += 4 - (__popc(__vcmpeq4(w[q], 0xffffffffu)) >> 3);
+        for (int q = 0; q < 7; ++q) c += 4 - (__popc(__vcmpeq4(w[q], 0xffffffffu)) >> 3);  // word 7: stage offset
       }
       v[i] = c;
     } else {

@@ -49,7 +49,14 @@ struct XBox {
 };
 static_assert(sizeof(XBox) == 8, "layout");
 
-constexpr int XPOS_W = 32;  // position-table row: final CSR position of each of the 27 stencil slots
+constexpr int XPOS_W = 32;  // position-table row: bytes 0-26 final CSR position of each of the 27 stencil
+                            // slots (255: none), byte 27 unused, bytes 28-29 the row's offset in the
+                            // fill kernel's staging area (its write-out order), bytes 30-31 unused
+
+// write-out piece (one per <= 128 consecutive CSR entries of one run of consecutive owned rows of a
+// chunk): bits 0-11 staging offset of the first entry, 12-18 chunk row (thread) of the run's first
+// row, 19-26 number of entries
+constexpr int XPIECE_N = 128;
 
 struct XSetupArgs {
   int64_t nel_local;
@@ -67,6 +74,8 @@ struct XSetupArgs {
                        // point index in the box}
   int64_t xstride;
   uint8_t *pos;        // [n_local][XPOS_W]
+  uint32_t *piece;     // [nel_local][nchunk][1 + maxp]: piece count, then the write-out pieces
+  int kz, maxrow, maxp, nchunk;  // fill-kernel chunking (xfill_geom)
   int *err;            // set to 1 on any inconsistency
 };
 
@@ -77,6 +86,8 @@ struct XFillArgs {
   const int32_t *xmap;
   const int2 *xhalo;
   const uint8_t *pos;
+  const uint32_t *piece;
+  int maxp, nchunk;
   const double *X;
   int64_t xstride;
   int64_t row_begin;
@@ -101,6 +112,10 @@ inline int64_t xmap_points(int p, const int cmax[3]) {
   const int pb = xfill_nb(p, cmax) + 1;
   return (int64_t)pb * pb * pb;
 }
+
+// chunking of the fill kernel instantiated for (p, cmax): row layers per chunk, rows per chunk,
+// write-out pieces per chunk (capacity), chunks per element
+void xfill_geom(int p, const int cmax[3], int *kz, int *maxrow, int *maxp, int *nchunk);
 
 cudaError_t launch_xh1_setup(int p, const XSetupArgs &a, cudaStream_t st);
 cudaError_t launch_xh1_fill(int p, const XFillArgs &a, cudaStream_t st, int *smem_out);

@@ -17,6 +17,10 @@
 #include "lor_device.cuh"
 #include "lor_xframe.h"
 
+#ifndef XMINB
+#define XMINB 5  // CTAs per SM of the one-chunk fill kernels (p <= 4): 96 registers
+#endif
+
 namespace lorb {
 
 namespace {
@@ -52,11 +56,52 @@ __device__ __forceinline__ double dot3x(const double *a, const double *b) { retu
 
 }  // namespace
 
+// ============================================================================== fill kernel
+// Compile-time geometry of the shared-memory boxes.  NB = cell-box extent per axis the kernel is
+// built for: P+1 (every element of the mesh has a box of at most P+1 cells per axis: elements
+// owning entities on one side per axis -- lexicographic and orientation-scrambled structured
+// meshes) or P+2 (general).  All box-local index arithmetic then has constant strides.
+template <int P, int NB>
+struct XCfg {
+  static constexpr int PB = NB + 1;                 // points per axis of the point box
+  static constexpr int NPB = PB * PB * PB;
+  static constexpr int LAY = NB * NB;               // cells per layer
+  static constexpr int CE = 32;                     // stored entries per cell (36 packed minus the
+                                                    // four body diagonals, exactly 0 under the vertex rule)
+  static constexpr int CP = 35;                     // cell pitch (doubles): 2*CP = 6 (mod 32), conflict-free
+                                                    // cell writes and row gathers; 35 >= 27*10/8 holds a
+                                                    // chunk's staged rows in one ring slot
+  static constexpr bool ONE = NB * LAY * CP * 8 <= 36 * 1024;  // all cells resident: one chunk
+  static constexpr int KZ = ONE ? P + 1 : 1;       // row layers per chunk
+  static constexpr int NR = ONE ? NB : 2;          // resident cell layers (ring)
+  static constexpr int NP1 = P + 1;
+  static constexpr int MAXROW = KZ * NP1 * NP1;     // rows per chunk (<= 125 for P <= 4, (P+1)^2 else)
+  static constexpr int OFF_XG = 3 * NPB * 8;
+  static constexpr int OFF_CM = (OFF_XG + NPB * 4 + 15) / 16 * 16;
+  static constexpr int MAXP = MAXROW + (MAXROW * 27 + XPIECE_N - 1) / XPIECE_N + 1;  // pieces per chunk
+  static constexpr int NCHUNK = ONE ? 1 : P + 1;
+  static constexpr int OFF_MT = OFF_CM + NR * LAY * CP * 8;              // per chunk row: out int64
+  static constexpr int OFF_SO = OFF_MT + 8 * MAXROW;                      // per chunk row: staging offset
+  static constexpr int OFF_PC = OFF_SO + 4 * MAXROW;                      // the chunk's write-out pieces
+  static constexpr int SMEM = OFF_PC + 4 * MAXP;
+  // staging of a chunk's rows for the coalesced write-out: the values of every row in final
+  // position order, rows in ascending row order (setup), and the box point of each column
+  // (uint16), placed over cell storage no longer needed (one chunk: all of it; ring: the slot the
+  // next chunk overwrites first)
+  static constexpr int STAGE = MAXROW * 27 * 10;
+  static_assert(STAGE <= (ONE ? NR * LAY * CP * 8 : LAY * CP * 8), "stage does not fit");
+  static_assert(MAXROW <= 128, "one row per thread per chunk");
+  static_assert(MAXROW * 27 <= 4096, "12-bit staging offsets");
+  static_assert(MAXP <= 256, "two piece records per thread");
+};
+
 // ============================================================================== setup kernel
-// Box table of every element (125 boxes of the extended frame) and the position table of every
-// owned row: final position of each of the 27 stencil slots in the ascending-column CSR row.
-template <int P>
+// Box table of every element (125 boxes of the extended frame), the position table of every
+// owned row (final position of each of the 27 stencil slots in the ascending-column CSR row, and
+// the row's staging offset), and the write-out pieces of every chunk of the fill kernel.
+template <int P, int NB>
 __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
+  using CF = XCfg<P, NB>;
   const int64_t e = blockIdx.x;
   if (e >= A.nel_local) return;
   __shared__ XElem H;
@@ -157,6 +202,77 @@ __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
     }
   }
   constexpr int NP1 = P + 1;
+  // fill-kernel chunks (owned-row bounding box [olo, ohi], z layers in chunks of KZ): the chunk's
+  // rows are staged in ascending row order (so consecutive rows are consecutive CSR ranges), and
+  // every run of consecutive rows is written out in pieces of <= XPIECE_N entries
+  __shared__ uint16_t so_l[NP1 * NP1 * NP1];
+  __shared__ int s_g[128], s_len[128], s_so[128], s_t[128];
+  {
+    const int rnx = H.ohi[0] - H.olo[0] + 1, rny = H.ohi[1] - H.olo[1] + 1;
+    const int t = threadIdx.x;
+    int ch = 0;
+    for (int z0 = H.olo[2]; z0 <= H.ohi[2]; z0 += CF::KZ, ++ch) {
+      const int z1 = (z0 + CF::KZ - 1 < H.ohi[2]) ? z0 + CF::KZ - 1 : H.ohi[2];
+      const int nrow = rnx * rny * (z1 - z0 + 1);
+      if (ch >= A.nchunk || nrow > CF::MAXROW) atomicExch(A.err, 1);
+      int g = 0x7fffffff, len = 0, l = -1;
+      if (t < nrow && t < CF::MAXROW) {
+        const int q = t / rnx;
+        const int x[3] = {H.olo[0] + t - q * rnx, H.olo[1] + q % rny, z0 + q / rny};
+        const int tau = lcls(x[0], P) + 3 * lcls(x[1], P) + 9 * lcls(x[2], P);
+        if ((H.own >> tau) & 1) {
+          bool okg = true;
+          g = gid(x, okg);
+          const int64_t r = (int64_t)g - A.row_begin;
+          if (!okg || r < 0) {
+            atomicExch(A.err, 1);
+            g = 0x7fffffff;
+          } else {
+            len = A.cnt[r];
+            l = x[0] + NP1 * (x[1] + NP1 * x[2]);
+          }
+        }
+      }
+      s_g[t] = g;
+      s_len[t] = len;
+      __syncthreads();
+      int rank = 0, so = 0;
+      if (l >= 0) {
+        for (int u = 0; u < nrow; ++u)
+          if (s_g[u] < g) {
+            ++rank;
+            so += s_len[u];
+          }
+        if (so + len > 4095) atomicExch(A.err, 1);
+        so_l[l] = (uint16_t)so;
+      }
+      __syncthreads();
+      if (l >= 0) {
+        s_t[rank] = t;
+        s_so[t] = so;
+      }
+      int nr = __syncthreads_count(l >= 0);
+      if (t == 0 && ch < A.nchunk) {
+        uint32_t *pc = A.piece + ((int64_t)e * A.nchunk + ch) * (1 + A.maxp);
+        int np = 0;
+        for (int k = 0; k < nr;) {
+          int k2 = k + 1;
+          while (k2 < nr && s_g[s_t[k2]] == s_g[s_t[k2 - 1]] + 1) ++k2;
+          const int t0 = s_t[k], so0 = s_so[t0];
+          const int tot = s_so[s_t[k2 - 1]] + s_len[s_t[k2 - 1]] - so0;
+          for (int off = 0; off < tot; off += XPIECE_N) {
+            const int n = (tot - off < XPIECE_N) ? tot - off : XPIECE_N;
+            if (np < A.maxp) pc[1 + np] = (uint32_t)(so0 + off) | ((uint32_t)t0 << 12) | ((uint32_t)n << 19);
+            ++np;
+          }
+          k = k2;
+        }
+        if (np > A.maxp) atomicExch(A.err, 1);
+        pc[0] = (uint32_t)np;
+      }
+      __syncthreads();
+    }
+  }
   for (int l = threadIdx.x; l < NP1 * NP1 * NP1; l += blockDim.x) {
     const int x[3] = {l % NP1, (l / NP1) % NP1, l / (NP1 * NP1)};
     const int tau = lcls(x[0], P) + 3 * lcls(x[1], P) + 9 * lcls(x[2], P);
@@ -184,6 +300,7 @@ __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
     }
     uint32_t w[XPOS_W / 4];
     for (int i = 0; i < XPOS_W / 4; ++i) w[i] = 0xffffffffu;
+    w[7] = 0xffff0000u | so_l[l];
     for (int j = 0; j < 27; ++j) {
       if (ids[j] < 0) continue;
       int rk = 0;
@@ -198,37 +315,6 @@ __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
     dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
-
-// ============================================================================== fill kernel
-// Compile-time geometry of the shared-memory boxes.  NB = cell-box extent per axis the kernel is
-// built for: P+1 (every element of the mesh has a box of at most P+1 cells per axis: elements
-// owning entities on one side per axis -- lexicographic and orientation-scrambled structured
-// meshes) or P+2 (general).  All box-local index arithmetic then has constant strides.
-template <int P, int NB>
-struct XCfg {
-  static constexpr int PB = NB + 1;                 // points per axis of the point box
-  static constexpr int NPB = PB * PB * PB;
-  static constexpr int LAY = NB * NB;               // cells per layer
-  static constexpr int CE = 32;                     // stored entries per cell (36 packed minus the
-                                                    // four body diagonals, exactly 0 under the vertex rule)
-  static constexpr int CP = 33;                     // cell pitch (doubles): odd, conflict-free row gathers
-  static constexpr bool ONE = NB * LAY * CP * 8 <= 36 * 1024;  // all cells resident: one chunk
-  static constexpr int KZ = ONE ? P + 1 : 1;       // row layers per chunk
-  static constexpr int NR = ONE ? NB : 2;          // resident cell layers (ring)
-  static constexpr int NP1 = P + 1;
-  static constexpr int MAXROW = KZ * NP1 * NP1;     // rows per chunk (<= 125 for P <= 4, (P+1)^2 else)
-  static constexpr int OFF_XG = 3 * NPB * 8;
-  static constexpr int OFF_CM = (OFF_XG + NPB * 4 + 15) / 16 * 16;
-  static constexpr int OFF_MT = OFF_CM + NR * LAY * CP * 8;              // per chunk row: out int64
-  static constexpr int OFF_PX = OFF_MT + 8 * MAXROW;                      // px int16 | len << 16 (int32)
-  static constexpr int SMEM = OFF_PX + 4 * MAXROW;
-  // staging of a chunk's rows for the coalesced write-out: values in final position order and the
-  // stencil slot of each position, placed over cell storage no longer needed (one chunk: all of it;
-  // ring: the slot the next chunk overwrites first)
-  static constexpr int STAGE = MAXROW * 27 * 9;
-  static_assert(STAGE <= (ONE ? NR * LAY * CP * 8 : LAY * CP * 8), "stage does not fit");
-  static_assert(MAXROW <= 128, "one row per thread per chunk");
-};
 
 // packed index of the cell-matrix entry (a, b), a <= b, with the four body diagonals removed
 __host__ __device__ constexpr int cidx(int a, int b) {
@@ -282,17 +368,21 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
     else dst += v;
   };
   bool ok = true;
+  double dg[8];  // the eight diagonal entries (four corners each) accumulate in registers
+#pragma unroll
+  for (int q = 0; q < 8; ++q) dg[q] = 0.0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     // corners are evaluated one after the other (the fence keeps the compiler from hoisting every
-    // corner's loads and arithmetic at once: ~200 registers otherwise); the corner re-reads its
-    // four points from shared memory
+    // corner's loads and arithmetic at once: ~200 registers otherwise; caching the eight points in
+    // registers instead spills at 128); the corner re-reads its four points from shared memory
     asm volatile("" ::: "memory");
     double j[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) j[d][k] = X(q | (1 << d), k) - X(q & ~(1 << d), k);
+      for (int k = 0; k < 3; ++k)
+        j[d][k] = X(q | (1 << d), k) - X(q & ~(1 << d), k);
     double r[3][3];
     cross3x(j[1], j[2], r[0]);
     cross3x(j[2], j[0], r[1]);
@@ -309,10 +399,10 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
     double Qs[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) Qs[d] = s0 * Q[d][0] + s1 * Q[d][1] + s2 * Q[d][2];
-    put(q, q, q, s0 * Qs[0] + s1 * Qs[1] + s2 * Qs[2] + b8 * det);
-    put(q, q ^ 1, q ^ 1, Q[0][0]);
-    put(q, q ^ 2, q ^ 2, Q[1][1]);
-    put(q, q ^ 4, q ^ 4, Q[2][2]);
+    dg[q] += s0 * Qs[0] + s1 * Qs[1] + s2 * Qs[2] + b8 * det;
+    dg[q ^ 1] += Q[0][0];
+    dg[q ^ 2] += Q[1][1];
+    dg[q ^ 4] += Q[2][2];
     put(q, q, q ^ 1, -s0 * Qs[0]);
     put(q, q, q ^ 2, -s1 * Qs[1]);
     put(q, q, q ^ 4, -s2 * Qs[2]);
@@ -320,6 +410,8 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
     put(q, q ^ 1, q ^ 4, s0 * s2 * Q[0][2]);
     put(q, q ^ 2, q ^ 4, s1 * s2 * Q[1][2]);
   }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[cidx(q, q)] = dg[q];
   return ok;
 }
 
@@ -334,7 +426,8 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   int32_t *XG = reinterpret_cast<int32_t *>(smem + CF::OFF_XG);
   double *cm = reinterpret_cast<double *>(smem + CF::OFF_CM);
   int64_t *m_out = reinterpret_cast<int64_t *>(smem + CF::OFF_MT);
-  int32_t *m_px = reinterpret_cast<int32_t *>(smem + CF::OFF_PX);
+  int32_t *m_so = reinterpret_cast<int32_t *>(smem + CF::OFF_SO);
+  uint32_t *m_pc = reinterpret_cast<uint32_t *>(smem + CF::OFF_PC);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if ((int64_t)blockIdx.x >= A.nel_local) return;
   const int64_t el = A.order ? A.order[blockIdx.x] : blockIdx.x;
@@ -381,8 +474,13 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   const int rnx = ohi0 - olo0 + 1, rny = ohi1 - olo1 + 1;
   const double alpha = A.alpha, beta = A.beta;
   double *stage_v = cm;  // overwritten per chunk, see below
-  for (int z0 = zlo; z0 <= zhi; z0 += CF::KZ) {
+  for (int z0 = zlo, ch = 0; z0 <= zhi; z0 += CF::KZ, ++ch) {
     const int z1 = (z0 + CF::KZ - 1 < zhi) ? z0 + CF::KZ - 1 : zhi;
+    // the chunk's write-out pieces (setup), consumed after the staging barrier
+    const uint32_t *pcs = A.piece + ((int64_t)el * CF::NCHUNK + ch) * (1 + CF::MAXP);
+    const int npc = (int)__ldg(pcs);
+    const uint32_t pc0 = tid < CF::MAXP ? __ldg(pcs + 1 + tid) : 0u;
+    const uint32_t pc1 = tid + 128 < CF::MAXP ? __ldg(pcs + 129 + tid) : 0u;
     // cell layers to compute now (lattice coordinates): [z0-1 (first chunk only), z1] within the box
     int c0 = (z0 == zlo) ? z0 - 1 : z0;
     int c1 = z1;
@@ -446,31 +544,36 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     __syncthreads();  // every row has read the cells: stage over the cell storage
     // stage: ONE chunk -> all cells; ring -> the slot of layer z0-1 (next chunk's first write)
     stage_v = CF::ONE ? cm : cm + (((z0 - 1 - clo2) % NR + NR) % NR) * LAY * CP;
-    int8_t *stage_j = reinterpret_cast<int8_t *>(stage_v + CF::MAXROW * 27);  // point offset of the column
+    uint16_t *stage_p = reinterpret_cast<uint16_t *>(stage_v + CF::MAXROW * 27);  // box point of the column
     if (hasrow) {
-      int len = 0;
+      const int so = (int)(pw[7] & 0xffffu);  // the row's staging offset (setup: ascending row order)
 #pragma unroll
       for (int jj = 0; jj < 27; ++jj) {
         const int ps = (int)((pw[jj >> 2] >> (8 * (jj & 3))) & 255u);
         if (ps != 255) {
-          stage_v[tid * 27 + ps] = acc[jj];
-          stage_j[tid * 27 + ps] = (int8_t)((jj % 3 - 1) + PB * ((jj / 3) % 3 - 1) + PB * PB * (jj / 9 - 1));
-          ++len;
+          stage_v[so + ps] = acc[jj];
+          stage_p[so + ps] = (uint16_t)(px + (jj % 3 - 1) + PB * ((jj / 3) % 3 - 1) + PB * PB * (jj / 9 - 1));
         }
       }
       m_out[tid] = out;
-      m_px[tid] = px | (len << 16);
-    } else if (tid < nrow) {
-      m_px[tid] = 0;
+      m_so[tid] = so;
     }
+    if (tid < CF::MAXP) m_pc[tid] = pc0;
+    if (tid + 128 < CF::MAXP) m_pc[tid + 128] = pc1;
     __syncthreads();
-    // coalesced write-out: one warp per row, lane = final column position
-    for (int row = warp; row < nrow; row += 4) {
-      const int mp = m_px[row];
-      if (lane < (mp >> 16)) {
-        const int64_t o = m_out[row] + lane;
-        __stcs(A.col + o, XG[(mp & 0xffff) + (int)stage_j[row * 27 + lane]]);
-        __stcs(A.val + o, stage_v[row * 27 + lane]);
+    // coalesced write-out: one warp per piece (<= 128 consecutive CSR entries of a run of
+    // consecutive rows), four entries per lane
+    for (int pc = warp; pc < npc; pc += 4) {
+      const uint32_t rec = m_pc[pc];
+      const int s0 = (int)(rec & 0xfffu), t0 = (int)((rec >> 12) & 127u), n = (int)(rec >> 19);
+      const int64_t o = m_out[t0] + (s0 - m_so[t0]);
+#pragma unroll
+      for (int u = 0; u < XPIECE_N / 32; ++u) {
+        const int k = lane + 32 * u;
+        if (k < n) {
+          __stcs(A.col + o + k, XG[stage_p[s0 + k]]);
+          __stcs(A.val + o + k, stage_v[s0 + k]);
+        }
       }
     }
     __syncthreads();
@@ -481,8 +584,37 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
 template <int P>
 static cudaError_t xh1_setup_p(const XSetupArgs &a, cudaStream_t st) {
   if (a.nel_local <= 0) return cudaSuccess;
-  k_xh1_setup<P><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  if (a.nb == P + 1) k_xh1_setup<P, P + 1><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  else k_xh1_setup<P, P + 2><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+template <int P, int NB>
+static void geom_nb(int *kz, int *maxrow, int *maxp, int *nchunk) {
+  using CF = XCfg<P, NB>;
+  *kz = CF::KZ;
+  *maxrow = CF::MAXROW;
+  *maxp = CF::MAXP;
+  *nchunk = CF::NCHUNK;
+}
+template <int P>
+static void geom_p(const int cmax[3], int *kz, int *maxrow, int *maxp, int *nchunk) {
+  if (xfill_nb(P, cmax) == P + 1) geom_nb<P, P + 1>(kz, maxrow, maxp, nchunk);
+  else geom_nb<P, P + 2>(kz, maxrow, maxp, nchunk);
+}
+void xfill_geom(int p, const int cmax[3], int *kz, int *maxrow, int *maxp, int *nchunk) {
+  *kz = *maxrow = *maxp = *nchunk = 0;
+  switch (p) {
+    case 1: geom_p<1>(cmax, kz, maxrow, maxp, nchunk); break;
+    case 2: geom_p<2>(cmax, kz, maxrow, maxp, nchunk); break;
+    case 3: geom_p<3>(cmax, kz, maxrow, maxp, nchunk); break;
+    case 4: geom_p<4>(cmax, kz, maxrow, maxp, nchunk); break;
+    case 5: geom_p<5>(cmax, kz, maxrow, maxp, nchunk); break;
+    case 6: geom_p<6>(cmax, kz, maxrow, maxp, nchunk); break;
+    case 7: geom_p<7>(cmax, kz, maxrow, maxp, nchunk); break;
+    case 8: geom_p<8>(cmax, kz, maxrow, maxp, nchunk); break;
+    default: break;
+  }
 }
 
 template <int P, int NB>
@@ -491,7 +623,7 @@ static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_ou
   constexpr int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
-  constexpr int MINB = (smem <= 44 * 1024) ? 5 : 3;
+  constexpr int MINB = (smem <= 44 * 1024) ? XMINB : 3;
   auto k = k_xh1_fill<P, NB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
