@@ -111,6 +111,7 @@ struct lor_ctx_s {
   cudaStream_t stream = nullptr;
   ElemTopo *topo = nullptr;
   int32_t *order = nullptr;  // CTA -> local element, Morton order of element centroids
+  std::vector<int32_t> order_host;  // host copy (empty: natural order)
   double *X = nullptr;
   int64_t xstride = 0;
   SpaceDev sp[3];
@@ -284,6 +285,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     x.ncy = S.xc[1];
     x.ncz = S.xc[2];
     x.err = c->err;
+    x.tstamp = c->tstamp;
     CUDA_TRY(c, launch_xh1_fill(c->p, x, c->stream, nullptr));
     if (c->nel_local > 0) c->launches++;
     CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
@@ -504,6 +506,7 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
       std::vector<int32_t> ord((size_t)n);
       for (int64_t e = 0; e < n; ++e) ord[e] = key[e].second;
       if (dev_upload(c, &c->order, ord.data(), ord.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "order");
+      c->order_host = ord;
     }
     if (dev_upload(c, &c->X, padded.data(), padded.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "X");
   }
@@ -709,6 +712,17 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     if (c->nel_local * c->xstride >= (int64_t(1) << 31)) {
       why = "E-vector index exceeds int32";
     } else if (xframe_build(plan, A.elem_vert, xe, S.xc, &why)) {
+      // records in processing order, so a CTA reads its record, restriction and gather list by
+      // its own index (one dependent load less)
+      {
+        std::vector<XElem> xo(xe.size());
+        for (size_t b = 0; b < xe.size(); ++b) {
+          const int32_t e = c->order_host.empty() ? (int32_t)b : c->order_host[b];
+          xo[b] = xe[(size_t)e];
+          xo[b].el = e;
+        }
+        xe.swap(xo);
+      }
       if (dev_upload(c, &S.xe, xe.data(), xe.size()) != cudaSuccess ||
           dev_alloc(c, &S.xbox, (size_t)c->nel_local * 125) != cudaSuccess ||
           dev_alloc(c, &S.xmap, (size_t)c->nel_local * xmap_points(A.p, S.xc)) != cudaSuccess ||

@@ -36,7 +36,8 @@ struct __align__(16) XElem {
   int8_t olo[3];     // bounding box [olo, ohi] of the owned rows (lattice coordinates)
   int8_t ohi[3];
   XNbr nbr[27];
-  uint8_t pad2[8];
+  int32_t el;        // the local element (records are stored in processing (CTA) order)
+  uint8_t pad2[4];
 };
 static_assert(sizeof(XElem) == 240, "layout");
 
@@ -60,7 +61,8 @@ constexpr int XPIECE_N = 128;
 
 struct XSetupArgs {
   int64_t nel_local;
-  const XElem *xe;
+  const XElem *xe;      // [nel_local] in processing order (CTA b -> element xe[b].el); xmap, xhalo,
+                        // box and piece below are stored in the same order
   const ElemTopo *topo;
   const int32_t *base[4];
   int64_t row_begin;
@@ -97,6 +99,8 @@ struct XFillArgs {
   double alpha, beta;
   int ncx, ncy, ncz;  // max cell-box extents over the elements (shared-memory sizing)
   int *err;
+  unsigned long long *tstamp;  // debug (LOR_PHASE_TIMING=1): per-CTA phase clocks, 16 per CTA
+  int64_t pf_dist;             // L2 prefetch distance in CTAs (resident CTAs of the grid; 0: off)
 };
 
 // host: regular-neighbourhood check and per-element extended-frame records (nranks == 1)

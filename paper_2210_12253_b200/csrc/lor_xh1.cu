@@ -12,6 +12,7 @@
 //             columns = global ids of the 27 stencil points, each stored at its final position in
 //             the row (setup position table: ascending global column order, reading P-5).
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "lor_device.cuh"
@@ -39,6 +40,8 @@ __device__ __forceinline__ void x_to_local(int p, uint32_t code, const int y[3],
     L[a] = ((code >> (6 + a)) & 1) ? -v : v;
   }
 }
+
+__device__ __forceinline__ void pf_l2(const void *a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
 
 __device__ __forceinline__ void xreport(int *err, int code, int64_t e, int cell) {
   if (atomicCAS(err, 0, code) == 0) {
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
       if (cb[a] == 2 && P < 2) ok = false;
     }
     const int ni = (ydelta(y[0], P) + 1) + 3 * (ydelta(y[1], P) + 1) + 9 * (ydelta(y[2], P) + 1);
-    int64_t f = e;
+    int64_t f = H.el;
     uint32_t code = 0 | (1u << 2) | (2u << 4) | (1u << 9) | (1u << 11) | (1u << 13);  // identity
     if (ni != 13) {
       f = H.nbr[ni].el;
@@ -430,11 +433,30 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   uint32_t *m_pc = reinterpret_cast<uint32_t *>(smem + CF::OFF_PC);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if ((int64_t)blockIdx.x >= A.nel_local) return;
-  const int64_t el = A.order ? A.order[blockIdx.x] : blockIdx.x;
+  const int64_t bs = blockIdx.x;  // processing slot: element record, restriction, gather list, pieces
+#define XSTAMP(k) \
+  do { if (A.tstamp && tid == 0) A.tstamp[(int64_t)blockIdx.x * 16 + (k)] = clock64(); } while (0)
+  XSTAMP(0);
   // element header word {own, clo, chi, olo, ohi} read by every thread (broadcast); all loads of the
   // prologue (extended restriction, own E-vector, neighbour points) are independent of each other
   // and complete at one barrier
-  const int4 hw = __ldg(reinterpret_cast<const int4 *>(A.xe + el));
+  const int4 hw = __ldg(reinterpret_cast<const int4 *>(A.xe + bs));
+  const int64_t el = __ldg(&A.xe[bs].el);  // same round trip as the header
+  // L2 prefetch for the CTA that takes this CTA's place about one CTA lifetime from now (slot +
+  // resident CTAs): its record, restriction and gather list now; its E-vector (needs its element
+  // id) after the cell phase; its neighbour points (need its gather list) before the write-out
+  constexpr int HC = NPB - NPT;
+  const int64_t nbs = bs + A.pf_dist;
+  const bool pf = A.pf_dist > 0 && nbs < A.nel_local;
+  int pf_el = -1;
+  int2 pf_h = make_int2(-1, 0);
+  if (pf) {
+    constexpr int LX = (int)((sizeof(XElem) + 127) / 128), LM = (NPB * 4 + 127) / 128 + 1, LH = (HC * 8 + 127) / 128 + 1;
+    if (tid < LX) pf_l2(reinterpret_cast<const char *>(A.xe + nbs) + 128 * tid);
+    else if (tid < LX + LM) pf_l2(reinterpret_cast<const char *>(A.xmap + nbs * NPB) + 128 * (tid - LX));
+    else if (tid < LX + LM + LH) pf_l2(reinterpret_cast<const char *>(A.xhalo + nbs * HC) + 128 * (tid - LX - LM));
+    if (tid == 127) pf_el = __ldg(&A.xe[nbs].el);
+  }
   const int clo0 = (int8_t)(hw.y & 255), clo1 = (int8_t)((hw.y >> 8) & 255), clo2 = (int8_t)((hw.y >> 16) & 255);
   const int ex0 = (int8_t)((hw.y >> 24) & 255) - clo0 + 1, ex1 = (int8_t)(hw.z & 255) - clo1 + 1,
             ex2 = (int8_t)((hw.z >> 8) & 255) - clo2 + 1;  // cell-box extents (<= NB)
@@ -445,7 +467,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   {
     if (tid == 0) s_bad = 0;
     // extended element restriction (setup): global id of every point of the box
-    const int32_t *xm = A.xmap + el * NPB;
+    const int32_t *xm = A.xmap + bs * NPB;
     for (int i = tid; i < NPB; i += blockDim.x) XG[i] = __ldg(xm + i);
     // own E-vector, one lattice x-row per thread
     const double *xs = A.X + el * A.xstride;
@@ -457,8 +479,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       for (int i = 0; i < NP1; ++i) dst[i] = __ldg(src + i);
     }
     // neighbour points of the box (setup gather list)
-    constexpr int HC = NPB - NPT;
-    const int2 *hl = A.xhalo + el * HC;
+    const int2 *hl = A.xhalo + bs * HC;
     for (int h = tid; h < HC; h += blockDim.x) {
       const int2 hv = __ldg(hl + h);
       if (hv.x >= 0) {
@@ -469,6 +490,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     }
   }
   __syncthreads();
+  XSTAMP(1);
   // rows: the owned-row bounding box [olo, ohi], z-layers in chunks of KZ
   const int zlo = olo2, zhi = ohi2;
   const int rnx = ohi0 - olo0 + 1, rny = ohi1 - olo1 + 1;
@@ -477,7 +499,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   for (int z0 = zlo, ch = 0; z0 <= zhi; z0 += CF::KZ, ++ch) {
     const int z1 = (z0 + CF::KZ - 1 < zhi) ? z0 + CF::KZ - 1 : zhi;
     // the chunk's write-out pieces (setup), consumed after the staging barrier
-    const uint32_t *pcs = A.piece + ((int64_t)el * CF::NCHUNK + ch) * (1 + CF::MAXP);
+    const uint32_t *pcs = A.piece + (bs * CF::NCHUNK + ch) * (1 + CF::MAXP);
     const int npc = (int)__ldg(pcs);
     const uint32_t pc0 = tid < CF::MAXP ? __ldg(pcs + 1 + tid) : 0u;
     const uint32_t pc1 = tid + 128 < CF::MAXP ? __ldg(pcs + 129 + tid) : 0u;
@@ -499,6 +521,16 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       }
     }
     __syncthreads();
+    if (ch == 0) XSTAMP(2);
+    if (pf && ch == 0) {
+      // next CTA's E-vector (3 x (p+1)^3 doubles, 128-byte aligned) and gather list entries
+      const int pe = __shfl_sync(0xffffffffu, pf_el, 31);
+      if (warp == 3 && pe >= 0) {
+        const char *xp = reinterpret_cast<const char *>(A.X + (int64_t)pe * A.xstride);
+        for (int l = lane; l < (3 * NPT * 8 + 127) / 128; l += 32) pf_l2(xp + 128 * l);
+      }
+      if (tid < HC) pf_h = __ldg(A.xhalo + nbs * HC + tid);
+    }
     if (s_bad && tid == 0) { xreport(A.err, 2, A.elem_begin + el, s_bad - 1); s_bad = 0; }
     // ---- rows of layers [z0, z1]: one thread per owned row, values from the <= 8 cells
     const int nrow = rnx * rny * (z1 - z0 + 1);
@@ -542,6 +574,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       }
     }
     __syncthreads();  // every row has read the cells: stage over the cell storage
+    if (ch == 0) XSTAMP(5);
     // stage: ONE chunk -> all cells; ring -> the slot of layer z0-1 (next chunk's first write)
     stage_v = CF::ONE ? cm : cm + (((z0 - 1 - clo2) % NR + NR) % NR) * LAY * CP;
     uint16_t *stage_p = reinterpret_cast<uint16_t *>(stage_v + CF::MAXROW * 27);  // box point of the column
@@ -561,6 +594,13 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     if (tid < CF::MAXP) m_pc[tid] = pc0;
     if (tid + 128 < CF::MAXP) m_pc[tid + 128] = pc1;
     __syncthreads();
+    if (ch == 0) XSTAMP(3);
+    if (pf_h.x >= 0) {  // next CTA's neighbour points
+      pf_l2(A.X + pf_h.x);
+      pf_l2(A.X + pf_h.x + NPT);
+      pf_l2(A.X + pf_h.x + 2 * NPT);
+      pf_h.x = -1;
+    }
     // coalesced write-out: one warp per piece (<= 128 consecutive CSR entries of a run of
     // consecutive rows), four entries per lane
     for (int pc = warp; pc < npc; pc += 4) {
@@ -578,6 +618,8 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     }
     __syncthreads();
   }
+  XSTAMP(4);
+#undef XSTAMP
 }
 
 // ============================================================================== launchers
@@ -627,7 +669,19 @@ static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_ou
   auto k = k_xh1_fill<P, NB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  k<<<(unsigned)a.nel_local, 128, smem, st>>>(a);
+  // L2 prefetch distance = resident CTAs of the grid (cached per instantiation; LOR_XPF=0: off)
+  static int64_t resident = -1;
+  if (resident < 0) {
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, smem);
+    const char *e = getenv("LOR_XPF");
+    resident = (e && !atoi(e)) ? 0 : (int64_t)nsm * occ;
+  }
+  XFillArgs b = a;
+  b.pf_dist = resident;
+  k<<<(unsigned)a.nel_local, 128, smem, st>>>(b);
   return cudaGetLastError();
 }
 
