@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     if (tid < LX) pf_l2(reinterpret_cast<const char *>(A.xe + nbs) + 128 * tid);
     else if (tid < LX + LM) pf_l2(reinterpret_cast<const char *>(A.xmap + nbs * NPB) + 128 * (tid - LX));
     else if (tid < LX + LM + LH) pf_l2(reinterpret_cast<const char *>(A.xhalo + nbs * HC) + 128 * (tid - LX - LM));
+    else if (tid == LX + LM + LH) pf_l2(A.piece + nbs * CF::NCHUNK * (1 + CF::MAXP));
     if (tid == 127) pf_el = __ldg(&A.xe[nbs].el);
   }
   const int clo0 = (int8_t)(hw.y & 255), clo1 = (int8_t)((hw.y >> 8) & 255), clo2 = (int8_t)((hw.y >> 16) & 255);
@@ -575,6 +576,12 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     }
     __syncthreads();  // every row has read the cells: stage over the cell storage
     if (ch == 0) XSTAMP(5);
+    if (pf_h.x >= 0) {  // next CTA's neighbour points
+      pf_l2(A.X + pf_h.x);
+      pf_l2(A.X + pf_h.x + NPT);
+      pf_l2(A.X + pf_h.x + 2 * NPT);
+      pf_h.x = -1;
+    }
     // stage: ONE chunk -> all cells; ring -> the slot of layer z0-1 (next chunk's first write)
     stage_v = CF::ONE ? cm : cm + (((z0 - 1 - clo2) % NR + NR) % NR) * LAY * CP;
     uint16_t *stage_p = reinterpret_cast<uint16_t *>(stage_v + CF::MAXROW * 27);  // box point of the column
@@ -595,12 +602,6 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     if (tid + 128 < CF::MAXP) m_pc[tid + 128] = pc1;
     __syncthreads();
     if (ch == 0) XSTAMP(3);
-    if (pf_h.x >= 0) {  // next CTA's neighbour points
-      pf_l2(A.X + pf_h.x);
-      pf_l2(A.X + pf_h.x + NPT);
-      pf_l2(A.X + pf_h.x + 2 * NPT);
-      pf_h.x = -1;
-    }
     // coalesced write-out: one warp per piece (<= 128 consecutive CSR entries of a run of
     // consecutive rows), four entries per lane
     for (int pc = warp; pc < npc; pc += 4) {
