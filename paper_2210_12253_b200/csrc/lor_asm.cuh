@@ -360,6 +360,12 @@ template <int DIM, int SP, int P, int QUAD>
 __device__ __forceinline__ bool compute_cell(const double *__restrict__ X, int cx, int cy, int cz, double alpha,
                                              double beta, double *__restrict__ out, int NC, int ci) {
   constexpr int NP1 = P + 1;
+  if (DIM == 3 && SP == SP_ND && QUAD == 0) {  // vertex rule: straight into the packed slots
+    auto XF = [&](int v, int k) -> double {
+      return X[k * ipow_c(NP1, 3) + (cx + (v & 1)) + NP1 * ((cy + ((v >> 1) & 1)) + NP1 * (cz + ((v >> 2) & 1)))];
+    };
+    return cell_nd_vertex_to(XF, alpha, beta, out + ci, NC);
+  }
   if (DIM == 3) {
     double C[8][3];
 #pragma unroll

@@ -315,6 +315,72 @@ __device__ __forceinline__ bool cell_nd(const double X[8][3], double alpha, doub
   return ok;
 }
 
+// ND vertex rule straight into the cell's packed slots out[t * NC] (t = tri(12, i, j)): the corner
+// coordinates are read from shared memory per corner (X(v, k): component k of cell vertex v), the
+// mass part accumulates in place (first corner stores, the second adds; an off-diagonal mass entry
+// has exactly one corner), the 6x6 face matrix of the curl part stays in registers and K = C^T M C
+// is added at the end.  Same terms as cell_nd<0> without its 78 + 21 register arrays.
+__host__ __device__ constexpr bool nd_share_corner(int i, int j) {
+  for (int q = 0; q < 8; ++q)
+    for (int d = 0; d < 3; ++d)
+      for (int e = 0; e < 3; ++e)
+        if (d != e && corner_edge(q, d) == i && corner_edge(q, e) == j) return true;
+  return false;
+}
+// first corner (lowest q) on edge eps: the edge's end with bit dir = 0
+__host__ __device__ constexpr bool nd_first_end(int q, int d) { return ((q >> d) & 1) == 0; }
+
+template <typename XF>
+__device__ __forceinline__ bool cell_nd_vertex_to(XF X, double alpha, double beta, double *__restrict__ out, int NC) {
+  double M[21];
+#pragma unroll
+  for (int i = 0; i < 21; ++i) M[i] = 0.0;
+  const double w = 0.125;
+  bool ok = true;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    asm volatile("" ::: "memory");  // one corner at a time (register pressure)
+    Jac3 J;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int hi = q | (1 << d), lo = q & ~(1 << d);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) J.j[d][k] = X(hi, k) - X(lo, k);
+    }
+    finish_jac(J);
+    ok &= J.det > 0.0;
+    const double rdet = 1.0 / J.det, sm = w * beta * rdet, sc = w * alpha * rdet;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int e = d; e < 3; ++e) {
+        const double qm = sm * dot3(J.r[d], J.r[e]);
+        double &dst = out[tri(12, corner_edge(q, d), corner_edge(q, e)) * NC];
+        if (d != e || nd_first_end(q, d)) dst = qm;
+        else dst += qm;
+        M[tri(6, 2 * d + ((q >> d) & 1), 2 * e + ((q >> e) & 1))] += sc * dot3(J.j[d], J.j[e]);
+      }
+  }
+  // curl-curl: K_ij = sum_{f in F(i), g in F(j)} C_fi M_fg C_gj, added to the mass part
+#pragma unroll
+  for (int i = 0; i < 12; ++i)
+#pragma unroll
+    for (int j = i; j < 12; ++j) {
+      double k = 0.0;
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int f = e_face(i, a), g = e_face(j, b);
+          k += (double)(c_sign(f, i) * c_sign(g, j)) * M[tri(6, f, g)];
+        }
+      double &dst = out[tri(12, i, j) * NC];
+      if (i == j || nd_share_corner(i, j)) dst += k;
+      else dst = k;
+    }
+  return ok;
+}
+
 // ------------------------------------------------------------------------ RT (3D): 6 x 6
 template <int QUAD>
 __device__ __forceinline__ bool cell_rt(const double X[8][3], double alpha, double beta, double *A /*21*/) {
