@@ -14,6 +14,8 @@
 // (tests/test_oracle_pins.py::test_cell_derham_factorizations).
 // Gauss-2: the same tensors at the 2^d interior points with all basis values.
 #pragma once
+#include <utility>
+
 #include "lor_device.cuh"
 
 namespace lorb {
@@ -330,6 +332,35 @@ __host__ __device__ constexpr bool nd_share_corner(int i, int j) {
 // first corner (lowest q) on edge eps: the edge's end with bit dir = 0
 __host__ __device__ constexpr bool nd_first_end(int q, int d) { return ((q >> d) & 1) == 0; }
 
+// packed index t -> (i, j), i <= j, of a symmetric 12 x 12 matrix
+__host__ __device__ constexpr int tri_i(int n, int t) {
+  int i = 0;
+  while (t >= n - i) { t -= n - i; ++i; }
+  return i;
+}
+__host__ __device__ constexpr int tri_j(int n, int t) {
+  int i = 0;
+  while (t >= n - i) { t -= n - i; ++i; }
+  return i + t;
+}
+template <int T>
+__device__ __forceinline__ void nd_curl_one(const double (&M)[21], double *__restrict__ out, int NC) {
+  constexpr int i = tri_i(12, T), j = tri_j(12, T);
+  constexpr int f0 = e_face(i, 0), f1 = e_face(i, 1), g0 = e_face(j, 0), g1 = e_face(j, 1);
+  constexpr double s00 = c_sign(f0, i) * c_sign(g0, j), s01 = c_sign(f0, i) * c_sign(g1, j);
+  constexpr double s10 = c_sign(f1, i) * c_sign(g0, j), s11 = c_sign(f1, i) * c_sign(g1, j);
+  static_assert(tri(12, i, j) == T, "packed index");
+  const double k = s00 * M[tri(6, f0, g0)] + s01 * M[tri(6, f0, g1)] + s10 * M[tri(6, f1, g0)] + s11 * M[tri(6, f1, g1)];
+  double &dst = out[T * NC];
+  if constexpr (i == j || nd_share_corner(i, j)) dst += k;
+  else dst = k;
+}
+template <int... T>
+__device__ __forceinline__ void nd_curl_all(const double (&M)[21], double *__restrict__ out, int NC,
+                                            std::integer_sequence<int, T...>) {
+  (nd_curl_one<T>(M, out, NC), ...);
+}
+
 template <typename XF>
 __device__ __forceinline__ bool cell_nd_vertex_to(XF X, double alpha, double beta, double *__restrict__ out, int NC) {
   double M[21];
@@ -361,23 +392,9 @@ __device__ __forceinline__ bool cell_nd_vertex_to(XF X, double alpha, double bet
         M[tri(6, 2 * d + ((q >> d) & 1), 2 * e + ((q >> e) & 1))] += sc * dot3(J.j[d], J.j[e]);
       }
   }
-  // curl-curl: K_ij = sum_{f in F(i), g in F(j)} C_fi M_fg C_gj, added to the mass part
-#pragma unroll
-  for (int i = 0; i < 12; ++i)
-#pragma unroll
-    for (int j = i; j < 12; ++j) {
-      double k = 0.0;
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int f = e_face(i, a), g = e_face(j, b);
-          k += (double)(c_sign(f, i) * c_sign(g, j)) * M[tri(6, f, g)];
-        }
-      double &dst = out[tri(12, i, j) * NC];
-      if (i == j || nd_share_corner(i, j)) dst += k;
-      else dst = k;
-    }
+  // curl-curl: K_ij = sum_{f in F(i), g in F(j)} C_fi M_fg C_gj, added to the mass part; one
+  // compile-time instance per packed entry (nested unrolled loops left M in local memory)
+  nd_curl_all(M, out, NC, std::make_integer_sequence<int, 78>{});
   return ok;
 }
 
