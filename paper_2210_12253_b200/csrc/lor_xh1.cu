@@ -499,11 +499,6 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   double *stage_v = cm;  // overwritten per chunk, see below
   for (int z0 = zlo, ch = 0; z0 <= zhi; z0 += CF::KZ, ++ch) {
     const int z1 = (z0 + CF::KZ - 1 < zhi) ? z0 + CF::KZ - 1 : zhi;
-    // the chunk's write-out pieces (setup), consumed after the staging barrier
-    const uint32_t *pcs = A.piece + (bs * CF::NCHUNK + ch) * (1 + CF::MAXP);
-    const int npc = (int)__ldg(pcs);
-    const uint32_t pc0 = tid < CF::MAXP ? __ldg(pcs + 1 + tid) : 0u;
-    const uint32_t pc1 = tid + 128 < CF::MAXP ? __ldg(pcs + 129 + tid) : 0u;
     // cell layers to compute now (lattice coordinates): [z0-1 (first chunk only), z1] within the box
     int c0 = (z0 == zlo) ? z0 - 1 : z0;
     int c1 = z1;
@@ -533,6 +528,11 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       if (tid < HC) pf_h = __ldg(A.xhalo + nbs * HC + tid);
     }
     if (s_bad && tid == 0) { xreport(A.err, 2, A.elem_begin + el, s_bad - 1); s_bad = 0; }
+    // the chunk's write-out pieces (setup), consumed after the staging barrier
+    const uint32_t *pcs = A.piece + (bs * CF::NCHUNK + ch) * (1 + CF::MAXP);
+    const int npc = (int)__ldg(pcs);
+    const uint32_t pc0 = tid < CF::MAXP ? __ldg(pcs + 1 + tid) : 0u;
+    const uint32_t pc1 = tid + 128 < CF::MAXP ? __ldg(pcs + 129 + tid) : 0u;
     // ---- rows of layers [z0, z1]: one thread per owned row, values from the <= 8 cells
     const int nrow = rnx * rny * (z1 - z0 + 1);
     double acc[27];
