@@ -540,6 +540,12 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
   int16_t *dlt = reinterpret_cast<int16_t *>(smem + CF::OFF_DL);
   if ((int64_t)blockIdx.x >= A.nel_local) return;
   const int64_t el = A.order ? A.order[blockIdx.x] : blockIdx.x;  // local element (locality-preserving order)
+  // L2 prefetch for the CTA that takes this CTA's place one residency later: its element id now,
+  // its topology/space records, E-vector and element restriction after the prologue
+  const int64_t pfb = (int64_t)blockIdx.x + A.pf_dist;
+  const bool pf = A.pf_dist > 0 && pfb < A.nel_local && A.plan_mode == 0;
+  int64_t pf_el = -1;
+  if (pf && tid == 0) pf_el = A.order ? __ldg(A.order + pfb) : pfb;
   LOR_STAMP(0);
   if (A.tstamp && tid == 0) A.tstamp[(int64_t)blockIdx.x * 16 + 6] = gtimer();
   {
@@ -557,10 +563,20 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
     if ((DIM * CF::NPTS) & 1) {
       if (tid == 0) X[DIM * CF::NPTS - 1] = __ldg(A.X + el * A.xstride + DIM * CF::NPTS - 1);
     }
-    if (tid == 0) { s_fin_n = 0; s_bad = 0; s_ownacc = 0; }
+    if (tid == 0) { s_fin_n = 0; s_bad = 0; s_ownacc = 0; s_nb = 0; }
+  }
+  // one-rank assembly: the element restriction comes from setup and the block table (used only by
+  // sorted records, i.e. multi-rank interface rows, and the setup passes) is skipped
+  const bool fast = A.emap != nullptr && A.plan_mode == 0;
+  if (fast) {
+    for (int l = tid; l < CF::NDPE; l += blockDim.x) {
+      gmap[l] = __ldg(A.emap + el * CF::NDPE + l);
+      bsg[l] = __ldg(A.esgn + el * CF::NDPE + l) < 0 ? 128 : 0;
+    }
   }
   __syncthreads();
   // ---- element block table, canonical axis order/directions, ascending-base order
+  if (!fast) {
   if (tid < NB) {
     const int s = tid / 27, tau = tid - 27 * s;
     Blk B;
@@ -594,6 +610,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
       blist[r] = (uint8_t)b;
     }
   }
+  }  // !fast
   // ---- slot -> local index offset relative to the row position in the column sub-lattice layout
   for (int i = tid; i < S * W; i += blockDim.x) {
     const int s = i / W, j = i - s * W;
@@ -605,6 +622,7 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
     dlt[i] = (int16_t)((uint8_t)(int8_t)(dx + ext_of<SP>(P, s2, 0) * (dy + ext_of<SP>(P, s2, 1) * dz)) | (s2 << 8));
   }
   // ---- element restriction in shared memory: global id and block/sign of every local dof
+  if (!fast)
   for (int l = tid; l < CF::NDPE; l += blockDim.x) {
     int s, x[3];
     decode_local<DIM, SP>(P, l, s, x);
@@ -616,6 +634,22 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
   __syncthreads();
   const int nb = s_nb;
   LOR_STAMP(1);
+  if (pf) {
+    const int64_t pe = __shfl_sync(0xffffffffu, pf_el, 0);
+    if (warp == 0 && pe >= 0) {
+      auto pfl = [](const void *a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); };
+      constexpr int LT = (int)((sizeof(ElemTopo) + 127) / 128), LE = (int)((sizeof(ElemSpace) + 127) / 128);
+      constexpr int LX = (DIM * CF::NPTS * 8 + 127) / 128;
+      if (lane < LT) pfl(reinterpret_cast<const char *>(A.topo + pe) + 128 * lane);
+      if (lane < LE) pfl(reinterpret_cast<const char *>(A.esp + pe) + 128 * lane);
+      for (int l = lane; l < LX; l += 32) pfl(reinterpret_cast<const char *>(A.X + pe * A.xstride) + 128 * l);
+      if (A.emap) {
+        constexpr int LM = (CF::NDPE * 4 + 127) / 128 + 1, LS = (CF::NDPE + 127) / 128 + 1;
+        for (int l = lane; l < LM; l += 32) pfl(reinterpret_cast<const char *>(A.emap + pe * CF::NDPE) + 128 * l);
+        if (lane < LS) pfl(reinterpret_cast<const char *>(A.esgn + pe * CF::NDPE) + 128 * lane);
+      }
+    }
+  }
 
   // ---- z-chunks of cell layers
   constexpr int NCHUNK = (DIM == 3) ? (P + KZ - 1) / KZ : 1;
@@ -907,7 +941,15 @@ cudaError_t launch_asm_p(const AsmArgs &a, int quad, cudaStream_t st, int *smem_
   auto run = [&](auto k) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem + pad);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    k<<<(unsigned)a.nel_local, 128, smem + pad, st>>>(a);
+    // L2 prefetch distance = resident CTAs of the grid (LOR_APF=0: off)
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, smem + pad);
+    static const bool apf = !(getenv("LOR_APF") && !atoi(getenv("LOR_APF")));
+    AsmArgs b = a;
+    b.pf_dist = apf ? (int64_t)nsm * occ : 0;
+    k<<<(unsigned)a.nel_local, 128, smem + pad, st>>>(b);
   };
   if (quad == 0) {
     if (DIM == 3 && SP == SP_H1 && minb == 8) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 8 : 4>);

@@ -100,6 +100,9 @@ struct SpaceDev {
   int2 *xhalo = nullptr;
   uint8_t *xpos = nullptr;
   uint32_t *xpiece = nullptr;
+  // one rank: element restriction of the element pass (k_dofmap at setup), NULL otherwise
+  int32_t *emap = nullptr;
+  int8_t *esgn = nullptr;
   int xc[3] = {0, 0, 0};
 };
 
@@ -325,6 +328,8 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.ownbase = S.ownbase;
   a.ownpos = S.ownpos;
   a.dbg = getenv("LOR_DBG") ? atoi(getenv("LOR_DBG")) : 0;
+  a.emap = S.emap;
+  a.esgn = S.esgn;
   CUDA_TRY(c, launch_assemble(c->dim, s, c->p, (int)quad, a, c->stream, nullptr));
   if (c->nel_local > 0) c->launches++;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
@@ -703,6 +708,26 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     a.ownbase = S.ownbase;
     a.ownpos = S.ownpos;
     if (launch_assemble(A.dim, s, A.p, 0, a, c->stream, nullptr) != cudaSuccess) return bail(LOR_ERR_CUDA, "own-row positions");
+  }
+  // one rank: the element restriction of every space, computed once (k_dofmap) and read by the
+  // element pass instead of rebuilding its block table per call (LOR_EMAP=0: off)
+  if (c->nranks == 1 && c->nel_local > 0 && !(getenv("LOR_EMAP") && !atoi(getenv("LOR_EMAP")))) {
+    for (int s = 0; s < 3; ++s) {
+      SpaceDev &S = c->sp[s];
+      if (!S.valid) continue;
+      const size_t n = (size_t)c->nel_local * S.ndpe;
+      if (dev_alloc(c, &S.emap, n) != cudaSuccess || dev_alloc(c, &S.esgn, n) != cudaSuccess)
+        return bail(LOR_ERR_OUT_OF_MEMORY, "element restriction");
+      DofmapArgs d;
+      d.p = A.p;
+      d.ndpe = S.ndpe;
+      d.nel_local = c->nel_local;
+      d.topo = c->topo;
+      fill_base(S, d.base);
+      d.map = S.emap;
+      d.sign = S.esgn;
+      if (launch_dofmap(A.dim, s, d, c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "element restriction");
+    }
   }
   // extended-frame H1 path: regular-neighbourhood check, element records, box and position tables
   if (A.dim == 3 && c->sp[SP_H1].valid && c->nel_local > 0 && !(getenv("LOR_XFRAME") && !atoi(getenv("LOR_XFRAME")))) {

@@ -90,6 +90,12 @@ struct AsmArgs {
   int *err;                      // [0] code, [1] element, [2] cell
   unsigned long long *tstamp;    // optional [grid][16] per-CTA phase clocks (LOR_PHASE_TIMING=1)
   int dbg;                       // dev experiments (LOR_DBG bits; 0 in production)
+  // one-rank assembly: the element restriction (global id and orientation sign of every local dof)
+  // from setup (lor_setup runs k_dofmap once; reused like the HO element restriction, PAPER.md
+  // l.537), so the element pass skips its block-table prologue.  NULL: computed per element.
+  const int32_t *emap = nullptr; // [nel_local][NDPE]
+  const int8_t *esgn = nullptr;  // [nel_local][NDPE] +-1
+  int64_t pf_dist = 0;           // L2 prefetch of the prologue data of CTA blockIdx + pf_dist (0: off)
 };
 
 struct PlanArgs {
