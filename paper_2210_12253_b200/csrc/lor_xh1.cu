@@ -79,11 +79,18 @@ struct XCfg {
   static constexpr int NR = ONE ? NB : 2;          // resident cell layers (ring)
   static constexpr int NP1 = P + 1;
   static constexpr int MAXROW = KZ * NP1 * NP1;     // rows per chunk (<= 125 for P <= 4, (P+1)^2 else)
-  static constexpr int OFF_XG = 3 * NPB * 8;
-  static constexpr int OFF_CM = (OFF_XG + NPB * 4 + 15) / 16 * 16;
+  // one chunk: E-vector box and cells are contiguous, and the staging of the element's rows (values
+  // and int32 columns, 12 B per entry) is placed over both once the cells have been read; ring:
+  // the restriction sits between them, staging uses one ring slot (values + uint16 box points)
+  static constexpr int XEB = 3 * NPB * 8;
+  static constexpr int STAGE1 = MAXROW * 27 * 12;
+  static constexpr int OFF_CM_1 = XEB;
+  static constexpr int CMB_1 = (XEB + NR * LAY * CP * 8 >= STAGE1) ? NR * LAY * CP * 8 : (STAGE1 - XEB + 15) / 16 * 16;
+  static constexpr int OFF_XG = ONE ? OFF_CM_1 + CMB_1 : XEB;
+  static constexpr int OFF_CM = ONE ? OFF_CM_1 : (OFF_XG + NPB * 4 + 15) / 16 * 16;
   static constexpr int MAXP = MAXROW + (MAXROW * 27 + XPIECE_N - 1) / XPIECE_N + 1;  // pieces per chunk
   static constexpr int NCHUNK = ONE ? 1 : P + 1;
-  static constexpr int OFF_MT = OFF_CM + NR * LAY * CP * 8;              // per chunk row: out int64
+  static constexpr int OFF_MT = ONE ? (OFF_XG + NPB * 4 + 15) / 16 * 16 : OFF_CM + NR * LAY * CP * 8;  // per chunk row: out int64
   static constexpr int OFF_SO = OFF_MT + 8 * MAXROW;                      // per chunk row: staging offset
   static constexpr int OFF_PC = OFF_SO + 4 * MAXROW;                      // the chunk's write-out pieces
   static constexpr int SMEM = OFF_PC + 4 * MAXP;
@@ -91,8 +98,7 @@ struct XCfg {
   // position order, rows in ascending row order (setup), and the box point of each column
   // (uint16), placed over cell storage no longer needed (one chunk: all of it; ring: the slot the
   // next chunk overwrites first)
-  static constexpr int STAGE = MAXROW * 27 * 10;
-  static_assert(STAGE <= (ONE ? NR * LAY * CP * 8 : LAY * CP * 8), "stage does not fit");
+  static_assert(ONE ? STAGE1 <= XEB + CMB_1 : MAXROW * 27 * 10 <= LAY * CP * 8, "stage does not fit");
   static_assert(MAXROW <= 128, "one row per thread per chunk");
   static_assert(MAXROW * 27 <= 4096, "12-bit staging offsets");
   static_assert(MAXP <= 256, "two piece records per thread");
@@ -425,7 +431,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   constexpr int NR = CF::NR;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_bad;
-  double *XE = reinterpret_cast<double *>(smem);
+  double *XE = reinterpret_cast<double *>(smem);  // one chunk: also the start of the staging area
   int32_t *XG = reinterpret_cast<int32_t *>(smem + CF::OFF_XG);
   double *cm = reinterpret_cast<double *>(smem + CF::OFF_CM);
   int64_t *m_out = reinterpret_cast<int64_t *>(smem + CF::OFF_MT);
@@ -583,8 +589,9 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       pf_h.x = -1;
     }
     // stage: ONE chunk -> all cells; ring -> the slot of layer z0-1 (next chunk's first write)
-    stage_v = CF::ONE ? cm : cm + (((z0 - 1 - clo2) % NR + NR) % NR) * LAY * CP;
-    uint16_t *stage_p = reinterpret_cast<uint16_t *>(stage_v + CF::MAXROW * 27);  // box point of the column
+    stage_v = CF::ONE ? XE : cm + (((z0 - 1 - clo2) % NR + NR) % NR) * LAY * CP;
+    uint16_t *stage_p = reinterpret_cast<uint16_t *>(stage_v + CF::MAXROW * 27);  // ring: box point of the column
+    int32_t *stage_c = reinterpret_cast<int32_t *>(stage_v + CF::MAXROW * 27);    // one chunk: the column
     if (hasrow) {
       const int so = (int)(pw[7] & 0xffffu);  // the row's staging offset (setup: ascending row order)
 #pragma unroll
@@ -592,7 +599,9 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
         const int ps = (int)((pw[jj >> 2] >> (8 * (jj & 3))) & 255u);
         if (ps != 255) {
           stage_v[so + ps] = acc[jj];
-          stage_p[so + ps] = (uint16_t)(px + (jj % 3 - 1) + PB * ((jj / 3) % 3 - 1) + PB * PB * (jj / 9 - 1));
+          const int pt = px + (jj % 3 - 1) + PB * ((jj / 3) % 3 - 1) + PB * PB * (jj / 9 - 1);
+          if constexpr (CF::ONE) stage_c[so + ps] = XG[pt];
+          else stage_p[so + ps] = (uint16_t)pt;
         }
       }
       m_out[tid] = out;
@@ -612,7 +621,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       for (int u = 0; u < XPIECE_N / 32; ++u) {
         const int k = lane + 32 * u;
         if (k < n) {
-          __stcs(A.col + o + k, XG[stage_p[s0 + k]]);
+          __stcs(A.col + o + k, CF::ONE ? stage_c[s0 + k] : XG[stage_p[s0 + k]]);
           __stcs(A.val + o + k, stage_v[s0 + k]);
         }
       }
