@@ -101,6 +101,8 @@ struct XFillArgs {
   int *err;
   unsigned long long *tstamp;  // debug (LOR_PHASE_TIMING=1): per-CTA phase clocks, 16 per CTA
   int64_t pf_dist;             // L2 prefetch distance in CTAs (resident CTAs of the grid; 0: off)
+  uint8_t cperm[128];          // one-chunk kernels: thread -> box cell (>= ncell: none), set by the launcher
+  uint8_t cinv[128];           // box cell -> thread (storage slot)
 };
 
 // host: regular-neighbourhood check and per-element extended-frame records (nranks == 1)

@@ -13,6 +13,7 @@
 //             the row (setup position table: ascending global column order, reading P-5).
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <cstring>
 #include <stdint.h>
 
 #include "lor_device.cuh"
@@ -82,7 +83,13 @@ struct XCfg {
   // one chunk: E-vector box and cells are contiguous, and the staging of the element's rows (values
   // and int32 columns, 12 B per entry) is placed over both once the cells have been read; ring:
   // the restriction sits between them, staging uses one ring slot (values + uint16 box points)
-  static constexpr int XEB = 3 * NPB * 8;
+  // E-vector box in shared memory: point (u0, u1, u2) at u0 + XR u1 + XS u2 per component (pitch
+  // XN).  One chunk: odd pitches (P = 4: 7, 43) so that a thread->cell assignment exists in which
+  // the 16 lanes of every half-warp read distinct banks (cell_perm); ring: dense
+  static constexpr int XR = ONE ? (PB % 2 ? PB : PB + 1) : PB;
+  static constexpr int XS = ONE ? PB * XR + 1 : PB * PB;
+  static constexpr int XN = ONE ? XS * PB : NPB;
+  static constexpr int XEB = 3 * XN * 8;
   static constexpr int STAGE1 = MAXROW * 27 * 12;
   static constexpr int OFF_CM_1 = XEB;
   static constexpr int CMB_1 = (XEB + NR * LAY * CP * 8 >= STAGE1) ? NR * LAY * CP * 8 : (STAGE1 - XEB + 15) / 16 * 16;
@@ -93,7 +100,8 @@ struct XCfg {
   static constexpr int OFF_MT = ONE ? (OFF_XG + NPB * 4 + 15) / 16 * 16 : OFF_CM + NR * LAY * CP * 8;  // per chunk row: out int64
   static constexpr int OFF_SO = OFF_MT + 8 * MAXROW;                      // per chunk row: staging offset
   static constexpr int OFF_PC = OFF_SO + 4 * MAXROW;                      // the chunk's write-out pieces
-  static constexpr int SMEM = OFF_PC + 4 * MAXP;
+  static constexpr int OFF_INV = OFF_PC + 4 * MAXP;                      // one chunk: cell -> storage slot
+  static constexpr int SMEM = OFF_INV + (ONE ? 128 : 0);
   // staging of a chunk's rows for the coalesced write-out: the values of every row in final
   // position order, rows in ascending row order (setup), and the box point of each column
   // (uint16), placed over cell storage no longer needed (one chunk: all of it; ring: the slot the
@@ -366,9 +374,9 @@ __host__ __device__ constexpr bool first_touch(int q, int a, int b) {
   return true;
 }
 
-template <int NPB, int PB>
+template <int XN, int XR, int XS>
 __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, double a8, double b8, double *__restrict__ o) {
-  auto X = [&](int v, int k) -> double { return XE[k * NPB + pb + (v & 1) + PB * (((v >> 1) & 1) + PB * ((v >> 2) & 1))]; };
+  auto X = [&](int v, int k) -> double { return XE[k * XN + pb + (v & 1) + XR * ((v >> 1) & 1) + XS * ((v >> 2) & 1)]; };
   // accumulate in the cell's (thread-private) shared-memory row: the first corner touching an
   // entry stores, later ones add (compile-time after unrolling)
   auto put = [&](int q, int ea, int eb, double v) {
@@ -437,6 +445,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   int64_t *m_out = reinterpret_cast<int64_t *>(smem + CF::OFF_MT);
   int32_t *m_so = reinterpret_cast<int32_t *>(smem + CF::OFF_SO);
   uint32_t *m_pc = reinterpret_cast<uint32_t *>(smem + CF::OFF_PC);
+  uint8_t *s_inv = smem + CF::OFF_INV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if ((int64_t)blockIdx.x >= A.nel_local) return;
   const int64_t bs = blockIdx.x;  // processing slot: element record, restriction, gather list, pieces
@@ -473,6 +482,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   const int pbase = -(clo0 + PB * (clo1 + PB * clo2));  // box-local index of lattice point 0
   {
     if (tid == 0) s_bad = 0;
+    if (CF::ONE && tid < NB * NB * NB) s_inv[tid] = A.cinv[tid];
     // extended element restriction (setup): global id of every point of the box
     const int32_t *xm = A.xmap + bs * NPB;
     for (int i = tid; i < NPB; i += blockDim.x) XG[i] = __ldg(xm + i);
@@ -481,7 +491,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     for (int rr = tid; rr < 3 * NP1 * NP1; rr += blockDim.x) {
       const int d = rr / (NP1 * NP1), x12 = rr - d * NP1 * NP1, x1 = x12 % NP1, x2 = x12 / NP1;
       const double *src = xs + d * NPT + x12 * NP1;
-      double *dst = XE + d * NPB + pbase + PB * (x1 + PB * x2);
+      double *dst = XE + d * CF::XN + (x1 - clo1) * CF::XR + (x2 - clo2) * CF::XS - clo0;
 #pragma unroll
       for (int i = 0; i < NP1; ++i) dst[i] = __ldg(src + i);
     }
@@ -490,9 +500,10 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     for (int h = tid; h < HC; h += blockDim.x) {
       const int2 hv = __ldg(hl + h);
       if (hv.x >= 0) {
-        XE[hv.y] = __ldg(A.X + hv.x);
-        XE[NPB + hv.y] = __ldg(A.X + hv.x + NPT);
-        XE[2 * NPB + hv.y] = __ldg(A.X + hv.x + 2 * NPT);
+        const int q = hv.y % PB + CF::XR * ((hv.y / PB) % PB) + CF::XS * (hv.y / (PB * PB));
+        XE[q] = __ldg(A.X + hv.x);
+        XE[CF::XN + q] = __ldg(A.X + hv.x + NPT);
+        XE[2 * CF::XN + q] = __ldg(A.X + hv.x + 2 * NPT);
       }
     }
   }
@@ -513,12 +524,16 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     if (c1 >= c0) {
       const int ncell = (c1 - c0 + 1) * LAY;
       const double a8 = 0.125 * alpha, b8 = 0.125 * beta;
-      for (int c = tid; c < ncell; c += blockDim.x) {
-        const int ux = c % NB, uy = (c / NB) % NB, uz = c0 - clo2 + c / LAY;  // box-local cell
+      for (int c = tid; c < (CF::ONE ? 128 : ncell); c += blockDim.x) {
+        // one chunk: thread -> cell by the bank-conflict-free permutation, cell stored at slot = thread
+        const int cc = CF::ONE ? (int)A.cperm[c] : c;
+        if (cc >= ncell) continue;
+        const int ux = cc % NB, uy = (cc / NB) % NB, uz = c0 - clo2 + cc / LAY;  // box-local cell
         if (ux >= ex0 || uy >= ex1) continue;
         const bool own = clo0 + ux >= 0 && clo0 + ux < P && clo1 + uy >= 0 && clo1 + uy < P && clo2 + uz >= 0 &&
                          clo2 + uz < P;
-        if (!cell_h1v<NPB, PB>(XE, ux + PB * (uy + PB * uz), a8, b8, cm + ((uz % NR) * LAY + uy * NB + ux) * CP) && own)
+        double *dstc = cm + (CF::ONE ? c : ((uz % NR) * LAY + uy * NB + ux)) * CP;
+        if (!cell_h1v<CF::XN, CF::XR, CF::XS>(XE, ux + CF::XR * uy + CF::XS * uz, a8, b8, dstc) && own)
           s_bad = 1 + (clo0 + ux) + P * ((clo1 + uy) + P * (clo2 + uz));
       }
     }
@@ -570,7 +585,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
         const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
         const int cx = u0 - ox, cy = u1 - oy, cz = u2 - oz;
         if (cx < 0 || cx >= ex0 || cy < 0 || cy >= ex1 || cz < 0 || cz >= ex2) continue;
-        const double *ce = cm + ((cz % NR) * LAY + cy * NB + cx) * CP;
+        const double *ce = cm + (CF::ONE ? (int)s_inv[cz * LAY + cy * NB + cx] : ((cz % NR) * LAY + cy * NB + cx)) * CP;
 #pragma unroll
         for (int jc = 0; jc < 8; ++jc) {
           if (body_diag(o, jc)) continue;
@@ -691,6 +706,37 @@ static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_ou
   }
   XFillArgs b = a;
   b.pf_dist = resident;
+  // one chunk: thread -> cell permutation.  The 64-bit E-vector loads of a half-warp are conflict
+  // free when its 16 cells have distinct (ux + XR uy + XS uz) mod 16: the i-th cell of every residue
+  // class goes to half-warp i.  Used when every class has NB^3/16 rounded down or up members, so
+  // that the cells occupy threads (= storage slots) 0 .. NB^3-1; identity otherwise.
+  static bool pinit = false;
+  static uint8_t perm[128], inv[128];
+  if (!pinit) {
+    constexpr int N3 = NB * NB * NB;
+    int cls[16][16], ncls[16] = {0};
+    bool ok = CF::ONE && N3 <= 128;
+    for (int c = 0; c < N3 && ok; ++c) {
+      const int r = (c % NB + CF::XR * ((c / NB) % NB) + CF::XS * (c / (NB * NB))) % 16;
+      if (ncls[r] >= 16) ok = false;
+      else cls[r][ncls[r]++] = c;
+    }
+    int lo = 128, hi = 0;
+    for (int r = 0; r < 16; ++r) { lo = ncls[r] < lo ? ncls[r] : lo; hi = ncls[r] > hi ? ncls[r] : hi; }
+    ok = ok && hi - lo <= 1 && hi <= 8;
+    for (int t = 0; t < 128; ++t) { perm[t] = (uint8_t)(t < N3 ? t : 255); inv[t] = (uint8_t)t; }
+    if (ok) {
+      int t = 0;
+      for (int i = 0; i < hi; ++i)
+        for (int r = 0; r < 16; ++r)
+          if (i < ncls[r]) perm[t++] = (uint8_t)cls[r][i];
+      for (int q = t; q < 128; ++q) perm[q] = 255;
+      for (int q = 0; q < t; ++q) inv[perm[q]] = (uint8_t)q;
+    }
+    pinit = true;
+  }
+  memcpy(b.cperm, perm, 128);
+  memcpy(b.cinv, inv, 128);
   k<<<(unsigned)a.nel_local, 128, smem, st>>>(b);
   return cudaGetLastError();
 }
