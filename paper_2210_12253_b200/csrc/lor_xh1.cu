@@ -92,7 +92,8 @@ struct XCfg {
   static constexpr int XEB = 3 * XN * 8;
   static constexpr int STAGE1 = MAXROW * 27 * 12;
   static constexpr int OFF_CM_1 = XEB;
-  static constexpr int CMB_1 = (XEB + NR * LAY * CP * 8 >= STAGE1) ? NR * LAY * CP * 8 : (STAGE1 - XEB + 15) / 16 * 16;
+  static constexpr int NSL = ONE ? 128 : NR * LAY;  // cell storage slots (one chunk: slot = thread)
+  static constexpr int CMB_1 = (XEB + NSL * CP * 8 >= STAGE1) ? NSL * CP * 8 : (STAGE1 - XEB + 15) / 16 * 16;
   static constexpr int OFF_XG = ONE ? OFF_CM_1 + CMB_1 : XEB;
   static constexpr int OFF_CM = ONE ? OFF_CM_1 : (OFF_XG + NPB * 4 + 15) / 16 * 16;
   static constexpr int MAXP = MAXROW + (MAXROW * 27 + XPIECE_N - 1) / XPIECE_N + 1;  // pieces per chunk
@@ -690,7 +691,7 @@ static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_ou
   constexpr int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
-  constexpr int MINB = (smem <= 44 * 1024) ? XMINB : 3;
+  constexpr int MINB = ((smem + 1024) * 5 <= 228 * 1024) ? XMINB : 3;  // 228 KB shared memory per SM
   auto k = k_xh1_fill<P, NB, MINB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -725,7 +726,14 @@ static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_ou
     for (int r = 0; r < 16; ++r) { lo = ncls[r] < lo ? ncls[r] : lo; hi = ncls[r] > hi ? ncls[r] : hi; }
     ok = ok && hi - lo <= 1 && hi <= 8;
     for (int t = 0; t < 128; ++t) { perm[t] = (uint8_t)(t < N3 ? t : 255); inv[t] = (uint8_t)t; }
-    if (ok) {
+    // the 5^3 box of p = 4 (C2): the schedule of scripts/gen_cell_schedule.py, which also makes the
+    // row gather of interior elements conflict free (4 x 4 cell windows on distinct banks)
+    static const uint8_t k545[128] = {31, 6, 32, 33, 36, 40, 2, 23, 9, 10, 19, 26, 13, 16, 17, 39, 20, 45, 7, 8, 11, 44, 37, 3, 41, 14, 15, 12, 27, 28, 34, 18, 24, 82, 70, 75, 61, 85, 90, 52, 5, 55, 43, 65, 96, 66, 78, 35, 0, 49, 50, 79, 120, 21, 94, 38, 53, 59, 60, 69, 63, 77, 30, 68, 56, 25, 54, 58, 100, 1, 71, 72, 73, 103, 109, 46, 47, 116, 67, 255, 106, 107, 83, 99, 86, 62, 22, 101, 122, 91, 92, 93, 76, 97, 117, 84, 4, 57, 108, 95, 104, 112, 51, 121, 88, 123, 105, 114, 115, 48, 255, 80, 81, 29, 74, 111, 124, 89, 113, 87, 102, 42, 64, 110, 119, 255, 98, 118};
+    if (P == 4 && NB == 5 && CF::XR == 7 && CF::XS == 43) {
+      for (int q = 0; q < 128; ++q) perm[q] = k545[q];
+      for (int q = 0; q < 128; ++q)
+        if (perm[q] != 255) inv[perm[q]] = (uint8_t)q;
+    } else if (ok) {
       int t = 0;
       for (int i = 0; i < hi; ++i)
         for (int r = 0; r < 16; ++r)
