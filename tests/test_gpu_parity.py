@@ -152,3 +152,23 @@ def test_full_size_c2_row_sampled(torch_cuda, oracle_lib):
     d = np.diff(rp)
     assert d.min() >= 8 and d.max() == 27
     assert (np.diff(col.astype(np.int64)).reshape(-1)[np.diff(np.repeat(np.arange(q["n_local"]), d)) == 0] > 0).all()
+
+
+@pytest.mark.parametrize("space", ["h1", "nd", "rt"])
+def test_setup_restriction_path_bitwise(torch_cuda, monkeypatch, space):
+    """One-rank element pass reading the setup element restriction (k_dofmap) gives
+    bit-identical CSR arrays to the per-element block-table path (LOR_EMAP=0); H1 through the
+    element pass (extended-frame path off)."""
+    from paper_2210_12253_b200.lor import LOR
+    m = mg.box_mesh(3, (3, 3, 2), 3, jitter=True, scramble=True)
+    monkeypatch.setenv("LOR_XFRAME", "0")
+    out = []
+    for emap in ("1", "0"):
+        monkeypatch.setenv("LOR_EMAP", emap)
+        ctx = LOR(m)
+        rp, col, val = ctx.assemble(space, 1.3, 0.7, "vertex")
+        ctx.sync()
+        out.append((to_host(rp), to_host(col), to_host(val)))
+        ctx.close()
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
