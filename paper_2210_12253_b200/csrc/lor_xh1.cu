@@ -525,9 +525,10 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     if (c1 >= c0) {
       const int ncell = (c1 - c0 + 1) * LAY;
       const double a8 = 0.125 * alpha, b8 = 0.125 * beta;
-      for (int c = tid; c < (CF::ONE ? 128 : ncell); c += blockDim.x) {
-        // one chunk: thread -> cell by the bank-conflict-free permutation, cell stored at slot = thread
-        const int cc = CF::ONE ? (int)A.cperm[c] : c;
+      for (int c = tid; c < (CF::ONE ? 128 : 128 * (c1 - c0 + 1)); c += blockDim.x) {
+        // thread -> cell by the bank-conflict-free permutation (one chunk: the whole box, cell
+        // stored at slot = thread; ring: one layer per 128 threads, natural slots)
+        const int cc = CF::ONE ? (int)A.cperm[c] : ((int)A.cperm[c & 127] < LAY ? (int)A.cperm[c & 127] + LAY * (c >> 7) : ncell);
         if (cc >= ncell) continue;
         const int ux = cc % NB, uy = (cc / NB) % NB, uz = c0 - clo2 + cc / LAY;  // box-local cell
         if (ux >= ex0 || uy >= ex1) continue;
@@ -649,6 +650,48 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
 }
 
 // ============================================================================== launchers
+// Proper edge colouring of the bipartite multigraph (L[i], R[i]) (classes < 16) with `colors`
+// colours (Koenig: possible when no class has more than `colors` edges), by alternating-path
+// recolouring.  Used to give every half-warp (one colour) cells with distinct bank residues.
+static bool konig16(int n, const int *L, const int *R, int colors, int *col) {
+  int atL[16][8], atR[16][8];
+  if (colors > 8) return false;
+  for (int a = 0; a < 16; ++a)
+    for (int k = 0; k < 8; ++k) atL[a][k] = atR[a][k] = -1;
+  int path[256];
+  for (int i = 0; i < n; ++i) {
+    const int u = L[i], v = R[i];
+    int a = -1, b = -1;
+    for (int k = 0; k < colors && a < 0; ++k)
+      if (atL[u][k] < 0) a = k;
+    for (int k = 0; k < colors && b < 0; ++k)
+      if (atR[v][k] < 0) b = k;
+    if (a < 0 || b < 0) return false;
+    if (a != b && atR[v][a] >= 0) {  // flip the a/b path that starts at v with its a-edge
+      int np = 0, node = v, k = a;
+      bool right = true;
+      for (;;) {
+        const int e = right ? atR[node][k] : atL[node][k];
+        if (e < 0 || np >= 256) break;
+        path[np++] = e;
+        node = right ? L[e] : R[e];
+        right = !right;
+        k = (k == a) ? b : a;
+      }
+      for (int q = 0; q < np; ++q) { atL[L[path[q]]][col[path[q]]] = -1; atR[R[path[q]]][col[path[q]]] = -1; }
+      for (int q = 0; q < np; ++q) {
+        col[path[q]] = (col[path[q]] == a) ? b : a;
+        atL[L[path[q]]][col[path[q]]] = path[q];
+        atR[R[path[q]]][col[path[q]]] = path[q];
+      }
+    }
+    col[i] = a;
+    atL[u][a] = i;
+    atR[v][a] = i;
+  }
+  return true;
+}
+
 template <int P>
 static cudaError_t xh1_setup_p(const XSetupArgs &a, cudaStream_t st) {
   if (a.nel_local <= 0) return cudaSuccess;
@@ -729,7 +772,23 @@ static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_ou
     // the 5^3 box of p = 4 (C2): the schedule of scripts/gen_cell_schedule.py, which also makes the
     // row gather of interior elements conflict free (4 x 4 cell windows on distinct banks)
     static const uint8_t k545[128] = {31, 6, 32, 33, 36, 40, 2, 23, 9, 10, 19, 26, 13, 16, 17, 39, 20, 45, 7, 8, 11, 44, 37, 3, 41, 14, 15, 12, 27, 28, 34, 18, 24, 82, 70, 75, 61, 85, 90, 52, 5, 55, 43, 65, 96, 66, 78, 35, 0, 49, 50, 79, 120, 21, 94, 38, 53, 59, 60, 69, 63, 77, 30, 68, 56, 25, 54, 58, 100, 1, 71, 72, 73, 103, 109, 46, 47, 116, 67, 255, 106, 107, 83, 99, 86, 62, 22, 101, 122, 91, 92, 93, 76, 97, 117, 84, 4, 57, 108, 95, 104, 112, 51, 121, 88, 123, 105, 114, 115, 48, 255, 80, 81, 29, 74, 111, 124, 89, 113, 87, 102, 42, 64, 110, 119, 255, 98, 118};
-    if (P == 4 && NB == 5 && CF::XR == 7 && CF::XS == 43) {
+    if (!CF::ONE && NB * NB <= 128) {
+      // ring: per layer, the cells of a half-warp read distinct E-vector banks (ux + XR uy) and
+      // write distinct cell-storage banks (slot = uy NB + ux, pitch CP = 3 mod 16)
+      constexpr int N2 = NB * NB;
+      int Lc[128], Rc[128], col[128];
+      for (int c = 0; c < N2; ++c) {
+        Lc[c] = (c % NB + CF::XR * (c / NB)) % 16;
+        Rc[c] = (c * (CF::CP % 16)) % 16;
+      }
+      for (int t = 0; t < 128; ++t) perm[t] = 255;
+      if (konig16(N2, Lc, Rc, 8, col)) {
+        int fill[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int c = 0; c < N2; ++c) perm[16 * col[c] + fill[col[c]]++] = (uint8_t)c;
+      } else {
+        for (int t = 0; t < 128; ++t) perm[t] = (uint8_t)(t < N2 ? t : 255);
+      }
+    } else if (P == 4 && NB == 5 && CF::XR == 7 && CF::XS == 43) {
       for (int q = 0; q < 128; ++q) perm[q] = k545[q];
       for (int q = 0; q < 128; ++q)
         if (perm[q] != 255) inv[perm[q]] = (uint8_t)q;
