@@ -193,6 +193,11 @@ struct AsmCfg {
   static constexpr int OFF_RL = OFF_TS + NT * TSB;                         // row order list uint16[MAXR]
   static constexpr int SMEM = (OFF_RL + 2 * MAXR + 15) / 16 * 16;
   static_assert(TZS >= W, "slot positions overwrite the block-size bytes");
+  // CTAs per SM the shared memory allows (228 KB per SM, 1 KB reserved per CTA), 2..5: the
+  // register budget of __launch_bounds__ follows it (ND: 3 -> 168 registers, no spills)
+  static constexpr int MINB_FIT = (228 * 1024) / (SMEM + 1024);
+  static constexpr int MINB_CAP = (DIM == 3 && SP == SP_H1) ? 5 : 4;  // measured best caps (RT at 5 spills)
+  static constexpr int MINB_SMEM = MINB_FIT > MINB_CAP ? MINB_CAP : (MINB_FIT < 2 ? 2 : MINB_FIT);
 };
 
 
@@ -955,7 +960,7 @@ cudaError_t launch_asm_p(const AsmArgs &a, int quad, cudaStream_t st, int *smem_
     if (DIM == 3 && SP == SP_H1 && minb == 8) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 8 : 4>);
     else if (DIM == 3 && SP == SP_H1 && minb == 6) run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 6 : 4>);
     else if (DIM == 3 && SP == SP_H1 && minb == 4) run(k_assemble<DIM, SP, P, 0, KZ, 4>);
-    else run(k_assemble<DIM, SP, P, 0, KZ, (DIM == 3 && SP == SP_H1) ? 5 : 4>);
+    else run(k_assemble<DIM, SP, P, 0, KZ, CF::MINB_SMEM>);
   } else {
     run(k_assemble<DIM, SP, P, 1, KZ, 4>);
   }
