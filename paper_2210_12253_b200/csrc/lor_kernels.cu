@@ -204,25 +204,37 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(const int32_t *__restrict__ cnt
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
-  const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_I;
-  int v[SCAN_I];
-  long long tsum = 0;
+  const int64_t tb = tile * SCAN_TILE;
+  const int64_t base = tb + (int64_t)threadIdx.x * SCAN_I;
+  // the tile's counts are read coalesced (lane = consecutive rows) and transposed through shared
+  // memory to the blocked order of the per-thread scan; the row offsets go back the same way.
+  // Row-major [SCAN_T][SCAN_I + 1] (padded: conflict-free in both directions).
+  __shared__ long long s_buf[SCAN_T * (SCAN_I + 1)];
+  auto padi = [](int e) { return (e / SCAN_I) * (SCAN_I + 1) + e % SCAN_I; };
 #pragma unroll
   for (int i = 0; i < SCAN_I; ++i) {
-    const int64_t k = base + i;
-    if (pos) {
-      int c = 0;
-      if (k < n) {
+    const int e = i * SCAN_T + threadIdx.x;
+    const int64_t k = tb + e;
+    int c = 0;
+    if (k < n) {
+      if (pos) {
         const uint4 *pr = reinterpret_cast<const uint4 *>(pos + k * 32);
         const uint4 a = __ldcs(pr), b = __ldcs(pr + 1);
         const unsigned w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int q = 0; q < 7; ++q) c += 4 - (__popc(__vcmpeq4(w[q], 0xffffffffu)) >> 3);  // word 7: stage offset
+      } else {
+        c = cnt[k];
       }
-      v[i] = c;
-    } else {
-      v[i] = (k < n) ? cnt[k] : 0;
     }
+    s_buf[padi(e)] = c;
+  }
+  __syncthreads();
+  int v[SCAN_I];
+  long long tsum = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_I; ++i) {
+    v[i] = (int)s_buf[threadIdx.x * (SCAN_I + 1) + i];
     tsum += v[i];
   }
   // block-level exclusive scan of thread sums
@@ -281,11 +293,16 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(const int32_t *__restrict__ cnt
   long long run = s_prefix + texcl;
 #pragma unroll
   for (int i = 0; i < SCAN_I; ++i) {
-    const int64_t k = base + i;
-    if (k < n) row_ptr[k] = run;
+    s_buf[threadIdx.x * (SCAN_I + 1) + i] = run;  // own counts were read before the barrier above
     run += v[i];
   }
   if (base <= n - 1 && n - 1 < base + SCAN_I) row_ptr[n] = run;  // thread holding the last item
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < SCAN_I; ++i) {
+    const int e = i * SCAN_T + threadIdx.x;
+    if (tb + e < n) row_ptr[tb + e] = s_buf[padi(e)];
+  }
   if (n == 0 && tile == 0 && threadIdx.x == 0) row_ptr[0] = 0;
 }
 
