@@ -172,3 +172,29 @@ def test_setup_restriction_path_bitwise(torch_cuda, monkeypatch, space):
         ctx.close()
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("cfg,space", [("C4", "nd"), ("C5", "rt")])
+def test_full_size_c4_c5_row_sampled(torch_cuda, oracle_lib, cfg, space):
+    """C4 (Nedelec) and C5 (Raviart-Thomas), 32^3 hexes, p = 4, in the launch configuration bench.py
+    times: nnz from the pattern closed forms, sampled rows vs the oracle,
+    sorted unique columns in every row."""
+    from paper_2210_12253_b200.lor import LOR
+    m, form = mg.config_mesh(cfg)
+    assert form["space"] == space
+    ctx = LOR(m)
+    q = ctx.query(space)
+    expect = {"nd": (6390144, 208306560), "rt": (6340608, 69255168)}[space]
+    assert (q["n_local"], q["nnz"]) == expect
+    rp, col, val = ctx.assemble(space, form["alpha"], form["beta"], form["quad"])
+    ctx.sync()
+    rp, col, val = to_host(rp), to_host(col), to_host(val)
+    rng = np.random.default_rng(7)
+    rows = np.unique(np.concatenate([rng.integers(0, q["n_local"], 2000), [0, q["n_local"] - 1]]))
+    ref = oracle_lib.assemble_rows(m, rows, space, "vertex", form["alpha"], form["beta"])
+    compare_rows(rp, col, val, ref, 0, what=f"{cfg} sampled")
+    d = np.diff(rp)
+    assert d.max() == {"nd": 33, "rt": 11}[space]
+    same_row = np.diff(np.repeat(np.arange(q["n_local"]), d)) == 0
+    assert (np.diff(col.astype(np.int64))[same_row] > 0).all()
+    ctx.close()
