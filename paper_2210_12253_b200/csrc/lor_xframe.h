@@ -56,8 +56,8 @@ constexpr int XPOS_W = 32;  // position-table row: bytes 0-26 final CSR position
 
 // write-out piece (one per <= 128 consecutive CSR entries of one run of consecutive owned rows of a
 // chunk): bits 0-11 staging offset of the first entry, 12-18 chunk row (thread) of the run's first
-// row, 19-26 number of entries
-constexpr int XPIECE_N = 128;
+// row, 19-27 number of entries
+constexpr int XPIECE_N = 256;
 
 struct XSetupArgs {
   int64_t nel_local;
