@@ -95,6 +95,8 @@ lor_status lor_destroy(lor_ctx ctx);
 /* Waits on the context stream; returns DEGENERATE_GEOMETRY if any sub-cell had det J <= 0
  * in an earlier call (message names element and sub-cell), CUDA on launch failures. */
 lor_status lor_sync(lor_ctx ctx);
+/* Message of the last failure on ctx; lor_last_error(NULL) returns the message of this thread's last
+ * failed lor_setup / lor_plan_dry_run (which have no context to hold it). */
 const char *lor_last_error(lor_ctx ctx);
 
 /* Sizes of the assembled operator of `space` on this rank (synchronous, fixed at setup). */
@@ -128,6 +130,16 @@ lor_status lor_discrete_curl(lor_ctx ctx, lor_csr *out);
  * DESIGN.md, signs[...] in {-1,+1} (NULL allowed; must be NULL-or-valid for H1).
  * DEVICE buffers.  n_elem_local = elem_rank_begin[rank+1] - elem_rank_begin[rank]. */
 lor_status lor_dof_map(lor_ctx ctx, lor_space space, int32_t *elem_dofs, int8_t *signs);
+/* Transpose of the element restriction (the dof -> element "inverse offsets", PAPER.md l.412-415
+ * and SURVEY 8(b)): for every owned row r (local index, [0, n_rows_local)) the list of
+ * (local element * ndof_per_el + local dof) pairs of this rank's elements whose dof is r, in
+ * ascending order: entries[offsets[r] .. offsets[r+1]).  offsets[n_rows_local+1] int64, entries
+ * int32, both caller-owned DEVICE buffers; cap_entries >= lor_query_transpose's count, else
+ * BUFFER_TOO_SMALL with nothing written.  On one rank this is the complete transpose; on several
+ * ranks it lists the pairs of the rank's own elements only.  Enqueued on the context stream
+ * (count, scan, fill, per-row sort).  INVALID_ARGUMENT if n_elem_local * ndof_per_el >= 2^31. */
+lor_status lor_query_transpose(lor_ctx ctx, lor_space space, int64_t *n_entries);
+lor_status lor_dof_transpose(lor_ctx ctx, lor_space space, int64_t *offsets, int32_t *entries, int64_t cap_entries);
 lor_status lor_query_elements(lor_ctx ctx, int64_t *elem_begin, int64_t *n_elem_local, int *ndof_per_el_h1,
                               int *ndof_per_el_nd, int *ndof_per_el_rt);
 

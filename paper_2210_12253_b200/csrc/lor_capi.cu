@@ -104,6 +104,8 @@ struct SpaceDev {
   int32_t *emap = nullptr;
   int8_t *esgn = nullptr;
   int xc[3] = {0, 0, 0};
+  int64_t n_tr = 0;             // entries of the dof transpose (local elements x owned local dofs)
+  int32_t *trmap = nullptr;     // element restriction workspace of lor_dof_transpose (nranks > 1)
 };
 
 }  // namespace
@@ -127,6 +129,7 @@ struct lor_ctx_s {
   cudaEvent_t ev[8] = {};
   int nphase = 0;
   int fin_smem = 0;
+  int dbg = 0;  // LOR_DBG at setup (dev experiments; 0 in production)
   std::vector<void *> allocs;
 };
 
@@ -148,6 +151,9 @@ int64_t class_rows(int dim, int space, int p, int tau) {
   }
   return tot;
 }
+
+// message of the last failed lor_setup / lor_plan_dry_run (no context exists then), per thread
+thread_local std::string g_setup_error;
 
 lor_status fail(lor_ctx c, lor_status st, const std::string &msg) {
   if (c) c->last_error = msg;
@@ -327,7 +333,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.tstamp = c->tstamp;
   a.ownbase = S.ownbase;
   a.ownpos = S.ownpos;
-  a.dbg = getenv("LOR_DBG") ? atoi(getenv("LOR_DBG")) : 0;
+  a.dbg = c->dbg;
   a.emap = S.emap;
   a.esgn = S.esgn;
   CUDA_TRY(c, launch_assemble(c->dim, s, c->p, (int)quad, a, c->stream, nullptr));
@@ -395,7 +401,7 @@ lor_status lor_plan_dry_run(const lor_setup_args *args, int64_t *info, int64_t *
     in.elem_rank_begin = A.elem_rank_begin;
     plan.build(in);
   } catch (const std::exception &ex) {
-    fprintf(stderr, "lor_plan_dry_run: %s\n", ex.what());
+    g_setup_error = std::string("lor_plan_dry_run: ") + ex.what();
     return LOR_ERR_INVALID_ARGUMENT;
   }
   for (int s = 0; s < 3; ++s) {
@@ -418,14 +424,20 @@ lor_status lor_plan_dry_run(const lor_setup_args *args, int64_t *info, int64_t *
 }
 
 lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
-  if (!out) return LOR_ERR_INVALID_ARGUMENT;
+  g_setup_error.clear();
+  if (!out || !args) {
+    g_setup_error = "lor_setup: null args/out";
+    return LOR_ERR_INVALID_ARGUMENT;
+  }
   *out = nullptr;
-  if (!args) return LOR_ERR_INVALID_ARGUMENT;
   const lor_setup_args &A = *args;
   if (!(A.dim == 2 || A.dim == 3) || A.p < 1 || A.p > 8 || A.n_vert <= 0 || A.n_elem <= 0 || !A.elem_vert ||
       A.nranks < 1 || A.rank < 0 || A.rank >= A.nranks || (!A.elem_nodes && !A.vert_xyz) ||
-      (A.nranks > 1 && !A.elem_rank_begin))
+      (A.nranks > 1 && !A.elem_rank_begin)) {
+    g_setup_error = "lor_setup: invalid argument (dim in {2,3}, 1 <= p <= 8, counts > 0, non-null arrays, "
+                    "0 <= rank < nranks, elem_rank_begin when nranks > 1)";
     return LOR_ERR_INVALID_ARGUMENT;
+  }
   lor_ctx c = new lor_ctx_s();
   c->dim = A.dim;
   c->p = A.p;
@@ -434,9 +446,12 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
   c->device = A.device;
   c->stream = reinterpret_cast<cudaStream_t>(A.cuda_stream);
   c->nel = A.n_elem;
+  c->dbg = getenv("LOR_DBG") ? atoi(getenv("LOR_DBG")) : 0;
   auto bail = [&](lor_status st, const std::string &msg) {
+    cudaError_t ce = cudaGetLastError();
+    g_setup_error = "lor_setup: " + msg;
+    if (ce != cudaSuccess) g_setup_error += std::string(" (") + cudaGetErrorString(ce) + ")";
     lor_destroy(c);
-    (void)msg;
     return st;
   };
   if (cudaSetDevice(A.device) != cudaSuccess) return bail(LOR_ERR_CUDA, "cudaSetDevice");
@@ -453,8 +468,9 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     in.elem_rank_begin = A.elem_rank_begin;
     plan.build(in);
   } catch (const std::exception &ex) {
-    fprintf(stderr, "lor_setup: %s\n", ex.what());
     return bail(LOR_ERR_INVALID_ARGUMENT, ex.what());
+  } catch (...) {
+    return bail(LOR_ERR_OUT_OF_MEMORY, "host plan: allocation failure");
   }
   c->elem_begin = plan.elem_begin;
   c->nel_local = plan.nel_local;
@@ -544,6 +560,10 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     S.n_global = P.n_global;
     S.row_begin = P.row_begin;
     S.n_local = P.n_local;
+    S.n_tr = 0;
+    for (int64_t e = 0; e < plan.nel_local; ++e)
+      for (int tau = 0; tau < (A.dim == 3 ? 27 : 9); ++tau)
+        if (plan.topo[e].flags[tau] & TF_OWNED) S.n_tr += class_rows(A.dim, s, A.p, tau);
     for (int t = 0; t < 4; ++t)
       if (dev_upload(c, &S.base[t], P.base[t].data(), P.base[t].size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "base");
     if (dev_upload(c, &S.esp, P.esp.data(), P.esp.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "esp");
@@ -824,7 +844,7 @@ lor_status lor_sync(lor_ctx c) {
   return LOR_OK;
 }
 
-const char *lor_last_error(lor_ctx c) { return c ? c->last_error.c_str() : "null context"; }
+const char *lor_last_error(lor_ctx c) { return c ? c->last_error.c_str() : g_setup_error.c_str(); }
 
 lor_status lor_query(lor_ctx c, lor_space space, int64_t *n_rows_local, int64_t *row_begin, int64_t *n_rows_global,
                      int64_t *nnz_local) {
@@ -960,6 +980,46 @@ lor_status lor_dof_map(lor_ctx c, lor_space space, int32_t *elem_dofs, int8_t *s
   a.sign = signs;
   CUDA_TRY(c, launch_dofmap(c->dim, space, a, c->stream));
   c->launches++;
+  return LOR_OK;
+}
+
+lor_status lor_query_transpose(lor_ctx c, lor_space space, int64_t *n_entries) {
+  if (!c || space < 0 || space > 2 || !n_entries) return LOR_ERR_INVALID_ARGUMENT;
+  const SpaceDev &S = c->sp[space];
+  if (!S.valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
+  *n_entries = S.n_tr;
+  return LOR_OK;
+}
+
+lor_status lor_dof_transpose(lor_ctx c, lor_space space, int64_t *offsets, int32_t *entries, int64_t cap_entries) {
+  if (!c || space < 0 || space > 2 || !offsets || (!entries && cap_entries > 0)) return LOR_ERR_INVALID_ARGUMENT;
+  SpaceDev &S = c->sp[space];
+  if (!S.valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
+  if (cap_entries < S.n_tr) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_entries < lor_query_transpose");
+  if ((int64_t)c->nel_local * S.ndpe >= (int64_t(1) << 31))
+    return fail(c, LOR_ERR_INVALID_ARGUMENT, "n_elem_local * ndof_per_el exceeds int32");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int32_t *map = S.emap;
+  if (!map) {  // element restriction of this rank's elements into a context workspace
+    if (!S.trmap) {
+      CUDA_TRY(c, cudaMalloc((void **)&S.trmap, sizeof(int32_t) * std::max<int64_t>(1, c->nel_local * S.ndpe)));
+      c->allocs.push_back(S.trmap);
+    }
+    DofmapArgs a;
+    a.p = c->p;
+    a.ndpe = S.ndpe;
+    a.nel_local = c->nel_local;
+    a.topo = c->topo;
+    fill_base(S, a.base);
+    a.map = S.trmap;
+    a.sign = nullptr;
+    CUDA_TRY(c, launch_dofmap(c->dim, space, a, c->stream));
+    c->launches++;
+    map = S.trmap;
+  }
+  CUDA_TRY(c, launch_transpose(map, c->nel_local * S.ndpe, S.row_begin, S.n_local, S.cnt, offsets, entries,
+                               S.scan_status, S.tile_ctr, c->stream));
+  c->launches += 4;
   return LOR_OK;
 }
 

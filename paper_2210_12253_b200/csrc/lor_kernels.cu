@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "lor_cells.cuh"
 #include "lor_device.cuh"
 #include "lor_kernels.h"
@@ -583,6 +585,57 @@ __global__ void __launch_bounds__(128) k_dofmap(DofmapArgs A) {
     A.map[el * A.ndpe + l] = B.g0 + B.str[0] * x[0] + B.str[1] * x[1] + B.str[2] * x[2];
     if (A.sign) A.sign[el * A.ndpe + l] = B.sigma;
   }
+}
+
+// ================================================================================ dof transpose
+// The dof -> (element, local dof) transpose of the element restriction (the paper's "inverse
+// offsets" of the element restriction): rows = this rank's owned dofs, entries
+// = local element * ndpe + local dof, ascending.  Count (integer atomics), scan (k_scan), fill
+// (atomic cursor), then each row's few entries sorted in place (insertion sort; valence <= 255).
+__global__ void k_tr_count(const int32_t *__restrict__ map, int64_t n_ent, int64_t row_begin, int64_t n_local,
+                           int32_t *__restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_ent; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = (int64_t)__ldg(map + i) - row_begin;
+    if (r >= 0 && r < n_local) atomicAdd(cnt + r, 1);
+  }
+}
+
+__global__ void k_tr_fill(const int32_t *__restrict__ map, int64_t n_ent, int64_t row_begin, int64_t n_local,
+                          const int64_t *__restrict__ off, int32_t *__restrict__ cursor, int32_t *__restrict__ ent) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_ent; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = (int64_t)__ldg(map + i) - row_begin;
+    if (r >= 0 && r < n_local) ent[off[r] + atomicAdd(cursor + r, 1)] = (int32_t)i;
+  }
+}
+
+__global__ void k_tr_sort(const int64_t *__restrict__ off, int64_t n_local, int32_t *__restrict__ ent) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_local; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = off[r], e = off[r + 1];
+    for (int64_t a = s + 1; a < e; ++a) {
+      const int32_t v = ent[a];
+      int64_t b = a;
+      while (b > s && ent[b - 1] > v) {
+        ent[b] = ent[b - 1];
+        --b;
+      }
+      ent[b] = v;
+    }
+  }
+}
+
+cudaError_t launch_transpose(const int32_t *map, int64_t n_ent, int64_t row_begin, int64_t n_local, int32_t *cnt,
+                             int64_t *off, int32_t *ent, unsigned long long *status, unsigned int *tile_ctr,
+                             cudaStream_t st) {
+  const unsigned ge = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_ent + 255) / 256, 148 * 16));
+  const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_local + 255) / 256, 148 * 16));
+  cudaError_t e;
+  if (n_local > 0 && (e = cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n_local, st)) != cudaSuccess) return e;
+  k_tr_count<<<ge, 256, 0, st>>>(map, n_ent, row_begin, n_local, cnt);
+  if ((e = launch_scan(cnt, off, n_local, status, tile_ctr, st)) != cudaSuccess) return e;
+  if (n_local > 0 && (e = cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n_local, st)) != cudaSuccess) return e;
+  k_tr_fill<<<ge, 256, 0, st>>>(map, n_ent, row_begin, n_local, off, cnt, ent);
+  k_tr_sort<<<gr, 256, 0, st>>>(off, n_local, ent);
+  return cudaGetLastError();
 }
 
 __global__ void k_rowptr_stride(int64_t *row_ptr, int64_t n, int w) {

@@ -175,5 +175,11 @@ cudaError_t launch_merge_rows(const MergeArgs &a, cudaStream_t st);
 cudaError_t launch_discrete(int which, const DiscArgs &a, cudaStream_t st);
 cudaError_t launch_rowptr_stride(int64_t *row_ptr, int64_t n, int w, cudaStream_t st);
 cudaError_t launch_dofmap(int dim, int space, const DofmapArgs &a, cudaStream_t st);
+// dof -> (local element * ndpe + local dof) transpose of an element restriction map[n_ent] for the
+// owned rows [row_begin, row_begin + n_local): off[n_local+1], ent[off[n_local]] ascending per row.
+// Launches 4 kernels (count, scan, fill, sort).
+cudaError_t launch_transpose(const int32_t *map, int64_t n_ent, int64_t row_begin, int64_t n_local, int32_t *cnt,
+                             int64_t *off, int32_t *ent, unsigned long long *status, unsigned int *tile_ctr,
+                             cudaStream_t st);
 
 }  // namespace lorb

@@ -343,8 +343,12 @@ __host__ __device__ constexpr int cidx(int a, int b) {
 }
 __host__ __device__ constexpr bool body_diag(int a, int b) { return (a ^ b) == 7; }
 
-// 1/x for x > 0: float seed + two Newton steps (relative error ~1e-28 before rounding)
+// 1/x for x > 0: float seed + two Newton steps (relative error ~1e-28 before rounding).  The
+// seed is only valid where x is a normal float away from overflow: outside [2^-120, 2^120] (cell
+// volumes of meshes scaled far from unit size, e.g. coordinates x 1e-14) the true division runs
+// instead, so the result never depends on the float range (tests/test_gpu_parity.py scaled meshes).
 __device__ __forceinline__ double rcp_pos(double x) {
+  if (__builtin_expect(!(x > 7.52316384526264e-37 && x < 1.329227995784916e36), 0)) return 1.0 / x;
   float rf;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)x));
   double r = (double)rf;
@@ -407,7 +411,7 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
     cross3x(j[0], j[1], r[2]);
     const double det = dot3x(j[0], r[0]);
     ok = ok && det > 0.0;
-    const double sa = a8 * rcp_pos(det);  // |det| within float range (cell volumes > 1e-37)
+    const double sa = a8 * rcp_pos(det);
     double Q[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -532,11 +536,11 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
         if (cc >= ncell) continue;
         const int ux = cc % NB, uy = (cc / NB) % NB, uz = c0 - clo2 + cc / LAY;  // box-local cell
         if (ux >= ex0 || uy >= ex1) continue;
-        const bool own = clo0 + ux >= 0 && clo0 + ux < P && clo1 + uy >= 0 && clo1 + uy < P && clo2 + uz >= 0 &&
-                         clo2 + uz < P;
         double *dstc = cm + (CF::ONE ? c : ((uz % NR) * LAY + uy * NB + ux)) * CP;
-        if (!cell_h1v<CF::XN, CF::XR, CF::XS>(XE, ux + CF::XR * uy + CF::XS * uz, a8, b8, dstc) && own)
-          s_bad = 1 + (clo0 + ux) + P * ((clo1 + uy) + P * (clo2 + uz));
+        // det J <= 0 in any cell of the box -- own or a neighbour's, which may be computed by no
+        // other CTA (an element owning no rows) -- is reported (extended-frame cell coordinates)
+        if (!cell_h1v<CF::XN, CF::XR, CF::XS>(XE, ux + CF::XR * uy + CF::XS * uz, a8, b8, dstc))
+          s_bad = 1 + (clo0 + ux + 1) + (P + 2) * ((clo1 + uy + 1) + (P + 2) * (clo2 + uz + 1));
       }
     }
     __syncthreads();
@@ -550,7 +554,23 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       }
       if (tid < HC) pf_h = __ldg(A.xhalo + nbs * HC + tid);
     }
-    if (s_bad && tid == 0) { xreport(A.err, 2, A.elem_begin + el, s_bad - 1); s_bad = 0; }
+    if (s_bad && tid == 0) {  // map the extended-frame cell to (element, cell) of the element it lies in
+      const int b = s_bad - 1, q[3] = {b % (P + 2) - 1, (b / (P + 2)) % (P + 2) - 1, b / ((P + 2) * (P + 2)) - 1};
+      const int ni = (q[0] < 0 ? 0 : (q[0] >= P ? 2 : 1)) + 3 * (q[1] < 0 ? 0 : (q[1] >= P ? 2 : 1)) +
+                     9 * (q[2] < 0 ? 0 : (q[2] >= P ? 2 : 1));
+      int64_t ee = el;
+      int kc[3] = {q[0], q[1], q[2]};
+      if (ni != 13) {
+        const XNbr nb = A.xe[bs].nbr[ni];
+        ee = nb.el;
+        int y0[3] = {q[0], q[1], q[2]}, y1[3] = {q[0] + 1, q[1] + 1, q[2] + 1}, L0[3], L1[3];
+        x_to_local(P, nb.code, y0, L0);
+        x_to_local(P, nb.code, y1, L1);
+        for (int a = 0; a < 3; ++a) kc[a] = L0[a] < L1[a] ? L0[a] : L1[a];
+      }
+      xreport(A.err, 2, A.elem_begin + ee, kc[0] + P * (kc[1] + P * kc[2]));
+      s_bad = 0;
+    }
     // the chunk's write-out pieces (setup), consumed after the staging barrier
     const uint32_t *pcs = A.piece + (bs * CF::NCHUNK + ch) * (1 + CF::MAXP);
     const int npc = (int)__ldg(pcs);

@@ -74,6 +74,8 @@ def lib():
         L.lor_update_coordinates.argtypes = [C.c_void_p, C.c_void_p]
         L.lor_last_phase_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float), C.c_int]
         L.lor_fill_path.argtypes = [C.c_void_p, C.c_int]
+        L.lor_query_transpose.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int64)]
+        L.lor_dof_transpose.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64]
         _lib = L
     return _lib
 
@@ -104,7 +106,7 @@ def plan_dry_run(mesh, rank=0, nranks=1, elem_rank_begin=None):
     recv = np.zeros((3, nranks), dtype=np.int64)
     rc = lib().lor_plan_dry_run(C.byref(a), info.ctypes.data, send.ctypes.data, recv.ctypes.data)
     if rc:
-        raise LorError(rc, "lor_plan_dry_run")
+        raise LorError(rc, lib().lor_last_error(None).decode())
     return info, send, recv
 
 
@@ -142,7 +144,7 @@ class LOR:
         h = C.c_void_p()
         rc = lib().lor_setup(C.byref(a), C.byref(h))
         if rc:
-            raise LorError(rc, "lor_setup failed (see stderr)")
+            raise LorError(rc, lib().lor_last_error(None).decode())
         self.h = h
         self.rank, self.nranks = rank, nranks
         eb, ne = C.c_int64(), C.c_int64()
@@ -244,6 +246,20 @@ class LOR:
         fn = lib().lor_discrete_grad if which in ("grad", 0) else lib().lor_discrete_curl
         self._check(fn(self.h, C.byref(self._csr(*out))))
         return out
+
+    def dof_transpose(self, space="h1"):
+        """(offsets[n_local+1] int64, entries int32) device tensors: per owned row the ascending
+        local element * ndpe + local dof pairs of this rank's elements (lor_dof_transpose)."""
+        t = self.torch
+        sp = SPACES.get(space, space)
+        n = C.c_int64()
+        self._check(lib().lor_query_transpose(self.h, sp, C.byref(n)))
+        q = self.query(sp)
+        off = t.empty(q["n_local"] + 1, dtype=t.int64, device=self.device)
+        ent = t.empty(max(n.value, 1), dtype=t.int32, device=self.device)
+        self._check(lib().lor_dof_transpose(self.h, sp, C.c_void_p(off.data_ptr()), C.c_void_p(ent.data_ptr()),
+                                            C.c_int64(ent.numel())))
+        return off, ent[:n.value]
 
     def dof_map(self, space="h1"):
         t = self.torch

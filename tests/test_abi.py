@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -64,3 +65,24 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle|lor_oracle|liblor_oracle", txt, re.M), f
+
+
+def test_setup_error_message_without_context():
+    """lor_setup has no context to hold its message: lor_last_error(NULL) returns it (boundary
+    defect of round 1: the binding printed 'see stderr' with nothing on stderr)."""
+    import ctypes
+    from paper_2210_12253_b200 import meshgen as mg
+    from paper_2210_12253_b200.lor import _SetupArgs, lib
+    L = lib()
+    m = mg.box_mesh(3, (2, 2, 2), 2)
+    vert = np.ascontiguousarray(m.vert)
+    elem = np.ascontiguousarray(m.elem, dtype=np.int64)
+    a = _SetupArgs()
+    a.dim, a.p = 3, 9
+    a.n_vert, a.vert_xyz = vert.shape[0], vert.ctypes.data
+    a.n_elem, a.elem_vert = elem.shape[0], elem.ctypes.data
+    a.rank, a.nranks = 0, 1
+    h = ctypes.c_void_p()
+    assert L.lor_setup(ctypes.byref(a), ctypes.byref(h)) == 1
+    msg = L.lor_last_error(None).decode()
+    assert "invalid argument" in msg and "p <= 8" in msg
