@@ -117,6 +117,16 @@ lor_status lor_assemble_h1(lor_ctx ctx, double alpha, double beta, lor_quad quad
 lor_status lor_assemble_nd(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
 lor_status lor_assemble_rt(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
 
+/* Numeric-only re-assembly (pattern reuse; "mesh motion or time-dependent
+ * variable coefficients"): `out` must hold the row_ptr / col written by an earlier
+ * lor_assemble_<space> call of this context with the same quadrature rule (the pattern is
+ * topological); only the values are recomputed from the current coordinates and alpha, beta.  No
+ * row lengths, no scan; on the extended-frame H1 path col is not written.  Same errors as
+ * lor_assemble_<space>; the caller guarantees the buffers are unchanged since that call. */
+lor_status lor_reassemble_h1(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
+lor_status lor_reassemble_nd(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
+lor_status lor_reassemble_rt(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
+
 /* Discrete gradient, Algorithm 1: row i (owned ND dof) has -sigma_i at the
  * H1 id of the edge's local tail and +sigma_i at its head, columns sorted; row_ptr[i] = 2i.
  * Discrete curl: row f (owned RT dof) has +-1 on its 4 LOR edges
@@ -183,9 +193,10 @@ int64_t lor_kernel_launches(lor_ctx ctx);
 int lor_last_phase_ms(lor_ctx ctx, float *ms, int cap);
 
 /* Which value-fill path lor_assemble_<space> takes with the vertex rule: 1 = extended-frame
- * single pass (every element writes the complete rows it owns, recomputing the
- * neighbour cells that touch them; 3D H1, one rank, meshes whose elements all have a regular
- * 3x3x3 coarse neighbourhood -- checked at setup), 0 = element pass + merge pass of partial rows.
+ * single pass (per call: row lengths k_xh1_count, scan, then every element writes the complete
+ * rows it owns, column positions derived from its extended restriction and the
+ * neighbour cells that touch its rows recomputed; 3D H1, one rank, meshes whose elements all have
+ * a regular 3x3x3 coarse neighbourhood -- checked at setup), 0 = element pass + merge pass.
  * LOR_XFRAME=0 in the environment at setup forces 0.  Returns -1 for an invalid context/space. */
 int lor_fill_path(lor_ctx ctx, lor_space space);
 

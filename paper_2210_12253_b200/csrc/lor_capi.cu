@@ -98,12 +98,11 @@ struct SpaceDev {
   XBox *xbox = nullptr;
   int32_t *xmap = nullptr;
   int2 *xhalo = nullptr;
-  uint8_t *xpos = nullptr;
-  uint32_t *xpiece = nullptr;
   // one rank: element restriction of the element pass (k_dofmap at setup), NULL otherwise
   int32_t *emap = nullptr;
   int8_t *esgn = nullptr;
   int xc[3] = {0, 0, 0};
+  uint32_t *xpos = nullptr;     // extended-frame path: per-call slot positions [n_local][8]
   int64_t n_tr = 0;             // entries of the dof transpose (local elements x owned local dofs)
   int32_t *trmap = nullptr;     // element restriction workspace of lor_dof_transpose (nranks > 1)
 };
@@ -252,7 +251,32 @@ lor_status finish(lor_ctx c, int s, lor_csr *out) {
   return LOR_OK;
 }
 
-lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, lor_csr *out) {
+XFillArgs xfill_args(lor_ctx c, const SpaceDev &S) {
+  XFillArgs x{};
+  x.nel_local = c->nel_local;
+  x.elem_begin = c->elem_begin;
+  x.order = c->order;
+  x.xe = S.xe;
+  x.xmap = S.xmap;
+  x.xhalo = S.xhalo;
+  x.X = c->X;
+  x.xstride = c->xstride;
+  x.row_begin = S.row_begin;
+  x.cnt = S.cnt;
+  x.pos = S.xpos;
+  x.sort32 = (S.n_global < (int64_t(1) << 26) && !(c->dbg & 1)) ? 1 : 0;  // LOR_DBG bit 0: force the rank path
+  x.ncx = S.xc[0];
+  x.ncy = S.xc[1];
+  x.ncz = S.xc[2];
+  x.err = c->err;
+  x.tstamp = c->tstamp;
+  return x;
+}
+
+// reuse = true: numeric-only re-assembly into buffers holding the pattern of an earlier full call of
+// the same space (NEXT-3): no row lengths, no scan; the extended-frame path
+// stores values only.
+lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, lor_csr *out, bool reuse = false) {
   if (!c) return LOR_ERR_INVALID_ARGUMENT;
   if (s < 0 || s > 2 || !c->sp[s].valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available for this mesh");
   if (quad != LOR_QUAD_VERTEX && quad != LOR_QUAD_GAUSS2) return fail(c, LOR_ERR_INVALID_ARGUMENT, "bad quadrature");
@@ -264,37 +288,28 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   c->nphase = 0;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   lor_status st = LOR_OK;
-  if (S.xok && quad == LOR_QUAD_VERTEX) {  // row counts from the extended-frame position table
-    CUDA_TRY(c, launch_scan(S.cnt, out->row_ptr, S.n_local, S.scan_status, S.tile_ctr, c->stream, S.xpos));
-    c->launches++;
-  } else {
-    st = run_count_scan(c, s, out->row_ptr);
-    if (st) return st;
+  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX;
+  if (!reuse) {  // symbolic part (A2): row lengths per call, then the int64 scan
+    if (xpath) {
+      XFillArgs x = xfill_args(c, S);
+      CUDA_TRY(c, launch_xh1_count(c->p, x, c->stream));
+      if (c->nel_local > 0) c->launches++;
+      CUDA_TRY(c, launch_scan(S.cnt, out->row_ptr, S.n_local, S.scan_status, S.tile_ctr, c->stream));
+      c->launches++;
+    } else {
+      st = run_count_scan(c, s, out->row_ptr);
+      if (st) return st;
+    }
   }
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
-  if (S.xok && quad == LOR_QUAD_VERTEX) {  // extended-frame path: every owned row in one pass
-    XFillArgs x{};
-    x.nel_local = c->nel_local;
-    x.elem_begin = c->elem_begin;
-    x.order = c->order;
-    x.xe = S.xe;
-    x.xmap = S.xmap;
-    x.xhalo = S.xhalo;
-    x.pos = S.xpos;
-    x.piece = S.xpiece;
-    x.X = c->X;
-    x.xstride = c->xstride;
-    x.row_begin = S.row_begin;
+  if (xpath) {  // extended-frame path: every owned row in one pass
+    XFillArgs x = xfill_args(c, S);
     x.row_ptr = out->row_ptr;
     x.col = out->col;
     x.val = out->val;
     x.alpha = alpha;
     x.beta = beta;
-    x.ncx = S.xc[0];
-    x.ncy = S.xc[1];
-    x.ncz = S.xc[2];
-    x.err = c->err;
-    x.tstamp = c->tstamp;
+    x.values_only = reuse ? 1 : 0;
     CUDA_TRY(c, launch_xh1_fill(c->p, x, c->stream, nullptr));
     if (c->nel_local > 0) c->launches++;
     CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
@@ -772,34 +787,19 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
           dev_alloc(c, &S.xbox, (size_t)c->nel_local * 125) != cudaSuccess ||
           dev_alloc(c, &S.xmap, (size_t)c->nel_local * xmap_points(A.p, S.xc)) != cudaSuccess ||
           dev_alloc(c, &S.xhalo, (size_t)c->nel_local * (xmap_points(A.p, S.xc) - (int64_t)(A.p + 1) * (A.p + 1) * (A.p + 1))) != cudaSuccess ||
-          dev_alloc(c, &S.xpos, (size_t)std::max<int64_t>(S.n_local, 1) * XPOS_W) != cudaSuccess)
+          dev_alloc(c, &S.xpos, (size_t)std::max<int64_t>(S.n_local, 1) * 8) != cudaSuccess)
         return bail(LOR_ERR_OUT_OF_MEMORY, "xframe");
-      int kz = 0, maxrow = 0, maxp = 0, nchunk = 0;
-      xfill_geom(A.p, S.xc, &kz, &maxrow, &maxp, &nchunk);
-      const size_t npiece = (size_t)c->nel_local * nchunk * (1 + maxp);
-      if (nchunk <= 0 || dev_alloc(c, &S.xpiece, npiece) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "xframe");
-      if (cudaMemset(S.xpiece, 0, npiece * sizeof(uint32_t)) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe");
-      if (cudaMemset(S.xpos, 0xff, (size_t)std::max<int64_t>(S.n_local, 1) * XPOS_W) != cudaSuccess)
-        return bail(LOR_ERR_CUDA, "xframe");
-      // S.cnt still holds the H1 row counts of the setup count pass
       XSetupArgs xa{};
       xa.nel_local = c->nel_local;
       xa.xe = S.xe;
       xa.topo = c->topo;
       fill_base(S, xa.base);
       xa.row_begin = S.row_begin;
-      xa.cnt = S.cnt;
       xa.box = S.xbox;
       xa.nb = xfill_nb(A.p, S.xc);
       xa.xmap = S.xmap;
       xa.xhalo = S.xhalo;
       xa.xstride = c->xstride;
-      xa.pos = S.xpos;
-      xa.piece = S.xpiece;
-      xa.kz = kz;
-      xa.maxrow = maxrow;
-      xa.maxp = maxp;
-      xa.nchunk = nchunk;
       xa.err = c->err;
       if (cudaMemset(c->err, 0, 4 * sizeof(int)) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe");
       if (launch_xh1_setup(A.p, xa, c->stream) != cudaSuccess) return bail(LOR_ERR_CUDA, "xframe setup");
@@ -808,6 +808,23 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
       cudaMemcpy(herr, c->err, sizeof(herr), cudaMemcpyDeviceToHost);
       cudaMemset(c->err, 0, sizeof(herr));
       S.xok = herr[0] == 0;
+      if (S.xok) {
+        // the per-call row lengths of the extended-frame path must equal those of the general
+        // minimal-element count (S.cnt still holds them from the nnz pass above)
+        int32_t *xc = nullptr;
+        std::vector<int32_t> h0((size_t)S.n_local), h1((size_t)S.n_local);
+        if (cudaMalloc((void **)&xc, sizeof(int32_t) * std::max<int64_t>(S.n_local, 1)) != cudaSuccess)
+          return bail(LOR_ERR_OUT_OF_MEMORY, "xframe check");
+        XFillArgs x = xfill_args(c, S);
+        x.cnt = xc;
+        cudaMemset(xc, 0, sizeof(int32_t) * std::max<int64_t>(S.n_local, 1));
+        const bool ok = launch_xh1_count(A.p, x, c->stream) == cudaSuccess && cudaStreamSynchronize(c->stream) == cudaSuccess &&
+                        cudaMemcpy(h0.data(), S.cnt, sizeof(int32_t) * S.n_local, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                        cudaMemcpy(h1.data(), xc, sizeof(int32_t) * S.n_local, cudaMemcpyDeviceToHost) == cudaSuccess;
+        cudaFree(xc);
+        if (!ok) return bail(LOR_ERR_CUDA, "xframe check");
+        S.xok = h0 == h1;
+      }
       if (!S.xok) fprintf(stderr, "lor_setup: extended-frame tables inconsistent, using the element + merge passes\n");
     } else if (getenv("LOR_XFRAME_VERBOSE")) {
       fprintf(stderr, "lor_setup: extended-frame path off: %s\n", why.c_str());
@@ -877,6 +894,16 @@ lor_status lor_assemble_nd(lor_ctx c, double alpha, double beta, lor_quad quad, 
 }
 lor_status lor_assemble_rt(lor_ctx c, double alpha, double beta, lor_quad quad, lor_csr *out) {
   return assemble(c, SP_RT, alpha, beta, quad, out);
+}
+
+lor_status lor_reassemble_h1(lor_ctx c, double alpha, double beta, lor_quad quad, lor_csr *out) {
+  return assemble(c, SP_H1, alpha, beta, quad, out, true);
+}
+lor_status lor_reassemble_nd(lor_ctx c, double alpha, double beta, lor_quad quad, lor_csr *out) {
+  return assemble(c, SP_ND, alpha, beta, quad, out, true);
+}
+lor_status lor_reassemble_rt(lor_ctx c, double alpha, double beta, lor_quad quad, lor_csr *out) {
+  return assemble(c, SP_RT, alpha, beta, quad, out, true);
 }
 
 lor_status lor_update_coordinates(lor_ctx c, const double *elem_nodes) {

@@ -195,11 +195,8 @@ __global__ void __launch_bounds__(128) k_count(CountArgs A) {
 constexpr int SCAN_T = 128, SCAN_I = 16, SCAN_TILE = SCAN_T * SCAN_I;
 constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
 
-// pos != NULL: row counts are the numbers of valid (!= 255) slot positions (bytes 0-27) of the
-// extended-frame position table rows (lor_xframe.h, 32 bytes per row) instead of cnt[]
 __global__ void __launch_bounds__(SCAN_T) k_scan(const int32_t *__restrict__ cnt, int64_t *__restrict__ row_ptr, int64_t n,
-                                                 unsigned long long *status, unsigned int *tile_ctr,
-                                                 const uint8_t *__restrict__ pos) {
+                                                 unsigned long long *status, unsigned int *tile_ctr) {
   __shared__ unsigned int s_tile;
   __shared__ long long s_warp[SCAN_T / 32];
   __shared__ long long s_prefix;
@@ -217,19 +214,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan(const int32_t *__restrict__ cnt
   for (int i = 0; i < SCAN_I; ++i) {
     const int e = i * SCAN_T + threadIdx.x;
     const int64_t k = tb + e;
-    int c = 0;
-    if (k < n) {
-      if (pos) {
-        const uint4 *pr = reinterpret_cast<const uint4 *>(pos + k * 32);
-        const uint4 a = __ldcs(pr), b = __ldcs(pr + 1);
-        const unsigned w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int q = 0; q < 7; ++q) c += 4 - (__popc(__vcmpeq4(w[q], 0xffffffffu)) >> 3);  // word 7: stage offset
-      } else {
-        c = cnt[k];
-      }
-    }
-    s_buf[padi(e)] = c;
+    s_buf[padi(e)] = (k < n) ? cnt[k] : 0;
   }
   __syncthreads();
   int v[SCAN_I];
@@ -686,11 +671,11 @@ cudaError_t launch_build_tables(int dim, int space, int p, uint32_t *slot, uint8
 }
 
 cudaError_t launch_scan(const int32_t *cnt, int64_t *row_ptr, int64_t n, unsigned long long *status,
-                        unsigned int *tile_ctr, cudaStream_t st, const uint8_t *pos) {
+                        unsigned int *tile_ctr, cudaStream_t st) {
   const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (tiles + 1), st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(unsigned int), st);
-  k_scan<<<(unsigned)(tiles > 0 ? tiles : 1), SCAN_T, 0, st>>>(cnt, row_ptr, n, status, tile_ctr, pos);
+  k_scan<<<(unsigned)(tiles > 0 ? tiles : 1), SCAN_T, 0, st>>>(cnt, row_ptr, n, status, tile_ctr);
   return cudaGetLastError();
 }
 

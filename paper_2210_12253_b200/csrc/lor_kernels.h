@@ -165,7 +165,7 @@ int64_t tab_size_entries(int dim, int space);
 cudaError_t launch_build_tables(int dim, int space, int p, uint32_t *slot, uint8_t *size, uint32_t *pb, uint8_t *npb,
                                 uint8_t *lex, cudaStream_t st);
 cudaError_t launch_scan(const int32_t *cnt, int64_t *row_ptr, int64_t n, unsigned long long *status,
-                        unsigned int *tile_ctr, cudaStream_t st, const uint8_t *pos = nullptr);
+                        unsigned int *tile_ctr, cudaStream_t st);
 int64_t scan_status_words(int64_t n);
 // smem_out != NULL: only report the dynamic shared memory the kernel needs
 cudaError_t launch_assemble(int dim, int space, int p, int quad, const AsmArgs &a, cudaStream_t st, int *smem_out);

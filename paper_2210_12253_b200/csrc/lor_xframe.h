@@ -50,15 +50,6 @@ struct XBox {
 };
 static_assert(sizeof(XBox) == 8, "layout");
 
-constexpr int XPOS_W = 32;  // position-table row: bytes 0-26 final CSR position of each of the 27 stencil
-                            // slots (255: none), byte 27 unused, bytes 28-29 the row's offset in the
-                            // fill kernel's staging area (its write-out order), bytes 30-31 unused
-
-// write-out piece (one per <= 128 consecutive CSR entries of one run of consecutive owned rows of a
-// chunk): bits 0-11 staging offset of the first entry, 12-18 chunk row (thread) of the run's first
-// row, 19-27 number of entries
-constexpr int XPIECE_N = 256;
-
 struct XSetupArgs {
   int64_t nel_local;
   const XElem *xe;      // [nel_local] in processing order (CTA b -> element xe[b].el); xmap, xhalo,
@@ -66,7 +57,6 @@ struct XSetupArgs {
   const ElemTopo *topo;
   const int32_t *base[4];
   int64_t row_begin;
-  const int32_t *cnt;  // row lengths from k_count (consistency check)
   XBox *box;           // [nel_local][125]
   int nb;              // cell-box extent the fill kernel is built for (p+1 or p+2)
   int32_t *xmap;       // [nel_local][(nb+1)^3] extended element restriction: global id of every point
@@ -75,9 +65,6 @@ struct XSetupArgs {
                        // the element: {E-vector index of the x component (-1: outside [clo, chi+1]),
                        // point index in the box}
   int64_t xstride;
-  uint8_t *pos;        // [n_local][XPOS_W]
-  uint32_t *piece;     // [nel_local][nchunk][1 + maxp]: piece count, then the write-out pieces
-  int kz, maxrow, maxp, nchunk;  // fill-kernel chunking (xfill_geom)
   int *err;            // set to 1 on any inconsistency
 };
 
@@ -87,12 +74,12 @@ struct XFillArgs {
   const XElem *xe;
   const int32_t *xmap;
   const int2 *xhalo;
-  const uint8_t *pos;
-  const uint32_t *piece;
-  int maxp, nchunk;
   const double *X;
   int64_t xstride;
   int64_t row_begin;
+  int32_t *cnt;                // k_xh1_sym output: row lengths [n_local]
+  uint32_t *pos;               // k_xh1_sym output: [n_local][8] final position of each stencil slot
+                               // (bytes 0-26, 255 = not a column)
   const int64_t *row_ptr;
   int32_t *col;
   double *val;
@@ -101,6 +88,8 @@ struct XFillArgs {
   int *err;
   unsigned long long *tstamp;  // debug (LOR_PHASE_TIMING=1): per-CTA phase clocks, 16 per CTA
   int64_t pf_dist;             // L2 prefetch distance in CTAs (resident CTAs of the grid; 0: off)
+  int values_only;             // 1: numeric-only re-assembly, col is not written (pattern reuse)
+  int sort32;                  // 1: n_global < 2^26, the symbolic pass sorts packed 32-bit keys
   uint8_t cperm[128];          // one-chunk kernels: thread -> box cell (>= ncell: none), set by the launcher
   uint8_t cinv[128];           // box cell -> thread (storage slot)
 };
@@ -119,11 +108,9 @@ inline int64_t xmap_points(int p, const int cmax[3]) {
   return (int64_t)pb * pb * pb;
 }
 
-// chunking of the fill kernel instantiated for (p, cmax): row layers per chunk, rows per chunk,
-// write-out pieces per chunk (capacity), chunks per element
-void xfill_geom(int p, const int cmax[3], int *kz, int *maxrow, int *maxp, int *nchunk);
 
 cudaError_t launch_xh1_setup(int p, const XSetupArgs &a, cudaStream_t st);
 cudaError_t launch_xh1_fill(int p, const XFillArgs &a, cudaStream_t st, int *smem_out);
+cudaError_t launch_xh1_count(int p, const XFillArgs &a, cudaStream_t st);  // k_xh1_sym
 
 }  // namespace lorb

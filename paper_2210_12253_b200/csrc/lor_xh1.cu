@@ -16,6 +16,8 @@
 #include <cstring>
 #include <stdint.h>
 
+#include <utility>
+
 #include "lor_device.cuh"
 #include "lor_xframe.h"
 
@@ -96,21 +98,18 @@ struct XCfg {
   static constexpr int CMB_1 = (XEB + NSL * CP * 8 >= STAGE1) ? NSL * CP * 8 : (STAGE1 - XEB + 15) / 16 * 16;
   static constexpr int OFF_XG = ONE ? OFF_CM_1 + CMB_1 : XEB;
   static constexpr int OFF_CM = ONE ? OFF_CM_1 : (OFF_XG + NPB * 4 + 15) / 16 * 16;
-  static constexpr int MAXP = MAXROW + (MAXROW * 27 + XPIECE_N - 1) / XPIECE_N + 1;  // pieces per chunk
   static constexpr int NCHUNK = ONE ? 1 : P + 1;
   static constexpr int OFF_MT = ONE ? (OFF_XG + NPB * 4 + 15) / 16 * 16 : OFF_CM + NR * LAY * CP * 8;  // per chunk row: out int64
-  static constexpr int OFF_SO = OFF_MT + 8 * MAXROW;                      // per chunk row: staging offset
-  static constexpr int OFF_PC = OFF_SO + 4 * MAXROW;                      // the chunk's write-out pieces
-  static constexpr int OFF_INV = OFF_PC + 4 * MAXP;                      // one chunk: cell -> storage slot
+  static constexpr int OFF_SO = OFF_MT + 8 * MAXROW;                      // per chunk row: length
+  static constexpr int OFF_INV = OFF_SO + 4 * MAXROW;                     // one chunk: cell -> storage slot
   static constexpr int SMEM = OFF_INV + (ONE ? 128 : 0);
-  // staging of a chunk's rows for the coalesced write-out: the values of every row in final
-  // position order, rows in ascending row order (setup), and the box point of each column
-  // (uint16), placed over cell storage no longer needed (one chunk: all of it; ring: the slot the
+  // staging of a chunk's rows for the write-out: the values of every row in final position order
+  // in its thread's 27-entry segment, and the column (one chunk: int32) or its box point (ring:
+  // uint16), placed over cell storage no longer needed (one chunk: all of it; ring: the slot the
   // next chunk overwrites first)
   static_assert(ONE ? STAGE1 <= XEB + CMB_1 : MAXROW * 27 * 10 <= LAY * CP * 8, "stage does not fit");
   static_assert(MAXROW <= 128, "one row per thread per chunk");
   static_assert(MAXROW * 27 <= 4096, "12-bit staging offsets");
-  static_assert(MAXP <= 256, "two piece records per thread");
 };
 
 // ============================================================================== setup kernel
@@ -219,118 +218,169 @@ __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
       if (k != hc) atomicExch(A.err, 1);
     }
   }
-  constexpr int NP1 = P + 1;
-  // fill-kernel chunks (owned-row bounding box [olo, ohi], z layers in chunks of KZ): the chunk's
-  // rows are staged in ascending row order (so consecutive rows are consecutive CSR ranges), and
-  // every run of consecutive rows is written out in pieces of <= XPIECE_N entries
-  __shared__ uint16_t so_l[NP1 * NP1 * NP1];
-  __shared__ int s_g[128], s_len[128], s_so[128], s_t[128];
-  {
-    const int rnx = H.ohi[0] - H.olo[0] + 1, rny = H.ohi[1] - H.olo[1] + 1;
-    const int t = threadIdx.x;
-    int ch = 0;
-    for (int z0 = H.olo[2]; z0 <= H.ohi[2]; z0 += CF::KZ, ++ch) {
-      const int z1 = (z0 + CF::KZ - 1 < H.ohi[2]) ? z0 + CF::KZ - 1 : H.ohi[2];
-      const int nrow = rnx * rny * (z1 - z0 + 1);
-      if (ch >= A.nchunk || nrow > CF::MAXROW) atomicExch(A.err, 1);
-      int g = 0x7fffffff, len = 0, l = -1;
-      if (t < nrow && t < CF::MAXROW) {
-        const int q = t / rnx;
-        const int x[3] = {H.olo[0] + t - q * rnx, H.olo[1] + q % rny, z0 + q / rny};
-        const int tau = lcls(x[0], P) + 3 * lcls(x[1], P) + 9 * lcls(x[2], P);
-        if ((H.own >> tau) & 1) {
-          bool okg = true;
-          g = gid(x, okg);
-          const int64_t r = (int64_t)g - A.row_begin;
-          if (!okg || r < 0) {
-            atomicExch(A.err, 1);
-            g = 0x7fffffff;
-          } else {
-            len = A.cnt[r];
-            l = x[0] + NP1 * (x[1] + NP1 * x[2]);
-          }
-        }
-      }
-      s_g[t] = g;
-      s_len[t] = len;
-      __syncthreads();
-      int rank = 0, so = 0;
-      if (l >= 0) {
-        for (int u = 0; u < nrow; ++u)
-          if (s_g[u] < g) {
-            ++rank;
-            so += s_len[u];
-          }
-        if (so + len > 4095) atomicExch(A.err, 1);
-        so_l[l] = (uint16_t)so;
-      }
-      __syncthreads();
-      if (l >= 0) {
-        s_t[rank] = t;
-        s_so[t] = so;
-      }
-      int nr = __syncthreads_count(l >= 0);
-      if (t == 0 && ch < A.nchunk) {
-        uint32_t *pc = A.piece + ((int64_t)e * A.nchunk + ch) * (1 + A.maxp);
-        int np = 0;
-        for (int k = 0; k < nr;) {
-          int k2 = k + 1;
-          while (k2 < nr && s_g[s_t[k2]] == s_g[s_t[k2 - 1]] + 1) ++k2;
-          const int t0 = s_t[k], so0 = s_so[t0];
-          const int tot = s_so[s_t[k2 - 1]] + s_len[s_t[k2 - 1]] - so0;
-          for (int off = 0; off < tot; off += XPIECE_N) {
-            const int n = (tot - off < XPIECE_N) ? tot - off : XPIECE_N;
-            if (np < A.maxp) pc[1 + np] = (uint32_t)(so0 + off) | ((uint32_t)t0 << 12) | ((uint32_t)n << 19);
-            ++np;
-          }
-          k = k2;
-        }
-        if (np > A.maxp) atomicExch(A.err, 1);
-        pc[0] = (uint32_t)np;
-      }
-      __syncthreads();
-    }
-  }
-  for (int l = threadIdx.x; l < NP1 * NP1 * NP1; l += blockDim.x) {
-    const int x[3] = {l % NP1, (l / NP1) % NP1, l / (NP1 * NP1)};
-    const int tau = lcls(x[0], P) + 3 * lcls(x[1], P) + 9 * lcls(x[2], P);
-    if (!((H.own >> tau) & 1)) continue;
-    bool okg = true;
-    const int g = gid(x, okg);
-    int ids[27];
-    int nvalid = 0;
+}
+
+// The 351 pairs (j, k), j < k, of the 27 stencil slots as compile-time indices (a nested unrolled
+// loop is not unrolled by nvcc at this size, which would put key[] in local memory): pair t
+// compares key_k < key_j and moves one count of the rank bytes from k to j (branch-free).
+__host__ __device__ constexpr int pair_j(int t) {
+  int j = 0;
+  while (t >= 26 - j) { t -= 26 - j; ++j; }
+  return j;
+}
+__host__ __device__ constexpr int pair_k(int t) {
+  int j = 0;
+  while (t >= 26 - j) { t -= 26 - j; ++j; }
+  return j + 1 + t;
+}
+template <int T>
+__device__ __forceinline__ void rank_pair(const int (&key)[27], uint32_t (&pw)[7]) {
+  constexpr int j = pair_j(T), k = pair_k(T);
+  const uint32_t lt = (uint32_t)(key[k] < key[j]);
+  pw[j >> 2] += lt << (8 * (j & 3));
+  pw[k >> 2] -= lt << (8 * (k & 3));
+}
+template <int... T>
+__device__ __forceinline__ void rank_pairs(const int (&key)[27], uint32_t (&pw)[7], std::integer_sequence<int, T...>) {
+  (rank_pair<T>(key, pw), ...);
+}
+
+// Batcher odd-even merge sort network for 32 wires pruned to 27 live inputs (scripts/gen_sort27.py:
+// wires 27..31 hold +inf, comparators onto them dropped; checked there by exhaustive random tests):
+// comparator c = 32 a + b puts min on wire a, max on wire b.
+constexpr uint16_t kNet27[156] = {1, 67, 133, 199, 265, 331, 397, 463, 529, 595, 661, 727, 793, 2, 35, 134, 167, 266, 299, 398, 431, 530, 563, 662, 695, 794, 34, 166, 298, 430, 562, 694, 826, 4, 37, 70, 103, 268, 301, 334, 367, 532, 565, 598, 631, 68, 101, 332, 365, 596, 629, 34, 100, 166, 298, 364, 430, 562, 628, 694, 826, 8, 41, 74, 107, 140, 173, 206, 239, 536, 569, 602, 136, 169, 202, 235, 664, 697, 730, 68, 101, 200, 233, 332, 365, 596, 629, 728, 761, 34, 100, 166, 232, 298, 364, 430, 562, 628, 694, 760, 826, 16, 49, 82, 115, 148, 181, 214, 247, 280, 313, 346, 272, 305, 338, 371, 404, 437, 470, 503, 136, 169, 202, 235, 400, 433, 466, 499, 664, 697, 730, 68, 101, 200, 233, 332, 365, 464, 497, 596, 629, 728, 761, 34, 100, 166, 232, 298, 364, 430, 496, 562, 628, 694, 760, 826};
+template <int C>
+__device__ __forceinline__ void net_cmp(int (&v)[27]) {
+  constexpr int a = kNet27[C] >> 5, b = kNet27[C] & 31;
+  const int lo = min(v[a], v[b]), hi = max(v[a], v[b]);
+  v[a] = lo;
+  v[b] = hi;
+}
+template <int... C>
+__device__ __forceinline__ void sort27(int (&v)[27], std::integer_sequence<int, C...>) {
+  (net_cmp<C>(v), ...);
+}
+
+// Symbolic pass of the extended-frame path, per call (A2: the row lengths the
+// scan turns into I, and where every column goes in its row).  For every owned row of the element
+// (the minimal element containing its coarse entity):
+//   * its length: the stencil points sharing a cell with it -- per axis the offsets d whose cells
+//     [max(x, x+d) - 1, min(x, x+d)] meet the element's cell box, a product over the three axes;
+//   * the final position of each stencil slot in the ascending-column row (reading P-5): the order
+//     of the slot ids (extended element restriction, setup) -- a sorting network on packed keys
+//     (ids < 2^26), else the 351 pairwise comparisons.
+// One CTA (NT threads) per element.  Outputs cnt[row], pos[row][8 words] (bytes 0-26: position,
+// 255 = not a column).
+template <int P, int NB, int NT>
+__global__ void __launch_bounds__(NT) k_xh1_sym(XFillArgs A) {
+  constexpr int PB = NB + 1, NPB = PB * PB * PB;
+  __shared__ int32_t XG[NPB];
+  __shared__ __align__(16) uint8_t s_pos[NT * 28];  // per-thread position scatter
+  __shared__ uint32_t s_cls[P >= 5 ? 125 * 7 : 1];   // p >= 5: positions per row class
+  const int tid = threadIdx.x;
+  const int64_t bs = blockIdx.x;
+  if (bs >= A.nel_local) return;
+  const int4 hw = __ldg(reinterpret_cast<const int4 *>(A.xe + bs));
+  const int32_t *xm = A.xmap + bs * NPB;
+  for (int i = tid; i < NPB; i += NT) XG[i] = __ldg(xm + i);
+  const int clo[3] = {(int8_t)(hw.y & 255), (int8_t)((hw.y >> 8) & 255), (int8_t)((hw.y >> 16) & 255)};
+  const int chi[3] = {(int8_t)((hw.y >> 24) & 255), (int8_t)(hw.z & 255), (int8_t)((hw.z >> 8) & 255)};
+  const int olo[3] = {(int8_t)((hw.z >> 16) & 255), (int8_t)((hw.z >> 24) & 255), (int8_t)(hw.w & 255)};
+  const int ohi[3] = {(int8_t)((hw.w >> 8) & 255), (int8_t)((hw.w >> 16) & 255), (int8_t)((hw.w >> 24) & 255)};
+  const uint32_t own = (uint32_t)hw.x;
+  const int rnx = ohi[0] - olo[0] + 1, rny = ohi[1] - olo[1] + 1, nrow = rnx * rny * (ohi[2] - olo[2] + 1);
+  // positions of one row (lattice point x, per-axis valid-offset masks m)
+  auto row_positions = [&](const int x[3], const int m[3], uint32_t (&pw)[7]) {
+    const int px = (x[0] - clo[0]) + PB * ((x[1] - clo[1]) + PB * (x[2] - clo[2]));
+    int key[27];
+#pragma unroll
     for (int j = 0; j < 27; ++j) {
-      const int y[3] = {x[0] + j % 3 - 1, x[1] + (j / 3) % 3 - 1, x[2] + j / 9 - 1};
-      bool v = true;
+      const int dx = j % 3, dy = (j / 3) % 3, dz = j / 9;
+      const bool v = (m[0] >> dx) & (m[1] >> dy) & (m[2] >> dz) & 1;
+      key[j] = v ? XG[px + (dx - 1) + PB * (dy - 1) + PB * PB * (dz - 1)] : 0x7fffffff;
+    }
+    if (A.sort32) {
+      // sort the keys (id << 5 | slot); position i goes to the slot in the key's low bits (absent
+      // slots sort last: 0x7fffffe0 | slot)
+      int v[27];
+#pragma unroll
+      for (int j = 0; j < 27; ++j) v[j] = key[j] == 0x7fffffff ? (0x7fffffe0 | j) : ((key[j] << 5) | j);
+      sort27(v, std::make_integer_sequence<int, 156>{});
+      uint8_t *sp = s_pos + tid * 28;
+#pragma unroll
+      for (int q2 = 0; q2 < 7; ++q2) reinterpret_cast<uint32_t *>(sp)[q2] = 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < 27; ++i)
+        if (v[i] < 0x7fffffe0) sp[v[i] & 31] = (uint8_t)i;
+#pragma unroll
+      for (int q2 = 0; q2 < 7; ++q2) pw[q2] = reinterpret_cast<const uint32_t *>(sp)[q2];
+    } else {
+      // ranks as bytes: byte k starts at k (every j < k counted as smaller) and each pair (j, k)
+      // moves one count from k to j when key_k < key_j; absent slots carry the largest key
+#pragma unroll
+      for (int q2 = 0; q2 < 7; ++q2) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (4 * q2 + b < 27) w |= (uint32_t)(4 * q2 + b) << (8 * b);
+        pw[q2] = w;
+      }
+      rank_pairs(key, pw, std::make_integer_sequence<int, 351>{});
+#pragma unroll
+      for (int j = 0; j < 27; ++j) pw[j >> 2] |= (key[j] == 0x7fffffff ? 0xffu : 0u) << (8 * (j & 3));
+    }
+  };
+  auto masks = [&](const int x[3], int m[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      m[a] = ((x[a] - 1 >= clo[a] && x[a] - 1 <= chi[a]) ? 1 : 0) | ((x[a] - 1 <= chi[a] && x[a] >= clo[a]) ? 2 : 0) |
+             ((x[a] >= clo[a] && x[a] <= chi[a]) ? 4 : 0);
+  };
+  // p >= 5: rows whose three per-axis classes (x = 0, 1, [2, p-2], p-1, p) agree have the same
+  // coarse entities at the same stencil slots and the same affine order inside each -- hence the
+  // same positions: computed once per class from a representative row (125 classes vs (p+1)^3 rows)
+  constexpr bool CLS = P >= 5;
+  auto acls = [](int x) { return x <= 1 ? x : (x <= P - 2 ? 2 : (x == P - 1 ? 3 : 4)); };
+  __syncthreads();
+  if (CLS) {
+    for (int c = tid; c < 125; c += NT) {
+      const int k[3] = {c % 5, (c / 5) % 5, c / 25};
+      int x[3], m[3];
+      bool in = true;
+#pragma unroll
       for (int a = 0; a < 3; ++a) {
-        int lo = (x[a] > y[a] ? x[a] : y[a]) - 1, hi = x[a] < y[a] ? x[a] : y[a];
-        lo = lo < H.clo[a] ? H.clo[a] : lo;
-        hi = hi > H.chi[a] ? H.chi[a] : hi;
-        v = v && lo <= hi;
+        x[a] = k[a] <= 2 ? k[a] : (k[a] == 3 ? P - 1 : P);
+        in = in && x[a] >= olo[a] && x[a] <= ohi[a];
       }
-      ids[j] = v ? gid(y, okg) : -1;
-      nvalid += v;
+      if (!in) continue;
+      masks(x, m);
+      uint32_t pw[7];
+      row_positions(x, m, pw);
+#pragma unroll
+      for (int q2 = 0; q2 < 7; ++q2) s_cls[c * 7 + q2] = pw[q2];
     }
-    const int64_t r = (int64_t)g - A.row_begin;
-    if (!okg || r < 0 || A.cnt[r] != nvalid) {
-      atomicExch(A.err, 1);
-      continue;
+    __syncthreads();
+  }
+  for (int t = tid; t < nrow; t += NT) {
+    const int q = t / rnx;
+    const int x[3] = {olo[0] + t - q * rnx, olo[1] + q % rny, olo[2] + q / rny};
+    if (!((own >> (lcls(x[0], P) + 3 * lcls(x[1], P) + 9 * lcls(x[2], P))) & 1)) continue;
+    int m[3];
+    masks(x, m);
+    const int px = (x[0] - clo[0]) + PB * ((x[1] - clo[1]) + PB * (x[2] - clo[2]));
+    const int64_t r = (int64_t)XG[px] - A.row_begin;
+    A.cnt[r] = __popc(m[0]) * __popc(m[1]) * __popc(m[2]);
+    uint32_t pw[7];
+    if (CLS) {
+      const int c = acls(x[0]) + 5 * acls(x[1]) + 25 * acls(x[2]);
+#pragma unroll
+      for (int q2 = 0; q2 < 7; ++q2) pw[q2] = s_cls[c * 7 + q2];
+    } else {
+      row_positions(x, m, pw);
     }
-    uint32_t w[XPOS_W / 4];
-    for (int i = 0; i < XPOS_W / 4; ++i) w[i] = 0xffffffffu;
-    w[7] = 0xffff0000u | so_l[l];
-    for (int j = 0; j < 27; ++j) {
-      if (ids[j] < 0) continue;
-      int rk = 0;
-      for (int k = 0; k < 27; ++k) {
-        if (ids[k] >= 0 && ids[k] < ids[j]) ++rk;
-        if (k != j && ids[k] == ids[j]) atomicExch(A.err, 1);
-      }
-      w[j >> 2] = (w[j >> 2] & ~(0xffu << (8 * (j & 3)))) | ((uint32_t)rk << (8 * (j & 3)));
-    }
-    uint4 *dst = reinterpret_cast<uint4 *>(A.pos + r * XPOS_W);
-    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    uint4 *dst = reinterpret_cast<uint4 *>(A.pos + r * 8);
+    dst[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+    dst[1] = make_uint4(pw[4], pw[5], pw[6], 0xffffffffu);
   }
 }
 
@@ -343,12 +393,12 @@ __host__ __device__ constexpr int cidx(int a, int b) {
 }
 __host__ __device__ constexpr bool body_diag(int a, int b) { return (a ^ b) == 7; }
 
-// 1/x for x > 0: float seed + two Newton steps (relative error ~1e-28 before rounding).  The
-// seed is only valid where x is a normal float away from overflow: outside [2^-120, 2^120] (cell
-// volumes of meshes scaled far from unit size, e.g. coordinates x 1e-14) the true division runs
-// instead, so the result never depends on the float range (tests/test_gpu_parity.py scaled meshes).
-__device__ __forceinline__ double rcp_pos(double x) {
-  if (__builtin_expect(!(x > 7.52316384526264e-37 && x < 1.329227995784916e36), 0)) return 1.0 / x;
+// 1/x for x > 0: float seed + two Newton steps (relative error ~1e-28 before rounding).  The seed
+// needs x inside the normal float range: outside [2^-120, 2^120] (cell volumes of meshes scaled far
+// from unit size, e.g. coordinates x 1e-14) x = m 2^e is reduced to m in [0.5, 1) first and the
+// result scaled back by 2^-e (inline, no division slow path), so the result never depends on the
+// float range (tests/test_gpu_boundary.py scaled meshes).
+__device__ __forceinline__ double rcp_newton(double x) {
   float rf;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)x));
   double r = (double)rf;
@@ -356,6 +406,15 @@ __device__ __forceinline__ double rcp_pos(double x) {
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
+}
+__device__ __forceinline__ double rcp_pos(double x) {
+  if (__builtin_expect(x > 7.52316384526264e-37 && x < 1.329227995784916e36, 1)) return rcp_newton(x);
+  const int hi = __double2hiint(x), ex = ((hi >> 20) & 0x7ff) - 1022;  // x = m 2^ex, m in [0.5, 1)
+  const double m = __hiloint2double((hi & 0x800fffff) | (1022 << 20), __double2loint(x));
+  const double r = rcp_newton(m);
+  // 2^-ex in two factors (each a normal double for |ex| <= 1022)
+  const int e1 = -ex / 2, e2 = -ex - e1;
+  return r * __hiloint2double((e1 + 1023) << 20, 0) * __hiloint2double((e2 + 1023) << 20, 0);
 }
 
 // One LOR cell under the vertex rule (reading P-1), computed by one thread with the corner loop
@@ -437,7 +496,9 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
   return ok;
 }
 
-template <int P, int NB, int MINB>
+// WCOL = false: numeric-only re-assembly (pattern reuse): col keeps what the
+// previous full call wrote, only val is stored.
+template <int P, int NB, int MINB, bool WCOL>
 __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   using CF = XCfg<P, NB>;
   constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1, PB = CF::PB, NPB = CF::NPB, LAY = CF::LAY, CP = CF::CP;
@@ -447,9 +508,8 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
   double *XE = reinterpret_cast<double *>(smem);  // one chunk: also the start of the staging area
   int32_t *XG = reinterpret_cast<int32_t *>(smem + CF::OFF_XG);
   double *cm = reinterpret_cast<double *>(smem + CF::OFF_CM);
-  int64_t *m_out = reinterpret_cast<int64_t *>(smem + CF::OFF_MT);
-  int32_t *m_so = reinterpret_cast<int32_t *>(smem + CF::OFF_SO);
-  uint32_t *m_pc = reinterpret_cast<uint32_t *>(smem + CF::OFF_PC);
+  int64_t *m_out = reinterpret_cast<int64_t *>(smem + CF::OFF_MT);  // per chunk row: CSR offset (-1: none)
+  int32_t *m_n = reinterpret_cast<int32_t *>(smem + CF::OFF_SO);     // per chunk row: length
   uint8_t *s_inv = smem + CF::OFF_INV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if ((int64_t)blockIdx.x >= A.nel_local) return;
@@ -475,7 +535,6 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     if (tid < LX) pf_l2(reinterpret_cast<const char *>(A.xe + nbs) + 128 * tid);
     else if (tid < LX + LM) pf_l2(reinterpret_cast<const char *>(A.xmap + nbs * NPB) + 128 * (tid - LX));
     else if (tid < LX + LM + LH) pf_l2(reinterpret_cast<const char *>(A.xhalo + nbs * HC) + 128 * (tid - LX - LM));
-    else if (tid == LX + LM + LH) pf_l2(A.piece + nbs * CF::NCHUNK * (1 + CF::MAXP));
     if (tid == 127) pf_el = __ldg(&A.xe[nbs].el);
   }
   const int clo0 = (int8_t)(hw.y & 255), clo1 = (int8_t)((hw.y >> 8) & 255), clo2 = (int8_t)((hw.y >> 16) & 255);
@@ -572,15 +631,11 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       s_bad = 0;
     }
     // the chunk's write-out pieces (setup), consumed after the staging barrier
-    const uint32_t *pcs = A.piece + (bs * CF::NCHUNK + ch) * (1 + CF::MAXP);
-    const int npc = (int)__ldg(pcs);
-    const uint32_t pc0 = tid < CF::MAXP ? __ldg(pcs + 1 + tid) : 0u;
-    const uint32_t pc1 = tid + 128 < CF::MAXP ? __ldg(pcs + 129 + tid) : 0u;
     // ---- rows of layers [z0, z1]: one thread per owned row, values from the <= 8 cells
     const int nrow = rnx * rny * (z1 - z0 + 1);
     double acc[27];
     uint32_t pw[8];
-    int px = 0;
+    int px = 0, nrw = 0;
     int64_t out = 0;
     bool hasrow = false;
     int x0 = 0, x1 = 0, x2 = 0;
@@ -595,7 +650,8 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
       px = pbase + x0 + PB * (x1 + PB * x2);
       const int64_t r = (int64_t)XG[px] - A.row_begin;
       out = __ldg(A.row_ptr + r);
-      const uint4 *pp = reinterpret_cast<const uint4 *>(A.pos + r * XPOS_W);
+      nrw = (int)(__ldg(A.row_ptr + r + 1) - out);
+      const uint4 *pp = reinterpret_cast<const uint4 *>(A.pos + r * 8);
       const uint4 pa = __ldcs(pp), pv = __ldcs(pp + 1);
       pw[0] = pa.x; pw[1] = pa.y; pw[2] = pa.z; pw[3] = pa.w;
       pw[4] = pv.x; pw[5] = pv.y; pw[6] = pv.z; pw[7] = pv.w;
@@ -629,8 +685,8 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     stage_v = CF::ONE ? XE : cm + (((z0 - 1 - clo2) % NR + NR) % NR) * LAY * CP;
     uint16_t *stage_p = reinterpret_cast<uint16_t *>(stage_v + CF::MAXROW * 27);  // ring: box point of the column
     int32_t *stage_c = reinterpret_cast<int32_t *>(stage_v + CF::MAXROW * 27);    // one chunk: the column
-    if (hasrow) {
-      const int so = (int)(pw[7] & 0xffffu);  // the row's staging offset (setup: ascending row order)
+    if (hasrow) {  // the row's values and columns in final position order at its thread's segment
+      const int so = tid * 27;
 #pragma unroll
       for (int jj = 0; jj < 27; ++jj) {
         const int ps = (int)((pw[jj >> 2] >> (8 * (jj & 3))) & 255u);
@@ -641,26 +697,22 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
           else stage_p[so + ps] = (uint16_t)pt;
         }
       }
-      m_out[tid] = out;
-      m_so[tid] = so;
     }
-    if (tid < CF::MAXP) m_pc[tid] = pc0;
-    if (tid + 128 < CF::MAXP) m_pc[tid + 128] = pc1;
+    if (tid < CF::MAXROW) {
+      m_out[tid] = hasrow ? out : -1;
+      m_n[tid] = hasrow ? nrw : 0;
+    }
     __syncthreads();
     if (ch == 0) XSTAMP(3);
-    // coalesced write-out: one warp per piece (<= 128 consecutive CSR entries of a run of
-    // consecutive rows), four entries per lane
-    for (int pc = warp; pc < npc; pc += 4) {
-      const uint32_t rec = m_pc[pc];
-      const int s0 = (int)(rec & 0xfffu), t0 = (int)((rec >> 12) & 127u), n = (int)(rec >> 19);
-      const int64_t o = m_out[t0] + (s0 - m_so[t0]);
-#pragma unroll
-      for (int u = 0; u < XPIECE_N / 32; ++u) {
-        const int k = lane + 32 * u;
-        if (k < n) {
-          __stcs(A.col + o + k, CF::ONE ? stage_c[s0 + k] : XG[stage_p[s0 + k]]);
-          __stcs(A.val + o + k, stage_v[s0 + k]);
-        }
+    // write-out: one warp per row, lane k stores entry k (consecutive rows are consecutive CSR
+    // ranges inside a coarse entity, so the sectors a row leaves partial are completed by its
+    // neighbour row while both are in L2)
+    for (int t = warp; t < nrow; t += 4) {
+      const int64_t o = m_out[t];
+      const int n = m_n[t];
+      if (o >= 0 && lane < n) {
+        if (WCOL) __stcs(A.col + o + lane, CF::ONE ? stage_c[t * 27 + lane] : XG[stage_p[t * 27 + lane]]);
+        __stcs(A.val + o + lane, stage_v[t * 27 + lane]);
       }
     }
     __syncthreads();
@@ -721,43 +773,21 @@ static cudaError_t xh1_setup_p(const XSetupArgs &a, cudaStream_t st) {
 }
 
 template <int P, int NB>
-static void geom_nb(int *kz, int *maxrow, int *maxp, int *nchunk) {
-  using CF = XCfg<P, NB>;
-  *kz = CF::KZ;
-  *maxrow = CF::MAXROW;
-  *maxp = CF::MAXP;
-  *nchunk = CF::NCHUNK;
-}
-template <int P>
-static void geom_p(const int cmax[3], int *kz, int *maxrow, int *maxp, int *nchunk) {
-  if (xfill_nb(P, cmax) == P + 1) geom_nb<P, P + 1>(kz, maxrow, maxp, nchunk);
-  else geom_nb<P, P + 2>(kz, maxrow, maxp, nchunk);
-}
-void xfill_geom(int p, const int cmax[3], int *kz, int *maxrow, int *maxp, int *nchunk) {
-  *kz = *maxrow = *maxp = *nchunk = 0;
-  switch (p) {
-    case 1: geom_p<1>(cmax, kz, maxrow, maxp, nchunk); break;
-    case 2: geom_p<2>(cmax, kz, maxrow, maxp, nchunk); break;
-    case 3: geom_p<3>(cmax, kz, maxrow, maxp, nchunk); break;
-    case 4: geom_p<4>(cmax, kz, maxrow, maxp, nchunk); break;
-    case 5: geom_p<5>(cmax, kz, maxrow, maxp, nchunk); break;
-    case 6: geom_p<6>(cmax, kz, maxrow, maxp, nchunk); break;
-    case 7: geom_p<7>(cmax, kz, maxrow, maxp, nchunk); break;
-    case 8: geom_p<8>(cmax, kz, maxrow, maxp, nchunk); break;
-    default: break;
-  }
-}
-
-template <int P, int NB>
 static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_out) {
   using CF = XCfg<P, NB>;
   constexpr int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
   constexpr int MINB = ((smem + 1024) * 5 <= 228 * 1024) ? XMINB : 3;  // 228 KB shared memory per SM
-  auto k = k_xh1_fill<P, NB, MINB>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  auto k = a.values_only ? k_xh1_fill<P, NB, MINB, false> : k_xh1_fill<P, NB, MINB, true>;
+  static bool attr = false;
+  if (!attr) {
+    for (auto kk : {k_xh1_fill<P, NB, MINB, false>, k_xh1_fill<P, NB, MINB, true>}) {
+      cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(kk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    attr = true;
+  }
   // L2 prefetch distance = resident CTAs of the grid (cached per instantiation; LOR_XPF=0: off)
   static int64_t resident = -1;
   if (resident < 0) {
@@ -844,6 +874,30 @@ cudaError_t launch_xh1_setup(int p, const XSetupArgs &a, cudaStream_t st) {
     case 6: return xh1_setup_p<6>(a, st);
     case 7: return xh1_setup_p<7>(a, st);
     case 8: return xh1_setup_p<8>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int P>
+static cudaError_t xh1_count_p(const XFillArgs &a, cudaStream_t st) {
+  if (a.nel_local <= 0) return cudaSuccess;
+  // one thread per owned row (most elements own p^3: 64 threads for p <= 4, 128 above)
+  constexpr int NT = P <= 4 ? 64 : 128;
+  if (a.ncx <= P + 1 && a.ncy <= P + 1 && a.ncz <= P + 1) k_xh1_sym<P, P + 1, NT><<<(unsigned)a.nel_local, NT, 0, st>>>(a);
+  else k_xh1_sym<P, P + 2, NT><<<(unsigned)a.nel_local, NT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xh1_count(int p, const XFillArgs &a, cudaStream_t st) {
+  switch (p) {
+    case 1: return xh1_count_p<1>(a, st);
+    case 2: return xh1_count_p<2>(a, st);
+    case 3: return xh1_count_p<3>(a, st);
+    case 4: return xh1_count_p<4>(a, st);
+    case 5: return xh1_count_p<5>(a, st);
+    case 6: return xh1_count_p<6>(a, st);
+    case 7: return xh1_count_p<7>(a, st);
+    case 8: return xh1_count_p<8>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }

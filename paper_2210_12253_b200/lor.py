@@ -57,7 +57,8 @@ def lib():
         L.lor_kernel_launches.argtypes = [C.c_void_p]
         L.lor_query.argtypes = [C.c_void_p, C.c_int] + [C.POINTER(C.c_int64)] * 4
         L.lor_query_discrete.argtypes = [C.c_void_p, C.c_int] + [C.POINTER(C.c_int64)] * 3
-        for name in ("lor_assemble_h1", "lor_assemble_nd", "lor_assemble_rt"):
+        for name in ("lor_assemble_h1", "lor_assemble_nd", "lor_assemble_rt", "lor_reassemble_h1", "lor_reassemble_nd",
+                     "lor_reassemble_rt"):
             getattr(L, name).argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int, C.POINTER(_Csr)]
         L.lor_discrete_grad.argtypes = [C.c_void_p, C.POINTER(_Csr)]
         L.lor_discrete_curl.argtypes = [C.c_void_p, C.POINTER(_Csr)]
@@ -230,6 +231,14 @@ class LOR:
         if out is None:
             out = self.alloc(q["n_local"], q["nnz"])
         fn = (lib().lor_assemble_h1, lib().lor_assemble_nd, lib().lor_assemble_rt)[sp]
+        self._check(fn(self.h, C.c_double(alpha), C.c_double(beta), QUADS.get(quad, quad), C.byref(self._csr(*out))))
+        return out
+
+    def reassemble(self, space="h1", alpha=1.0, beta=1.0, quad="vertex", out=None):
+        """Numeric-only re-assembly into ``out`` = the buffers of an earlier ``assemble`` of the same
+        space and rule (pattern reuse, lor_reassemble_*): values from the current coordinates."""
+        sp = SPACES.get(space, space)
+        fn = (lib().lor_reassemble_h1, lib().lor_reassemble_nd, lib().lor_reassemble_rt)[sp]
         self._check(fn(self.h, C.c_double(alpha), C.c_double(beta), QUADS.get(quad, quad), C.byref(self._csr(*out))))
         return out
 

@@ -135,3 +135,29 @@ def test_degenerate_cell_reported_from_any_box(torch_cuda, p, shuffle):
     with pytest.raises(LorError) as ei:
         ctx.sync()
     assert f"degenerate-geometry(element={bad}," in str(ei.value)
+
+
+@pytest.mark.parametrize("space,quad,p", [("h1", "vertex", 4), ("h1", "vertex", 7), ("h1", "gauss2", 3),
+                                          ("nd", "vertex", 3), ("rt", "vertex", 3)])
+def test_reassemble_after_mesh_motion(torch_cuda, oracle_lib, space, quad, p):
+    """lor_reassemble_* (numeric-only re-assembly with pattern reuse): full
+    assembly on mesh A, then the coordinates move to mesh B (same topology, lor_update_coordinates)
+    and only the values are recomputed into the same buffers: equal to the oracle on B, and the
+    pattern arrays are those of the full call."""
+    from paper_2210_12253_b200.lor import LOR
+    ma = mg.box_mesh(3, (3, 2, 2), p)
+    mb = mg.box_mesh(3, (3, 2, 2), p, jitter=True)
+    ctx = LOR(ma)
+    q = ctx.query(space)
+    out = ctx.assemble(space, 1.0, 1.0, quad)
+    ctx.sync()
+    rp0, col0 = to_host(out[0]).copy(), to_host(out[1]).copy()
+    import torch
+    ctx.update_coordinates(torch.from_numpy(np.ascontiguousarray(mb.X)).cuda())
+    ctx.reassemble(space, 1.3, 0.7, quad, out=out)
+    ctx.sync()
+    rp, col, val = (to_host(t) for t in out)
+    assert np.array_equal(rp, rp0) and np.array_equal(col, col0)
+    ref = oracle_lib.assemble(mb, space, quad, 1.3, 0.7)
+    compare_csr_arrays(rp, col, val, ref, 0, q["n_local"], f"reassemble {space} {quad} p={p}")
+    ctx.close()
