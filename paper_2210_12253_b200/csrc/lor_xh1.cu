@@ -704,15 +704,25 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     }
     __syncthreads();
     if (ch == 0) XSTAMP(3);
-    // write-out: one warp per row, lane k stores entry k (consecutive rows are consecutive CSR
-    // ranges inside a coarse entity, so the sectors a row leaves partial are completed by its
-    // neighbour row while both are in L2)
-    for (int t = warp; t < nrow; t += 4) {
-      const int64_t o = m_out[t];
-      const int n = m_n[t];
-      if (o >= 0 && lane < n) {
-        if (WCOL) __stcs(A.col + o + lane, CF::ONE ? stage_c[t * 27 + lane] : XG[stage_p[t * 27 + lane]]);
-        __stcs(A.val + o + lane, stage_v[t * 27 + lane]);
+    // write-out: one warp per row, lane k stores entry k, two rows in flight per warp (consecutive
+    // rows of a coarse entity are consecutive CSR ranges: the sectors a row leaves partial are
+    // completed by its neighbour while both are in L2)
+    for (int t = warp; t < nrow; t += 8) {
+      const int t2 = t + 4;
+      const int64_t o = m_out[t], o2 = t2 < nrow ? m_out[t2] : -1;
+      const int n = m_n[t], n2 = t2 < nrow ? m_n[t2] : 0;
+      const bool w1 = o >= 0 && lane < n, w2 = o2 >= 0 && lane < n2;
+      int32_t c1 = 0, c2 = 0;
+      double v1 = 0.0, v2 = 0.0;
+      if (w1) { c1 = CF::ONE ? stage_c[t * 27 + lane] : XG[stage_p[t * 27 + lane]]; v1 = stage_v[t * 27 + lane]; }
+      if (w2) { c2 = CF::ONE ? stage_c[t2 * 27 + lane] : XG[stage_p[t2 * 27 + lane]]; v2 = stage_v[t2 * 27 + lane]; }
+      if (w1) {
+        if (WCOL) __stcs(A.col + o + lane, c1);
+        __stcs(A.val + o + lane, v1);
+      }
+      if (w2) {
+        if (WCOL) __stcs(A.col + o2 + lane, c2);
+        __stcs(A.val + o2 + lane, v2);
       }
     }
     __syncthreads();
