@@ -2,24 +2,28 @@
 
     python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl reference]
 
-A "step" is one full assembly call lor_assemble_* through the C ABI: row counts, int64 scan,
-fused element assembly (sub-cell matrices + CSR column/value fill + merge of shared rows) and,
-for N > 1, the NCCL interface exchange + merge of interface rows (PAPER.md Step S1.2, A1-A3).
-Workload at N = 1: BASELINE configs[1] = C2 (3D H1 diffusion+mass, 32^3 hexes, p = 4); at N > 1
-the same per GPU (32 x 32 x 32N elements, z-slabs: weak scaling).  Inputs are resident in HBM
-when the timed region starts; L2 is flushed (512 MiB write) before every timed step.
+A "step" is one full assembly call lor_assemble_<space> through the C ABI (SURVEY P-24, PAPER.md
+l.306-374): the per-call symbolic pass (row lengths and column positions, A2), the int64 scan, the
+fused element pass (sub-cell matrices + CSR column/value fill, A1-A2; + merge of shared rows on the
+general path) and, for N > 1, the NCCL interface exchange + merge of interface rows (A3
+replacement).  Configs C4-G / C5-C time the discrete gradient / curl instead (Algorithm 1,
+l.417-445).  Workload at N = 1: BASELINE configs[1] = C2 (3D H1 diffusion+mass, 32^3 hexes,
+p = 4); at N > 1 the same per GPU (32 x 32 x 32N elements, z-slabs: weak scaling).  Inputs are
+resident in HBM when the timed region starts; L2 is flushed (512 MiB write) before every timed step.
 
-Reported: value = global rows / step time (MDOF/s, max over ranks); roofline of the dominant
-kernel (k_assemble) against MEASURED_PEAKS.json hbm_gbs; the CPU oracle on a bounded sample
-(cpu_baseline); e2e = the same call with the E-vector copied H2D from pinned host memory and
-the CSR copied back D2H inside the timed region.
+Reported beside the headline: the numeric-only re-assembly (pattern reuse, l.543-546,
+lor_reassemble_*), lor_setup time, the roofline of the dominant kernel against MEASURED_PEAKS.json,
+the CPU oracle pinned to one core (cpu_baseline), and e2e = the same call with the E-vector copied
+H2D from pinned host memory and the CSR copied back D2H inside the timed region.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -33,8 +37,15 @@ WORKLOADS = {
     "C2-J": "C2-J: C2 with jittered interior vertices (seed 12253)",
     "C3": "C3: 3D H1 diffusion+mass, 24^3 hex per GPU, p=8, Kershaw eps=0.3",
     "C4": "C4: 3D H(curl) Nedelec LOR, 32^3 hex per GPU, p=4, curl-curl+mass",
+    "C4-J": "C4-J: C4 with jittered interior vertices (seed 12253)",
     "C5": "C5: 3D H(div) Raviart-Thomas LOR, 32^3 hex per GPU, p=4, div-div+mass",
+    "C5-J": "C5-J: C5 with jittered interior vertices (seed 12253)",
+    "C4-G": "C4-G: discrete gradient (ND rows x H1 cols) on the C4 mesh, 32^3 hex per GPU, p=4",
+    "C5-C": "C5-C: discrete curl (RT rows x ND cols) on the C5 mesh, 32^3 hex per GPU, p=4",
 }
+DISCRETE = {"C4-G": ("C4", "grad"), "C5-C": ("C5", "curl")}
+# the paper's own numbers for the discrete operators (context only; 1 V100)
+PAPER_DISCRETE_GDOFS = {"grad": 12.0, "curl": 4.5}
 
 
 def peaks():
@@ -42,8 +53,8 @@ def peaks():
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -95,31 +106,77 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def algorithmic_bytes(mesh, q, dim, p, nel_local):
-    """SURVEY 8(d) d.3 adapted to this design: coordinate E-vector +
-    per-element topology records + row_ptr + col/val; the dominant kernel k_assemble reads the
-    E-vector, the topology/space records and row_ptr, and writes col/val."""
+def algorithmic_bytes(q, dim, p, nel_local, ndpe, space):
+    """B_asm = coordinate E-vector + element->dof map (int32, + int8 signs for
+    ND/RT) + row_ptr (int64) + col (int32) + val (fp64): what the method itself must move."""
     npts = (p + 1) ** dim
-    coords = 8 * dim * npts * nel_local
-    topo = (192 + 256) * nel_local
-    rowptr = 8 * (q["n_local"] + 1)
-    out = 12 * q["nnz"]
-    return dict(call=coords + topo + rowptr + out, k_assemble=coords + topo + rowptr + out)
+    return (8 * dim * npts * nel_local + (4 + (1 if space != "h1" else 0)) * ndpe * nel_local
+            + 8 * (q["n_local"] + 1) + 12 * q["nnz"])
 
 
-def cpu_baseline(cfg, space, form, sample_n):
-    """The oracle as it stands (single-threaded C, test infrastructure) on a bounded sample."""
-    from oracle import oracle as O
-    from paper_2210_12253_b200 import meshgen as mg
-    O.build()
-    m, _ = mg.config_mesh(cfg, n=sample_n)
-    t0 = time.perf_counter()
-    A = O.assemble(m, space, form["quad"], form["alpha"], form["beta"])
-    dt = time.perf_counter() - t0
-    rows = A.row_ptr.shape[0] - 1
-    return {"value": rows / dt / 1e6, "unit": "MDOF/s", "cores": 1, "kind": "oracle",
-            "sample": f"{cfg} recipe at {sample_n}^3 elements ({rows} rows, {A.nnz} nnz), full oracle assembly, "
-                      f"{dt:.2f} s"}
+def discrete_bytes(which, nel_local, ndpe, n_rows):
+    """B_G = (4 ndpe_H1 + 5 ndpe_ND) nel + 8 (n_ND + 1) + 24 n_ND (2 entries per
+    row); B_C = (5 ndpe_ND + 5 ndpe_RT) nel + 8 (n_RT + 1) + 48 n_RT (4 entries per row)."""
+    if which == "grad":
+        return (4 * ndpe[0] + 5 * ndpe[1]) * nel_local + 8 * (n_rows + 1) + 24 * n_rows
+    return (5 * ndpe[1] + 5 * ndpe[2]) * nel_local + 8 * (n_rows + 1) + 48 * n_rows
+
+
+def host_info():
+    info = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU(s)"):
+                info[k.strip()] = v.strip()
+        with open("/proc/meminfo") as f:
+            info["MemTotal"] = f.readline().split(":")[1].strip()
+    except Exception:
+        pass
+    return info
+
+
+ORACLE_SNIPPET = r"""
+import json, sys, time
+sys.path.insert(0, {root!r})
+from oracle import oracle as O
+from paper_2210_12253_b200 import meshgen as mg
+O.build()
+m, form = mg.config_mesh({cfg!r}, n={n})
+t0 = time.perf_counter()
+if {which!r}:
+    A = O.discrete(m, {which!r})
+else:
+    A = O.assemble(m, form["space"], form["quad"], form["alpha"], form["beta"])
+dt = time.perf_counter() - t0
+print(json.dumps(dict(rows=int(A.row_ptr.shape[0] - 1), nnz=int(A.nnz), seconds=dt)))
+"""
+
+
+def cpu_baseline(cfg, n):
+    """The oracle as it stands (single-threaded C, test infrastructure), pinned to core 0
+    (taskset -c 0), on the workload's recipe at n^3 elements (n = 32: the full C2/C4/C5 mesh)."""
+    base, which = DISCRETE.get(cfg, (cfg, ""))
+    code = ORACLE_SNIPPET.format(root=ROOT, cfg=base, n=n, which=which)
+    cmd = [sys.executable, "-c", code]
+    pinned = False
+    try:
+        subprocess.run(["taskset", "-c", "0", "true"], check=True, capture_output=True)
+        cmd = ["taskset", "-c", "0"] + cmd
+        pinned = True
+    except Exception:
+        pass
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        return {"value": None, "unit": "MDOF/s", "cores": 1, "kind": "oracle", "error": res.stderr[-300:]}
+    d = json.loads(res.stdout.strip().splitlines()[-1])
+    return {"value": d["rows"] / d["seconds"] / 1e6, "unit": "MDOF/s", "cores": 1, "kind": "oracle",
+            "pinned": "taskset -c 0" if pinned else "unpinned",
+            "sample": f"{base} recipe at {n}^3 elements{' (the full workload)' if n == 32 and base != 'C3' else ''}: "
+                      f"{d['rows']} rows, {d['nnz']} nnz, {'discrete ' + which if which else 'full oracle assembly'} "
+                      f"in {d['seconds']:.2f} s",
+            "host": host_info()}
 
 
 def run_reference(args):
@@ -131,11 +188,12 @@ def run_reference(args):
     from paper_2210_12253_b200 import meshgen as mg
     O.build()
     cfg = args.config
-    m, form = mg.config_mesh(cfg, n=args.ref_n)
+    base, which = DISCRETE.get(cfg, (cfg, ""))
+    m, form = mg.config_mesh(base, n=args.ref_n)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        A = O.assemble(m, form["space"], form["quad"], form["alpha"], form["beta"])
+        A = O.discrete(m, which) if which else O.assemble(m, form["space"], form["quad"], form["alpha"], form["beta"])
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -148,25 +206,55 @@ def run_reference(args):
             "config": {"workload": WORKLOADS.get(cfg, cfg), "sample_elements": f"{args.ref_n}^3", "rows": rows,
                        "nnz": int(A.nnz)},
             "cpu_baseline": {"value": v, "unit": "MDOF/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{cfg} recipe at {args.ref_n}^3 elements per step"},
+                             "sample": f"{base} recipe at {args.ref_n}^3 elements per step"},
             "e2e": {"value": v, "unit": "MDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: re-run this script under torch.distributed.run
+    with N ranks on 127.0.0.1 (one process per GPU)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def timed(stream, fn, steps, flush):
+    """device time of `steps` calls of fn (CUDA events on the library stream, L2 flushed before each)."""
+    import torch
+    out = []
+    for i in range(steps):
+        flush.fill_(float(i))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        out.append(a.elapsed_time(b))
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-n", type=int, default=20, help="elements per axis of the oracle cpu_baseline sample")
+    ap.add_argument("--no-reassembly", action="store_true")
+    ap.add_argument("--cpu-n", type=int, default=None,
+                    help="elements per axis of the oracle cpu_baseline run (default: the full mesh, 32; C3: 12)")
     ap.add_argument("--ref-n", type=int, default=12, help="elements per axis per reference-arm step")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
 
     import torch
     import torch.distributed as dist
@@ -184,20 +272,41 @@ def main():
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
 
-    mesh, form = mg.config_mesh(args.config, gpus=world)
+    cfg = args.config.upper()
+    base, which = DISCRETE.get(cfg, (cfg, ""))
+    mesh, form = mg.config_mesh(base, gpus=world)
     nid = None
     if world > 1:
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     ctx = LOR(mesh, rank=rank, nranks=world, nccl_id=nid, device=local_rank, stream=stream)
+    torch.cuda.synchronize()
+    setup_ms = (time.perf_counter() - t0) * 1e3
     space = form["space"]
-    q = ctx.query(space)
-    out = ctx.alloc(q["n_local"], q["nnz"])
+    nel_local = ctx.n_elem_local
+    ndpe = (ctx.ndpe[0], ctx.ndpe[1], ctx.ndpe[2])
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    if which:
+        q = ctx.query_discrete(which)
+        ng = q["n_local"]
+        if world > 1:
+            tt = torch.tensor([ng], dtype=torch.int64, device=dev)
+            dist.all_reduce(tt)
+            ng = int(tt[0])
+        q = dict(n_local=q["n_local"], nnz=q["nnz"], n_global=ng)
+        out = ctx.alloc(q["n_local"], q["nnz"])
 
-    def step():
-        ctx.assemble(space, form["alpha"], form["beta"], form["quad"], out=out)
+        def step():
+            ctx.discrete(which, out=out)
+    else:
+        q = ctx.query(space)
+        out = ctx.alloc(q["n_local"], q["nnz"])
+
+        def step():
+            ctx.assemble(space, form["alpha"], form["beta"], form["quad"], out=out)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -205,45 +314,65 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     phases = []
     l0 = ctx.launches()
     with ClockSampler(dev.index) as clk:
+        step_ms = []
         for i in range(args.steps):
-            flush.fill_(float(i))  # L2 flush outside the timed step
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-            ev[i][1].synchronize()
+            step_ms += timed(stream, step, 1, flush)
             phases.append(ctx.phase_ms())
     ctx.sync()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches = ctx.launches() - l0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
     t_ms = statistics.mean(step_ms)
-    # the fill step: element pass k_assemble + merge pass k_merge_rows
-    asm_ms = statistics.mean(p[1] + (p[2] if len(p) > 3 else 0.0) for p in phases)
+    if which:
+        fill_ms = t_ms  # the discrete call: row_ptr stride kernel + k_discrete
+        kernel = f"discrete {which} (k_discrete, a{8 if which == 'grad' else 9})"
+        B = discrete_bytes(which, nel_local, ndpe, q["n_local"])
+    else:
+        # phases: [symbolic + scan, element pass / fill, merge pass, exchange + finalize]
+        fill_ms = statistics.mean(p[1] + (p[2] if len(p) > 3 else 0.0) for p in phases)
+        kernel = ("fill step a6 = k_xh1_fill" if ctx.fill_path(space) == 1 else
+                  "fill step a6 = k_assemble + k_merge_rows")
+        B = algorithmic_bytes(q, mesh.dim, mesh.p, nel_local, ndpe[{"h1": 0, "nd": 1, "rt": 2}[space]], space)
     if world > 1:
-        tt = torch.tensor([t_ms, asm_ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_ms, fill_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms, asm_ms = float(tt[0]), float(tt[1])
+        t_ms, fill_ms = float(tt[0]), float(tt[1])
     value = q["n_global"] / (t_ms * 1e-3) / 1e6
-    nel_local = ctx.n_elem_local
-    B = algorithmic_bytes(mesh, q, mesh.dim, mesh.p, nel_local)
     peak, peak_kind = peaks()
-    achieved = B["k_assemble"] / (asm_ms * 1e-3) / 1e9
+    achieved = B / (fill_ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(args.config, {}).get("fill_dram_bytes")
+                traffic = json.load(f).get(cfg, {}).get("fill_dram_bytes")
         except Exception:
             traffic = None
 
-    # ---- e2e: pinned host E-vector H2D + assembly + CSR D2H, same public API ------------------
+    # ---- numeric-only re-assembly (pattern reuse), same buffers ---------------------------------
+    reasm = None
+    if not which and not args.no_reassembly:
+        def restep():
+            ctx.reassemble(space, form["alpha"], form["beta"], form["quad"], out=out)
+        for _ in range(3):
+            restep()
+        ctx.sync()
+        rt = statistics.mean(timed(stream, restep, args.steps, flush))
+        rphase = ctx.phase_ms()
+        if world > 1:
+            tt = torch.tensor([rt], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            rt = float(tt[0])
+        reasm = {"value": q["n_global"] / (rt * 1e-3) / 1e6, "unit": "MDOF/s", "ms_per_step": rt,
+                 "what": "lor_reassemble_* (PAPER.md l.543-546): values only into the pattern of the last full call; "
+                         "no symbolic pass, no scan" + ("; col not rewritten" if ctx.fill_path(space) == 1 else ""),
+                 "phases_ms": rphase}
+
+    # ---- e2e: pinned host E-vector H2D + the same call + CSR D2H, same public API ---------------
     e2e = None
     if not args.no_e2e:
         e0, e1 = ctx.elem_begin, ctx.elem_begin + nel_local
@@ -251,22 +380,15 @@ def main():
         hrp = torch.empty(q["n_local"] + 1, dtype=torch.int64).pin_memory()
         hcol = torch.empty(max(q["nnz"], 1), dtype=torch.int32).pin_memory()
         hval = torch.empty(max(q["nnz"], 1), dtype=torch.float64).pin_memory()
-        ne = max(3, min(args.steps, 10))
-        times = []
-        for i in range(ne + 2):
-            flush.fill_(float(i))
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+
+        def e2e_step():
             ctx.update_coordinates(Xh)
             step()
             hrp.copy_(out[0], non_blocking=True)
             hcol.copy_(out[1], non_blocking=True)
             hval.copy_(out[2], non_blocking=True)
-            b.record(stream)
-            b.synchronize()
-            if i >= 2:
-                times.append(a.elapsed_time(b))
-        te = statistics.mean(times)
+        timed(stream, e2e_step, 2, flush)
+        te = statistics.mean(timed(stream, e2e_step, max(3, min(args.steps, 10)), flush))
         if world > 1:
             tt = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -278,24 +400,32 @@ def main():
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(args.config, space, form, args.cpu_n)
+            cpu = cpu_baseline(cfg, args.cpu_n or (12 if base.startswith("C3") else 32))
         ph = [statistics.mean(p[i] for p in phases) for i in range(len(phases[0]))] if phases and phases[0] else []
         line = {
             "metric": METRIC, "value": value, "unit": "MDOF/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS.get(args.config, args.config), "rows_global": q["n_global"],
-                       "nnz_per_gpu": q["nnz"], "elements_per_gpu": nel_local, "p": mesh.p, "space": space,
-                       "l2": "flushed (512 MiB write) before every timed step",
-                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
-            "hbm_gbs": B["call"] / (t_ms * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": ("fill step a6 = k_xh1_fill" if ctx.fill_path(space) == 1 else
-                                                    "fill step a6 = k_assemble + k_merge_rows"), "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": traffic, "algorithmic_bytes_per_launch": B["k_assemble"], "avg_launch_ms": asm_ms},
-            "phases_ms": dict(zip(["count+scan", "k_assemble", "k_merge_rows", "exchange+finalize"], ph)),
+            "config": {"workload": WORKLOADS.get(cfg, cfg), "rows_global": q["n_global"],
+                       "nnz_per_gpu": q["nnz"], "elements_per_gpu": nel_local, "p": mesh.p,
+                       "space": which or space, "l2": "flushed (512 MiB write) before every timed step",
+                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "step": ("lor_discrete_" + which) if which else
+                               "lor_assemble_" + space + ": symbolic pass + scan + fill (full call, SURVEY P-24)"},
+            "hbm_gbs": B / (t_ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": B, "avg_launch_ms": fill_ms,
+                         "bytes_model": "SURVEY 8(d) d.3 (" + ("B_G" if which == "grad" else "B_C" if which else "B_asm") + ")"},
+            "phases_ms": ({} if which else dict(zip(["symbolic+scan", "fill (element pass)", "merge pass",
+                                                     "exchange+finalize"], ph))),
+            "setup_ms": setup_ms,
+            "reassembly": reasm,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
         }
+        if which:
+            line["paper_context"] = {"value": PAPER_DISCRETE_GDOFS[which] * 1e3, "unit": "MDOF/s",
+                                     "hardware": "1x V100 (PAPER.md l.663-664)", "note": "context only"}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
