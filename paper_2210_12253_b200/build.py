@@ -103,11 +103,13 @@ def build(force: bool = False, verbose: bool = True) -> str:
             (os.path.join(CSRC, "lor_capi.cu"), os.path.join(BUILD, "lor_capi.o")),
             (os.path.join(CSRC, "lor_plan.cpp"), os.path.join(BUILD, "lor_plan.o")),
             (os.path.join(CSRC, "lor_xframe.cpp"), os.path.join(BUILD, "lor_xframe.o")),
-            (os.path.join(CSRC, "lor_xh1.cu"), os.path.join(BUILD, "lor_xh1.o"))]
+            (os.path.join(CSRC, "lor_xh1.cu"), os.path.join(BUILD, "lor_xh1.o")),
+            (os.path.join(CSRC, "lor_xv_nd.cu"), os.path.join(BUILD, "lor_xv_nd.o")),
+            (os.path.join(CSRC, "lor_xv_rt.cu"), os.path.join(BUILD, "lor_xv_rt.o"))]
     jobs += [(u, u[:-3] + ".o") for u in units]
     # largest first (ND / high p) for better packing
-    jobs.sort(key=lambda j: (("_3_1_" in j[0]) * 10 + ("_3_0_" in j[0]) * 5 + int(j[0][-4]) if "asm_" in j[0] else 100),
-              reverse=True)
+    jobs.sort(key=lambda j: (("_3_1_" in j[0]) * 10 + ("_3_0_" in j[0]) * 5 + int(j[0][-4]) if "asm_" in j[0]
+                             else (200 if "lor_xv" in j[0] else 100)), reverse=True)
     nw = max(1, min(len(jobs), os.cpu_count() or 4))
     if verbose:
         print(f"[lor build] {len(jobs)} translation units on {nw} workers (p in {plist})", flush=True)

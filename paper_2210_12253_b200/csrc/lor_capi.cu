@@ -103,6 +103,10 @@ struct SpaceDev {
   int8_t *esgn = nullptr;
   int xc[3] = {0, 0, 0};
   uint32_t *xpos = nullptr;     // extended-frame path: per-call slot positions [n_local][8]
+  // extended-frame path of ND / RT (lor_xv.cuh): restriction of the box dofs, per-call positions
+  bool xvok = false;
+  uint32_t *xvmap = nullptr;
+  uint32_t *xvpos = nullptr;
   int64_t n_tr = 0;             // entries of the dof transpose (local elements x owned local dofs)
   int32_t *trmap = nullptr;     // element restriction workspace of lor_dof_transpose (nranks > 1)
 };
@@ -273,6 +277,31 @@ XFillArgs xfill_args(lor_ctx c, const SpaceDev &S) {
   return x;
 }
 
+XvArgs xv_args(lor_ctx c, int s) {
+  const SpaceDev &H = c->sp[SP_H1];
+  const SpaceDev &S = c->sp[s];
+  XvArgs x{};
+  x.nel_local = c->nel_local;
+  x.elem_begin = c->elem_begin;
+  x.xe = H.xe;
+  x.xhalo = H.xhalo;
+  x.topo = c->topo;
+  fill_base(S, x.base);
+  x.xvmap = S.xvmap;
+  x.X = c->X;
+  x.xstride = c->xstride;
+  x.row_begin = S.row_begin;
+  x.cnt = S.cnt;
+  x.pos = S.xvpos;
+  x.ncx = H.xc[0];
+  x.ncy = H.xc[1];
+  x.ncz = H.xc[2];
+  x.err = c->err;
+  const int sb = s == SP_ND ? 6 : 4;  // slot bits of the packed sort keys
+  x.sort32 = (S.n_global < (int64_t(1) << (31 - sb)) && !(c->dbg & 1)) ? 1 : 0;
+  return x;
+}
+
 // reuse = true: numeric-only re-assembly into buffers holding the pattern of an earlier full call of
 // the same space (NEXT-3): no row lengths, no scan; the extended-frame path
 // stores values only.
@@ -288,6 +317,28 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   c->nphase = 0;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   lor_status st = LOR_OK;
+  if (S.xvok && quad == LOR_QUAD_VERTEX) {  // ND / RT extended-frame path: every owned row in one pass
+    XvArgs x = xv_args(c, s);
+    if (!reuse) {
+      CUDA_TRY(c, launch_xv_sym(s, c->p, x, c->stream));
+      if (c->nel_local > 0) c->launches++;
+      CUDA_TRY(c, launch_scan(S.cnt, out->row_ptr, S.n_local, S.scan_status, S.tile_ctr, c->stream));
+      c->launches++;
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    x.row_ptr = out->row_ptr;
+    x.col = out->col;
+    x.val = out->val;
+    x.alpha = alpha;
+    x.beta = beta;
+    x.values_only = reuse ? 1 : 0;
+    CUDA_TRY(c, launch_xv_fill(s, c->p, x, c->stream));
+    if (c->nel_local > 0) c->launches++;
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    return LOR_OK;
+  }
   const bool xpath = S.xok && quad == LOR_QUAD_VERTEX;
   if (!reuse) {  // symbolic part (A2): row lengths per call, then the int64 scan
     if (xpath) {
@@ -826,6 +877,38 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
         S.xok = h0 == h1;
       }
       if (!S.xok) fprintf(stderr, "lor_setup: extended-frame tables inconsistent, using the element + merge passes\n");
+      // ND / RT on the same frame: restriction of the box dofs, checked like H1 (row lengths of the
+      // per-call symbolic pass == those of the general minimal-element count)
+      for (int sv = SP_ND; S.xok && sv <= SP_RT; ++sv) {
+        SpaceDev &V = c->sp[sv];
+        // ND stays on the element + merge passes unless LOR_XV_ND=1 (its extended-frame fill is
+        // still slower: DESIGN.md section 4); LOR_XV=0 turns the vector-space path off
+        const char *xv_env = getenv("LOR_XV"), *xvnd_env = getenv("LOR_XV_ND");
+        if (!V.valid || (xv_env && !atoi(xv_env)) || (sv == SP_ND && !(xvnd_env && atoi(xvnd_env))) ||
+            !xv_supported(sv, A.p, S.xc))
+          continue;
+        if (dev_alloc(c, &V.xvmap, (size_t)c->nel_local * xv_map_words(sv, A.p, S.xc)) != cudaSuccess ||
+            dev_alloc(c, &V.xvpos, (size_t)std::max<int64_t>(V.n_local, 1) * xv_pos_words(sv)) != cudaSuccess)
+          return bail(LOR_ERR_OUT_OF_MEMORY, "xframe (vector spaces)");
+        XvArgs x = xv_args(c, sv);
+        int32_t *vc = nullptr;
+        if (cudaMalloc((void **)&vc, sizeof(int32_t) * std::max<int64_t>(V.n_local, 1)) != cudaSuccess)
+          return bail(LOR_ERR_OUT_OF_MEMORY, "xframe check");
+        cudaMemset(vc, 0, sizeof(int32_t) * std::max<int64_t>(V.n_local, 1));
+        x.cnt = vc;
+        std::vector<int32_t> h0((size_t)V.n_local), h1((size_t)V.n_local);
+        int herr2[4] = {0, 0, 0, 0};
+        bool ok = cudaMemset(c->err, 0, 4 * sizeof(int)) == cudaSuccess && launch_xv_setup(sv, A.p, x, c->stream) == cudaSuccess &&
+                  launch_xv_sym(sv, A.p, x, c->stream) == cudaSuccess && cudaStreamSynchronize(c->stream) == cudaSuccess &&
+                  cudaMemcpy(herr2, c->err, sizeof(herr2), cudaMemcpyDeviceToHost) == cudaSuccess &&
+                  cudaMemcpy(h0.data(), V.cnt, sizeof(int32_t) * V.n_local, cudaMemcpyDeviceToHost) == cudaSuccess &&
+                  cudaMemcpy(h1.data(), vc, sizeof(int32_t) * V.n_local, cudaMemcpyDeviceToHost) == cudaSuccess;
+        cudaFree(vc);
+        cudaMemset(c->err, 0, 4 * sizeof(int));
+        if (!ok) return bail(LOR_ERR_CUDA, "xframe setup (vector spaces)");
+        V.xvok = herr2[0] == 0 && h0 == h1;
+        if (!V.xvok) fprintf(stderr, "lor_setup: extended-frame tables of space %d inconsistent, using the element + merge passes\n", sv);
+      }
     } else if (getenv("LOR_XFRAME_VERBOSE")) {
       fprintf(stderr, "lor_setup: extended-frame path off: %s\n", why.c_str());
     }
@@ -1080,7 +1163,7 @@ int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int
 
 int lor_fill_path(lor_ctx c, lor_space space) {
   if (!c || space < 0 || space > 2 || !c->sp[space].valid) return -1;
-  return c->sp[space].xok ? 1 : 0;
+  return (c->sp[space].xok || c->sp[space].xvok) ? 1 : 0;
 }
 
 int lor_last_phase_ms(lor_ctx c, float *ms, int cap) {

@@ -173,12 +173,11 @@ bool xframe_build(const HostPlan &plan, const int64_t *EV, std::vector<XElem> &o
     XElem &X = out[(size_t)le];
     memset(&X, 0, sizeof(X));
     const ElemTopo &T = plan.topo[(size_t)le];
-    for (int tau = 0; tau < 27; ++tau) {
-      const int c[3] = {tau % 3, (tau / 3) % 3, tau / 9};
-      bool rows = true;  // H1 rows on this slot exist (interior classes need p >= 2)
-      for (int a = 0; a < 3; ++a) rows = rows && (c[a] != 1 || p >= 2);
-      if (rows && (T.flags[tau] & TF_MIN) && (T.flags[tau] & TF_OWNED)) X.own |= 1u << tau;
-    }
+    // every coarse entity this element owns (minimal element, this rank), whether or not the space
+    // has dofs on it (H1 has none on edges / faces / interiors at p = 1; ND / RT do): the cell box
+    // must hold the cells around the rows of every space (lor_xv.cuh shares it)
+    for (int tau = 0; tau < 27; ++tau)
+      if ((T.flags[tau] & TF_MIN) && (T.flags[tau] & TF_OWNED)) X.own |= 1u << tau;
     for (int a = 0; a < 3; ++a) {
       bool lo = false, hi = false;
       for (int tau = 0; tau < 27; ++tau) {

@@ -94,6 +94,41 @@ struct XFillArgs {
   uint8_t cinv[128];           // box cell -> thread (storage slot)
 };
 
+// ---- extended frame of the vector spaces (lor_xv.cu): Nedelec (SP_ND) and Raviart-Thomas (SP_RT).
+// Family s: ND = edges along s (cell index along s, lattice point index along the other axes),
+// RT = faces normal to s (point index along s, cell indices along the others).  Box positions of a
+// family: per axis the cell range [clo, clo + nb - 1] (cell-index axes) or the point range
+// [clo, clo + nb] (point-index axes), lexicographic.  Map entry: global id | 0x80000000 when the
+// dof's global orientation is opposite to the extended frame's +axis orientation (sign -1);
+// 0xffffffff = no dof there.
+struct XvArgs {
+  int64_t nel_local, elem_begin;
+  const XElem *xe;             // shared with the H1 path (processing order)
+  const int2 *xhalo;           // coordinate gather list (shared with the H1 path)
+  const ElemTopo *topo;
+  const int32_t *base[4];      // entity first-dof ids of this space
+  uint32_t *xvmap;             // [nel_local][3][nvf] (setup)
+  const double *X;
+  int64_t xstride;
+  int64_t row_begin;
+  int32_t *cnt;                // symbolic pass: row lengths [n_local]
+  uint32_t *pos;               // symbolic pass: [n_local][pw] final position of each stencil slot (bytes, 255 = none)
+  const int64_t *row_ptr;
+  int32_t *col;
+  double *val;
+  double alpha, beta;
+  int ncx, ncy, ncz;
+  int *err;
+  int values_only;
+  int sort32;                  // ids < 2^(31 - slot bits): sorting network on packed keys
+};
+cudaError_t launch_xv_setup(int space, int p, const XvArgs &a, cudaStream_t st);
+cudaError_t launch_xv_sym(int space, int p, const XvArgs &a, cudaStream_t st);
+cudaError_t launch_xv_fill(int space, int p, const XvArgs &a, cudaStream_t st);
+int xv_supported(int space, int p, const int cmax[3]);   // 1: a fill kernel is instantiated (smem fits)
+int64_t xv_map_words(int space, int p, const int cmax[3]);  // per element
+int xv_pos_words(int space);                              // per row
+
 // host: regular-neighbourhood check and per-element extended-frame records (nranks == 1)
 struct HostPlan;
 bool xframe_build(const HostPlan &plan, const int64_t *elem_vert, std::vector<XElem> &out, int cmax[3],

@@ -19,6 +19,7 @@
 #include <utility>
 
 #include "lor_device.cuh"
+#include "lor_xdev.cuh"
 #include "lor_xframe.h"
 
 #ifndef XMINB
@@ -27,31 +28,9 @@
 
 namespace lorb {
 
+using namespace xdev;
+
 namespace {
-
-__device__ __forceinline__ int ycls(int y, int p) { return y < 0 ? 0 : (y == 0 ? 1 : (y < p ? 2 : (y == p ? 3 : 4))); }
-__device__ __forceinline__ int ydelta(int y, int p) { return y < 0 ? -1 : (y > p ? 1 : 0); }
-__device__ __forceinline__ int lcls(int l, int p) { return l == 0 ? 0 : (l == p ? 2 : 1); }
-
-// neighbour-local lattice coordinates of extended-frame point y (lor_xframe.h XNbr::code)
-__device__ __forceinline__ void x_to_local(int p, uint32_t code, const int y[3], int L[3]) {
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const int k = (code >> (2 * a)) & 3;
-    const int ok = (int)((code >> (9 + 2 * k)) & 3) - 1;
-    const int v = y[k] - p * ok;
-    L[a] = ((code >> (6 + a)) & 1) ? -v : v;
-  }
-}
-
-__device__ __forceinline__ void pf_l2(const void *a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
-
-__device__ __forceinline__ void xreport(int *err, int code, int64_t e, int cell) {
-  if (atomicCAS(err, 0, code) == 0) {
-    err[1] = (int)e;
-    err[2] = cell;
-  }
-}
 
 __device__ __forceinline__ void cross3x(const double *a, const double *b, double *c) {
   c[0] = a[1] * b[2] - a[2] * b[1];
@@ -220,47 +199,6 @@ __global__ void __launch_bounds__(128) k_xh1_setup(XSetupArgs A) {
   }
 }
 
-// The 351 pairs (j, k), j < k, of the 27 stencil slots as compile-time indices (a nested unrolled
-// loop is not unrolled by nvcc at this size, which would put key[] in local memory): pair t
-// compares key_k < key_j and moves one count of the rank bytes from k to j (branch-free).
-__host__ __device__ constexpr int pair_j(int t) {
-  int j = 0;
-  while (t >= 26 - j) { t -= 26 - j; ++j; }
-  return j;
-}
-__host__ __device__ constexpr int pair_k(int t) {
-  int j = 0;
-  while (t >= 26 - j) { t -= 26 - j; ++j; }
-  return j + 1 + t;
-}
-template <int T>
-__device__ __forceinline__ void rank_pair(const int (&key)[27], uint32_t (&pw)[7]) {
-  constexpr int j = pair_j(T), k = pair_k(T);
-  const uint32_t lt = (uint32_t)(key[k] < key[j]);
-  pw[j >> 2] += lt << (8 * (j & 3));
-  pw[k >> 2] -= lt << (8 * (k & 3));
-}
-template <int... T>
-__device__ __forceinline__ void rank_pairs(const int (&key)[27], uint32_t (&pw)[7], std::integer_sequence<int, T...>) {
-  (rank_pair<T>(key, pw), ...);
-}
-
-// Batcher odd-even merge sort network for 32 wires pruned to 27 live inputs (scripts/gen_sort27.py:
-// wires 27..31 hold +inf, comparators onto them dropped; checked there by exhaustive random tests):
-// comparator c = 32 a + b puts min on wire a, max on wire b.
-constexpr uint16_t kNet27[156] = {1, 67, 133, 199, 265, 331, 397, 463, 529, 595, 661, 727, 793, 2, 35, 134, 167, 266, 299, 398, 431, 530, 563, 662, 695, 794, 34, 166, 298, 430, 562, 694, 826, 4, 37, 70, 103, 268, 301, 334, 367, 532, 565, 598, 631, 68, 101, 332, 365, 596, 629, 34, 100, 166, 298, 364, 430, 562, 628, 694, 826, 8, 41, 74, 107, 140, 173, 206, 239, 536, 569, 602, 136, 169, 202, 235, 664, 697, 730, 68, 101, 200, 233, 332, 365, 596, 629, 728, 761, 34, 100, 166, 232, 298, 364, 430, 562, 628, 694, 760, 826, 16, 49, 82, 115, 148, 181, 214, 247, 280, 313, 346, 272, 305, 338, 371, 404, 437, 470, 503, 136, 169, 202, 235, 400, 433, 466, 499, 664, 697, 730, 68, 101, 200, 233, 332, 365, 464, 497, 596, 629, 728, 761, 34, 100, 166, 232, 298, 364, 430, 496, 562, 628, 694, 760, 826};
-template <int C>
-__device__ __forceinline__ void net_cmp(int (&v)[27]) {
-  constexpr int a = kNet27[C] >> 5, b = kNet27[C] & 31;
-  const int lo = min(v[a], v[b]), hi = max(v[a], v[b]);
-  v[a] = lo;
-  v[b] = hi;
-}
-template <int... C>
-__device__ __forceinline__ void sort27(int (&v)[27], std::integer_sequence<int, C...>) {
-  (net_cmp<C>(v), ...);
-}
-
 // Symbolic pass of the extended-frame path, per call (A2: the row lengths the
 // scan turns into I, and where every column goes in its row).  For every owned row of the element
 // (the minimal element containing its coarse entity):
@@ -299,36 +237,7 @@ __global__ void __launch_bounds__(NT) k_xh1_sym(XFillArgs A) {
       const bool v = (m[0] >> dx) & (m[1] >> dy) & (m[2] >> dz) & 1;
       key[j] = v ? XG[px + (dx - 1) + PB * (dy - 1) + PB * PB * (dz - 1)] : 0x7fffffff;
     }
-    if (A.sort32) {
-      // sort the keys (id << 5 | slot); position i goes to the slot in the key's low bits (absent
-      // slots sort last: 0x7fffffe0 | slot)
-      int v[27];
-#pragma unroll
-      for (int j = 0; j < 27; ++j) v[j] = key[j] == 0x7fffffff ? (0x7fffffe0 | j) : ((key[j] << 5) | j);
-      sort27(v, std::make_integer_sequence<int, 156>{});
-      uint8_t *sp = s_pos + tid * 28;
-#pragma unroll
-      for (int q2 = 0; q2 < 7; ++q2) reinterpret_cast<uint32_t *>(sp)[q2] = 0xffffffffu;
-#pragma unroll
-      for (int i = 0; i < 27; ++i)
-        if (v[i] < 0x7fffffe0) sp[v[i] & 31] = (uint8_t)i;
-#pragma unroll
-      for (int q2 = 0; q2 < 7; ++q2) pw[q2] = reinterpret_cast<const uint32_t *>(sp)[q2];
-    } else {
-      // ranks as bytes: byte k starts at k (every j < k counted as smaller) and each pair (j, k)
-      // moves one count from k to j when key_k < key_j; absent slots carry the largest key
-#pragma unroll
-      for (int q2 = 0; q2 < 7; ++q2) {
-        uint32_t w = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (4 * q2 + b < 27) w |= (uint32_t)(4 * q2 + b) << (8 * b);
-        pw[q2] = w;
-      }
-      rank_pairs(key, pw, std::make_integer_sequence<int, 351>{});
-#pragma unroll
-      for (int j = 0; j < 27; ++j) pw[j >> 2] |= (key[j] == 0x7fffffff ? 0xffu : 0u) << (8 * (j & 3));
-    }
+    xdev::row_positions<27>(key, A.sort32 != 0, s_pos + tid * 28, pw);
   };
   auto masks = [&](const int x[3], int m[3]) {
 #pragma unroll
@@ -392,30 +301,6 @@ __host__ __device__ constexpr int cidx(int a, int b) {
   return t - (t > 7) - (t > 13) - (t > 18) - (t > 22);
 }
 __host__ __device__ constexpr bool body_diag(int a, int b) { return (a ^ b) == 7; }
-
-// 1/x for x > 0: float seed + two Newton steps (relative error ~1e-28 before rounding).  The seed
-// needs x inside the normal float range: outside [2^-120, 2^120] (cell volumes of meshes scaled far
-// from unit size, e.g. coordinates x 1e-14) x = m 2^e is reduced to m in [0.5, 1) first and the
-// result scaled back by 2^-e (inline, no division slow path), so the result never depends on the
-// float range (tests/test_gpu_boundary.py scaled meshes).
-__device__ __forceinline__ double rcp_newton(double x) {
-  float rf;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rf) : "f"((float)x));
-  double r = (double)rf;
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-__device__ __forceinline__ double rcp_pos(double x) {
-  if (__builtin_expect(x > 7.52316384526264e-37 && x < 1.329227995784916e36, 1)) return rcp_newton(x);
-  const int hi = __double2hiint(x), ex = ((hi >> 20) & 0x7ff) - 1022;  // x = m 2^ex, m in [0.5, 1)
-  const double m = __hiloint2double((hi & 0x800fffff) | (1022 << 20), __double2loint(x));
-  const double r = rcp_newton(m);
-  // 2^-ex in two factors (each a normal double for |ex| <= 1022)
-  const int e1 = -ex / 2, e2 = -ex - e1;
-  return r * __hiloint2double((e1 + 1023) << 20, 0) * __hiloint2double((e2 + 1023) << 20, 0);
-}
 
 // One LOR cell under the vertex rule (reading P-1), computed by one thread with the corner loop
 // unrolled: at corner q the Jacobian columns are the cell edge vectors through q, Q = w a

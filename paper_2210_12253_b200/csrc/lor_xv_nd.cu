@@ -1,0 +1,10 @@
+// lor_xv_nd.cu -- Nedelec instantiations of the extended-frame vector-space kernels (lor_xv.cuh).
+#include "lor_xv.cuh"
+
+namespace lorb {
+
+cudaError_t xv_run_nd(int what, int p, const XvArgs &a, cudaStream_t st) { return run_sp<SP_ND>(what, p, a, st); }
+int xv_supported_nd(int p, const int cmax[3]) { return p >= 1 && p <= 8 ? supported_sp<SP_ND>(p, cmax) : 0; }
+int64_t xv_words_nd(int p, const int cmax[3]) { return p >= 1 && p <= 8 ? words_sp<SP_ND>(p, cmax) : 0; }
+
+}  // namespace lorb
