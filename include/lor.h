@@ -155,7 +155,10 @@ lor_status lor_query_elements(lor_ctx ctx, int64_t *elem_begin, int64_t *n_elem_
 
 /* Replace this rank's coordinate E-vector (mesh motion / per-step inputs):
  * elem_nodes = [n_elem_local][dim][(p+1)^dim] for elements elem_rank_begin[rank] .. +n_elem_local,
- * HOST (pinned for asynchrony) or DEVICE memory; enqueued on the context stream. */
+ * HOST (pinned for asynchrony) or DEVICE memory; enqueued on the context stream.  With nranks > 1
+ * and an NCCL communicator the extended frame's ghost layer (neighbour elements of other ranks)
+ * is then refreshed from the peers (grouped ncclSend/ncclRecv on the same stream; every rank must
+ * call it).  In LOR_EXCHANGE_MANUAL mode the ghost layer keeps the coordinates given at setup. */
 lor_status lor_update_coordinates(lor_ctx ctx, const double *elem_nodes);
 
 /* Exchange mode for nranks > 1 (A3 replacement).  LOR_EXCHANGE_NCCL (0, default when
@@ -174,6 +177,14 @@ lor_status lor_assemble_finish(lor_ctx ctx, lor_space space, lor_csr *out);
  * send_counts / recv_counts [3][nranks] = partial-row records exchanged with each peer (NULL ok).
  * Used by the multi-rank CPU tests (gloo) to check that the ranks' plans agree. */
 lor_status lor_plan_dry_run(const lor_setup_args *args, int64_t *info, int64_t *send_counts, int64_t *recv_counts);
+
+/* Host-only dry run of the extended frame for one rank (no GPU; dim == 3): info[0] = 1 if every
+ * local element has a regular 3x3x3 neighbourhood (the single-pass path applies), info[1] = ghost
+ * layer size (non-local elements sharing a vertex with a local one; their coordinates are held
+ * after the local ones), info[2] = largest cell-box extent, info[3] = local elements;
+ * send_counts / recv_counts[nranks] = elements whose coordinates this rank sends to / receives
+ * from each peer when the coordinates change (lor_update_coordinates, NCCL).  NULL allowed. */
+lor_status lor_xframe_dry_run(const lor_setup_args *args, int64_t *info, int64_t *send_counts, int64_t *recv_counts);
 
 /* Diagnostics: copy internal setup tables of `space` to host memory (what = 0: row-class slot
  * table uint32[S][729][W]; 1: block-size table uint8[S][729][3*27 or 27]; 2: per-CTA phase clocks

@@ -120,8 +120,15 @@ struct lor_ctx_s {
   ElemTopo *topo = nullptr;
   int32_t *order = nullptr;  // CTA -> local element, Morton order of element centroids
   std::vector<int32_t> order_host;  // host copy (empty: natural order)
-  double *X = nullptr;
+  double *X = nullptr;           // local elements, then the extended frame's ghost layer (nranks > 1)
   int64_t xstride = 0;
+  // extended frame on several ranks: ghost layer (non-local elements sharing a vertex with a local
+  // one), their topology records after the local ones, and the per-peer coordinate exchange lists
+  int64_t n_xghost = 0;
+  ElemTopo *xtopo = nullptr;
+  std::vector<int64_t> xg_send_count, xg_recv_begin, xg_recv_count;  // per peer (elements)
+  int32_t *xg_send_idx = nullptr;  // local element of every sent E-vector (peer-major)
+  double *xg_send_buf = nullptr;
   SpaceDev sp[3];
   int *err = nullptr;
   unsigned long long *tstamp = nullptr;  // per-CTA phase clocks of the last element pass (debug)
@@ -285,7 +292,7 @@ XvArgs xv_args(lor_ctx c, int s) {
   x.elem_begin = c->elem_begin;
   x.xe = H.xe;
   x.xhalo = H.xhalo;
-  x.topo = c->topo;
+  x.topo = c->xtopo ? c->xtopo : c->topo;
   fill_base(S, x.base);
   x.xvmap = S.xvmap;
   x.X = c->X;
@@ -434,6 +441,95 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   return LOR_OK;
 }
 
+// Extended frame on several ranks: the ghost layer's topology records and
+// coordinates after the local ones (coordinates from the caller's global E-vector, or interpolated
+// from the vertices), and the per-peer lists that refresh the ghost coordinates over NCCL when the
+// coordinates change (lor_update_coordinates).  Returns false with a reason if it cannot be built.
+bool xframe_ghost_layer(lor_ctx c, const HostPlan &plan, const lor_setup_args &A, const std::vector<int64_t> &xg,
+                        std::string &why) {
+  const int64_t ng = (int64_t)xg.size();
+  c->n_xghost = ng;
+  if (ng == 0) return true;
+  const int np = (A.dim == 3) ? (A.p + 1) * (A.p + 1) * (A.p + 1) : (A.p + 1) * (A.p + 1);
+  const int64_t raw = (int64_t)A.dim * np;
+  // topology records: local, then ghosts
+  std::vector<ElemTopo> xt((size_t)(c->nel_local + ng));
+  for (int64_t i = 0; i < c->nel_local; ++i) xt[(size_t)i] = plan.topo[(size_t)i];
+  for (int64_t g = 0; g < ng; ++g) xt[(size_t)(c->nel_local + g)] = plan.topo_of(xg[(size_t)g]);
+  if (dev_upload(c, &c->xtopo, xt.data(), xt.size()) != cudaSuccess) { why = "ghost topology upload"; return false; }
+  // coordinates: grow X by the ghost layer
+  double *X2 = nullptr;
+  if (cudaMalloc((void **)&X2, sizeof(double) * (size_t)((c->nel_local + ng) * c->xstride)) != cudaSuccess) {
+    why = "ghost coordinates allocation";
+    return false;
+  }
+  c->allocs.push_back(X2);
+  cudaMemcpy(X2, c->X, sizeof(double) * (size_t)(c->nel_local * c->xstride), cudaMemcpyDeviceToDevice);
+  std::vector<double> gh((size_t)(ng * c->xstride), 0.0), tmp;
+  for (int64_t g = 0; g < ng; ++g) {
+    const double *src;
+    if (A.elem_nodes) src = A.elem_nodes + xg[(size_t)g] * raw;
+    else {
+      interpolate_evector(A.dim, A.p, A.vert_xyz, A.elem_vert, xg[(size_t)g], 1, tmp);
+      src = tmp.data();
+    }
+    memcpy(&gh[(size_t)(g * c->xstride)], src, sizeof(double) * raw);
+  }
+  cudaMemcpy(X2 + c->nel_local * c->xstride, gh.data(), sizeof(double) * gh.size(), cudaMemcpyHostToDevice);
+  c->X = X2;  // the old local-only array stays in allocs (freed at destroy)
+  // exchange lists: ghosts held by peer q are a contiguous range of xg (ranks own contiguous
+  // element ranges, xg is sorted); this rank sends q the local elements in q's ghost layer
+  c->xg_send_count.assign(A.nranks, 0);
+  c->xg_recv_begin.assign(A.nranks, 0);
+  c->xg_recv_count.assign(A.nranks, 0);
+  std::vector<int32_t> sidx;
+  for (int q = 0; q < A.nranks; ++q) {
+    if (q == A.rank) continue;
+    for (int64_t g = 0; g < ng; ++g)
+      if (xg[(size_t)g] >= plan.erb[q] && xg[(size_t)g] < plan.erb[q + 1]) {
+        if (c->xg_recv_count[q] == 0) c->xg_recv_begin[q] = g;
+        ++c->xg_recv_count[q];
+      }
+    for (int64_t e : xframe_ghosts(plan, q))
+      if (e >= plan.elem_begin && e < plan.elem_begin + plan.nel_local) {
+        sidx.push_back((int32_t)(e - plan.elem_begin));
+        ++c->xg_send_count[q];
+      }
+  }
+  if (!sidx.empty()) {
+    if (dev_upload(c, &c->xg_send_idx, sidx.data(), sidx.size()) != cudaSuccess ||
+        dev_alloc(c, &c->xg_send_buf, sidx.size() * (size_t)c->xstride) != cudaSuccess) {
+      why = "ghost exchange buffers";
+      return false;
+    }
+  }
+  return true;
+}
+
+// refresh the ghost layer's coordinates from the peers (NCCL, context stream)
+lor_status exchange_ghost_coords(lor_ctx c) {
+  if (c->n_xghost == 0 || c->nranks == 1 || !c->comm) return LOR_OK;
+  int64_t ns = 0;
+  for (int64_t v : c->xg_send_count) ns += v;
+  if (ns > 0) CUDA_TRY(c, launch_gather_rows(c->X, c->xstride, c->xg_send_idx, ns, c->xg_send_buf, c->stream));
+  if (g_nccl.GroupStart() != ncclSuccess) return fail(c, LOR_ERR_NCCL, "ncclGroupStart");
+  int64_t so = 0;
+  for (int q = 0; q < c->nranks; ++q) {
+    if (q == c->rank) continue;
+    if (c->xg_send_count[q] > 0) {
+      if (g_nccl.Send(c->xg_send_buf + so * c->xstride, (size_t)(c->xg_send_count[q] * c->xstride * 8), ncclUint8, q,
+                      c->comm, c->stream) != ncclSuccess) { g_nccl.GroupEnd(); return fail(c, LOR_ERR_NCCL, "ncclSend"); }
+      so += c->xg_send_count[q];
+    }
+    if (c->xg_recv_count[q] > 0) {
+      if (g_nccl.Recv(c->X + (c->nel_local + c->xg_recv_begin[q]) * c->xstride, (size_t)(c->xg_recv_count[q] * c->xstride * 8),
+                      ncclUint8, q, c->comm, c->stream) != ncclSuccess) { g_nccl.GroupEnd(); return fail(c, LOR_ERR_NCCL, "ncclRecv"); }
+    }
+  }
+  if (g_nccl.GroupEnd() != ncclSuccess) return fail(c, LOR_ERR_NCCL, "ncclGroupEnd");
+  return LOR_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -486,6 +582,50 @@ lor_status lor_plan_dry_run(const lor_setup_args *args, int64_t *info, int64_t *
       if (recv_counts) recv_counts[s * A.nranks + q] = P.valid ? P.recv_count[q] : 0;
     }
   }
+  return LOR_OK;
+}
+
+lor_status lor_xframe_dry_run(const lor_setup_args *args, int64_t *info, int64_t *send_counts, int64_t *recv_counts) {
+  if (!args || !info) return LOR_ERR_INVALID_ARGUMENT;
+  const lor_setup_args &A = *args;
+  if (A.dim != 3 || A.p < 1 || A.p > 8 || A.n_vert <= 0 || A.n_elem <= 0 || !A.elem_vert || A.nranks < 1 || A.rank < 0 ||
+      A.rank >= A.nranks || (A.nranks > 1 && !A.elem_rank_begin))
+    return LOR_ERR_INVALID_ARGUMENT;
+  HostPlan plan;
+  try {
+    PlanInput in;
+    in.dim = A.dim;
+    in.p = A.p;
+    in.rank = A.rank;
+    in.nranks = A.nranks;
+    in.n_vert = A.n_vert;
+    in.n_elem = A.n_elem;
+    in.elem_vert = A.elem_vert;
+    in.elem_rank_begin = A.elem_rank_begin;
+    plan.build(in);
+  } catch (const std::exception &ex) {
+    g_setup_error = std::string("lor_xframe_dry_run: ") + ex.what();
+    return LOR_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<XElem> xe;
+  std::vector<int64_t> xg;
+  int cmax[3];
+  std::string why;
+  const bool ok = xframe_build(plan, A.elem_vert, xe, cmax, &why, A.nranks > 1 ? &xg : nullptr);
+  info[0] = ok ? 1 : 0;
+  info[1] = (int64_t)xg.size();
+  info[2] = ok ? std::max(cmax[0], std::max(cmax[1], cmax[2])) : 0;
+  info[3] = plan.nel_local;
+  for (int q = 0; q < A.nranks; ++q) {
+    int64_t sc = 0, rc = 0;
+    if (q != A.rank) {
+      for (int64_t e : xframe_ghosts(plan, q)) sc += (e >= plan.elem_begin && e < plan.elem_begin + plan.nel_local);
+      for (int64_t e : xg) rc += (e >= plan.erb[q] && e < plan.erb[q + 1]);
+    }
+    if (send_counts) send_counts[q] = sc;
+    if (recv_counts) recv_counts[q] = rc;
+  }
+  if (!ok) g_setup_error = why;
   return LOR_OK;
 }
 
@@ -819,10 +959,12 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
   if (A.dim == 3 && c->sp[SP_H1].valid && c->nel_local > 0 && !(getenv("LOR_XFRAME") && !atoi(getenv("LOR_XFRAME")))) {
     SpaceDev &S = c->sp[SP_H1];
     std::vector<XElem> xe;
+    std::vector<int64_t> xg;
     std::string why;
-    if (c->nel_local * c->xstride >= (int64_t(1) << 31)) {
+    if ((c->nel_local + (A.nranks > 1 ? (int64_t)xframe_ghosts(plan, A.rank).size() : 0)) * c->xstride >= (int64_t(1) << 31)) {
       why = "E-vector index exceeds int32";
-    } else if (xframe_build(plan, A.elem_vert, xe, S.xc, &why)) {
+    } else if (xframe_build(plan, A.elem_vert, xe, S.xc, &why, A.nranks > 1 ? &xg : nullptr) &&
+               !(A.nranks > 1 && !xframe_ghost_layer(c, plan, A, xg, why))) {
       // records in processing order, so a CTA reads its record, restriction and gather list by
       // its own index (one dependent load less)
       {
@@ -843,7 +985,7 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
       XSetupArgs xa{};
       xa.nel_local = c->nel_local;
       xa.xe = S.xe;
-      xa.topo = c->topo;
+      xa.topo = c->xtopo ? c->xtopo : c->topo;
       fill_base(S, xa.base);
       xa.row_begin = S.row_begin;
       xa.box = S.xbox;
@@ -997,7 +1139,7 @@ lor_status lor_update_coordinates(lor_ctx c, const double *elem_nodes) {
   if (c->nel_local > 0)
     CUDA_TRY(c, cudaMemcpy2DAsync(c->X, c->xstride * sizeof(double), elem_nodes, raw, raw, (size_t)c->nel_local,
                                   cudaMemcpyDefault, c->stream));
-  return LOR_OK;
+  return exchange_ghost_coords(c);  // extended frame on several ranks: the ghost layer follows
 }
 
 lor_status lor_set_exchange(lor_ctx c, int mode) {

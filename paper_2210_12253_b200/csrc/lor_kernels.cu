@@ -623,6 +623,24 @@ cudaError_t launch_transpose(const int32_t *map, int64_t n_ent, int64_t row_begi
   return cudaGetLastError();
 }
 
+// rows (stride doubles each) of X at the listed indices, packed into buf (ghost-layer coordinates
+// of the extended frame sent to a peer rank)
+__global__ void k_gather_rows(const double *__restrict__ X, int64_t stride, const int32_t *__restrict__ idx, int64_t n,
+                              double *__restrict__ buf) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * stride; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / stride, k = i - r * stride;
+    buf[i] = X[(int64_t)idx[r] * stride + k];
+  }
+}
+
+cudaError_t launch_gather_rows(const double *X, int64_t stride, const int32_t *idx, int64_t n, double *buf, cudaStream_t st) {
+  const int64_t tot = n * stride;
+  if (tot <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 16));
+  k_gather_rows<<<g, 256, 0, st>>>(X, stride, idx, n, buf);
+  return cudaGetLastError();
+}
+
 __global__ void k_rowptr_stride(int64_t *row_ptr, int64_t n, int w) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
     row_ptr[i] = (int64_t)w * i;

@@ -174,6 +174,7 @@ cudaError_t launch_plan_merge(const PlanArgs &a, int n_ose, cudaStream_t st);
 cudaError_t launch_merge_rows(const MergeArgs &a, cudaStream_t st);
 cudaError_t launch_discrete(int which, const DiscArgs &a, cudaStream_t st);
 cudaError_t launch_rowptr_stride(int64_t *row_ptr, int64_t n, int w, cudaStream_t st);
+cudaError_t launch_gather_rows(const double *X, int64_t stride, const int32_t *idx, int64_t n, double *buf, cudaStream_t st);
 cudaError_t launch_dofmap(int dim, int space, const DofmapArgs &a, cudaStream_t st);
 // dof -> (local element * ndpe + local dof) transpose of an element restriction map[n_ent] for the
 // owned rows [row_begin, row_begin + n_local): off[n_local+1], ent[off[n_local]] ascending per row.

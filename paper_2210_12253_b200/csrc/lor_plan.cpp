@@ -119,6 +119,46 @@ void slot_entity(int dim, int tau, int &type, int &lidx) {
   lidx = 2 * n + (c[n] == 2);
 }
 
+// topology record of any element e (entity ids, orientation codes, valences, TF_MIN / TF_OWNED
+// for this rank); valid after build()
+ElemTopo HostPlan::topo_of(int64_t e) const {
+  const int nc = 1 << dim, nle = (dim == 3) ? 12 : 4;
+  const int nslot = (dim == 3) ? 27 : 9;
+  auto owner = [&](int type, int64_t id) -> int {
+    if (type == 3) return elem_rank[id];
+    return elem_rank[inc_el[type][inc_off[type][id]]];
+  };
+  ElemTopo T;
+  for (int tau = 0; tau < 27; ++tau) {
+    T.ent[tau] = -1;
+    T.orient[tau] = 0;
+    T.val[tau] = 0;
+    T.flags[tau] = 0;
+  }
+  for (int i = 0; i < 3; ++i) T.pad[i] = 0;
+  for (int tau = 0; tau < nslot; ++tau) {
+    int type, lidx;
+    slot_entity(dim, tau, type, lidx);
+    uint8_t orient = 0;
+    int64_t id;
+    if (type == 0) id = EVp[e * nc + lidx];
+    else if (type == 1) { id = el_edge[e * nle + lidx]; orient = el_edge_rev[e * nle + lidx]; }
+    else if (type == 2) { id = el_face[e * 6 + lidx]; orient = el_face_code[e * 6 + lidx]; }
+    else id = e;
+    T.ent[tau] = (int32_t)id;
+    T.orient[tau] = orient;
+    if (type == 3) {
+      T.val[tau] = 1;
+      T.flags[tau] = TF_MIN | (elem_rank[e] == rank ? TF_OWNED : 0);
+    } else {
+      const int64_t k0 = inc_off[type][id], k1 = inc_off[type][id + 1];
+      T.val[tau] = (uint8_t)std::min<int64_t>(k1 - k0, 255);
+      T.flags[tau] = (inc_el[type][k0] == e ? TF_MIN : 0) | (owner(type, id) == rank ? TF_OWNED : 0);
+    }
+  }
+  return T;
+}
+
 void HostPlan::build(const PlanInput &in) {
   dim = in.dim;
   p = in.p;
@@ -254,43 +294,10 @@ void HostPlan::build(const PlanInput &in) {
       if (is_ghost[e]) ghost.push_back(e);
   }
   // ---- topology records (local elements, then ghosts) -------------------------------------------
+  EVp = EV;
   const int64_t ntop = nel_local + (int64_t)ghost.size();
   topo.assign(ntop, ElemTopo{});
-  auto slot_info = [&](int64_t e, int tau, int &type, int64_t &id, uint8_t &orient) {
-    int lidx;
-    slot_entity(dim, tau, type, lidx);
-    orient = 0;
-    if (type == 0) id = EV[e * nc + lidx];
-    else if (type == 1) { id = el_edge[e * nle + lidx]; orient = el_edge_rev[e * nle + lidx]; }
-    else if (type == 2) { id = el_face[e * 6 + lidx]; orient = el_face_code[e * 6 + lidx]; }
-    else id = e;
-  };
-  for (int64_t i = 0; i < ntop; ++i) {
-    int64_t e = (i < nel_local) ? elem_begin + i : ghost[i - nel_local];
-    ElemTopo &T = topo[i];
-    for (int tau = 0; tau < 27; ++tau) {
-      T.ent[tau] = -1;
-      T.orient[tau] = 0;
-      T.val[tau] = 0;
-      T.flags[tau] = 0;
-    }
-    for (int tau = 0; tau < nslot; ++tau) {
-      int type;
-      int64_t id;
-      uint8_t orient;
-      slot_info(e, tau, type, id, orient);
-      T.ent[tau] = (int32_t)id;
-      T.orient[tau] = orient;
-      if (type == 3) {
-        T.val[tau] = 1;
-        T.flags[tau] = TF_MIN | (elem_rank[e] == rank ? TF_OWNED : 0);
-      } else {
-        int64_t k0 = inc_off[type][id], k1 = inc_off[type][id + 1];
-        T.val[tau] = (uint8_t)std::min<int64_t>(k1 - k0, 255);
-        T.flags[tau] = (inc_el[type][k0] == e ? TF_MIN : 0) | (owner(type, id) == rank ? TF_OWNED : 0);
-      }
-    }
-  }
+  for (int64_t i = 0; i < ntop; ++i) topo[i] = topo_of((i < nel_local) ? elem_begin + i : ghost[i - nel_local]);
 
   // ---- per space numbering, rows, shared-row plan -------------------------------------------------
   for (int s = 0; s < 3; ++s) {
@@ -402,10 +409,9 @@ void HostPlan::build(const PlanInput &in) {
       ElemSpace &R = S.esp[i];
       for (int tau = 0; tau < 27; ++tau) { R.rec[tau] = -1; R.ose[tau] = -1; R.ebase[tau] = -1; R.sflags[tau] = 0; }
       for (int tau = 0; tau < nslot; ++tau) {
-        int type;
-        int64_t id;
-        uint8_t orient;
-        slot_info(e, tau, type, id, orient);
+        int type, lidx;
+        slot_entity(dim, tau, type, lidx);
+        const int64_t id = topo[(size_t)i].ent[tau];
         R.ebase[tau] = S.base[type].empty() ? -1 : S.base[type][id];
         if (type == 3 || nd[type] == 0) continue;
         int64_t k0 = inc_off[type][id], k1 = inc_off[type][id + 1];

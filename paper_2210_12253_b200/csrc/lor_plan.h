@@ -45,8 +45,10 @@ struct HostPlan {
   std::vector<int64_t> ghost;      // ghost element ids (topology records after the local ones)
   std::vector<ElemTopo> topo;      // local elements, then ghosts
   SpacePlan sp[3];
+  const int64_t *EVp = nullptr;    // the caller's elem_vert (valid during lor_setup)
 
   void build(const PlanInput &in);
+  ElemTopo topo_of(int64_t e) const;
 };
 
 int maxl_of(int dim, int space);

@@ -67,13 +67,37 @@ bool is_unit_cube(const XMap &f) {
 
 }  // namespace
 
-bool xframe_build(const HostPlan &plan, const int64_t *EV, std::vector<XElem> &out, int cmax[3], std::string *why) {
+// non-local elements sharing a coarse vertex with a local element (sorted): the ghost layer of the
+// extended frame on several ranks (every element of a 3x3x3 neighbourhood shares a vertex with its
+// centre); the same rule applied to another rank gives the elements this rank sends it
+std::vector<int64_t> xframe_ghosts(const HostPlan &plan, int rank) {
+  const int64_t *EV = plan.EVp;
+  std::vector<char> mark((size_t)plan.nel, 0);
+  for (int64_t e = plan.erb[rank]; e < plan.erb[rank + 1]; ++e)
+    for (int v = 0; v < 8; ++v) {
+      const int64_t vid = EV[e * 8 + v];
+      for (int64_t k = plan.inc_off[0][vid]; k < plan.inc_off[0][vid + 1]; ++k) {
+        const int64_t o = plan.inc_el[0][k];
+        if (plan.elem_rank[o] != rank) mark[(size_t)o] = 1;
+      }
+    }
+  std::vector<int64_t> g;
+  for (int64_t e = 0; e < plan.nel; ++e)
+    if (mark[(size_t)e]) g.push_back(e);
+  return g;
+}
+
+bool xframe_build(const HostPlan &plan, const int64_t *EV, std::vector<XElem> &out, int cmax[3], std::string *why,
+                  std::vector<int64_t> *xghost) {
   auto no = [&](const char *m) {
     if (why) *why = m;
     return false;
   };
   if (plan.dim != 3) return no("dim != 3");
-  if (plan.nranks != 1) return no("nranks > 1");
+  if (!xghost && plan.nranks != 1) return no("nranks > 1 without a ghost layer");
+  std::vector<int64_t> gl;
+  if (plan.nranks > 1) gl = xframe_ghosts(plan, plan.rank);
+  if (xghost) *xghost = gl;
   const int p = plan.p;
   const int64_t n = plan.nel_local;
   out.assign((size_t)n, XElem{});
@@ -213,7 +237,13 @@ bool xframe_build(const HostPlan &plan, const int64_t *EV, std::vector<XElem> &o
         if (s < 0) code |= 1u << (6 + a);
       }
       for (int k = 0; k < 3; ++k) code |= (uint32_t)(g.P[0][k] + 1) << (9 + 2 * k);
-      X.nbr[i].el = (int32_t)(g.el - plan.elem_begin);
+      if (g.el >= plan.elem_begin && g.el < plan.elem_begin + n) {
+        X.nbr[i].el = (int32_t)(g.el - plan.elem_begin);
+      } else {  // ghost layer: indices after the local elements
+        const auto it = std::lower_bound(gl.begin(), gl.end(), g.el);
+        if (it == gl.end() || *it != g.el) return no("neighbour outside the ghost layer");
+        X.nbr[i].el = (int32_t)(n + (it - gl.begin()));
+      }
       X.nbr[i].code = code;
     }
   }

@@ -129,10 +129,13 @@ int xv_supported(int space, int p, const int cmax[3]);   // 1: a fill kernel is 
 int64_t xv_map_words(int space, int p, const int cmax[3]);  // per element
 int xv_pos_words(int space);                              // per row
 
-// host: regular-neighbourhood check and per-element extended-frame records (nranks == 1)
+// host: regular-neighbourhood check and per-element extended-frame records.  nranks > 1 needs
+// xghost: the ghost layer (sorted global ids of the non-local elements sharing a vertex with a local
+// element) is returned there and neighbour indices >= n_elem_local refer to it.
 struct HostPlan;
 bool xframe_build(const HostPlan &plan, const int64_t *elem_vert, std::vector<XElem> &out, int cmax[3],
-                  std::string *why);
+                  std::string *why, std::vector<int64_t> *xghost = nullptr);
+std::vector<int64_t> xframe_ghosts(const HostPlan &plan, int rank);
 
 // cell-box extent the fill kernel is instantiated for, and points per element of the extended map
 inline int xfill_nb(int p, const int cmax[3]) {

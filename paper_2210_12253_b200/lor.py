@@ -70,6 +70,7 @@ def lib():
         L.lor_exchange_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
         L.lor_assemble_finish.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Csr)]
         L.lor_plan_dry_run.argtypes = [C.POINTER(_SetupArgs), C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lor_xframe_dry_run.argtypes = [C.POINTER(_SetupArgs), C.c_void_p, C.c_void_p, C.c_void_p]
         L.lor_debug_dump.restype = C.c_int64
         L.lor_debug_dump.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
         L.lor_update_coordinates.argtypes = [C.c_void_p, C.c_void_p]
@@ -106,6 +107,28 @@ def plan_dry_run(mesh, rank=0, nranks=1, elem_rank_begin=None):
     send = np.zeros((3, nranks), dtype=np.int64)
     recv = np.zeros((3, nranks), dtype=np.int64)
     rc = lib().lor_plan_dry_run(C.byref(a), info.ctypes.data, send.ctypes.data, recv.ctypes.data)
+    if rc:
+        raise LorError(rc, lib().lor_last_error(None).decode())
+    return info, send, recv
+
+
+def xframe_dry_run(mesh, rank=0, nranks=1):
+    """Host-only extended-frame plan of one rank (no GPU): (info[4], send[nranks], recv[nranks]) --
+    lor_xframe_dry_run: regular neighbourhood, ghost layer size, largest cell box, local elements."""
+    vert = np.ascontiguousarray(mesh.vert, dtype=np.float64)
+    elem = np.ascontiguousarray(mesh.elem, dtype=np.int64)
+    erb = np.ascontiguousarray(mesh.elem_rank_begin if nranks > 1 else [0, elem.shape[0]], dtype=np.int64)
+    a = _SetupArgs()
+    a.dim, a.p = int(mesh.dim), int(mesh.p)
+    a.n_vert, a.vert_xyz = vert.shape[0], vert.ctypes.data
+    a.n_elem, a.elem_vert = elem.shape[0], elem.ctypes.data
+    a.elem_nodes = None
+    a.rank, a.nranks = rank, nranks
+    a.elem_rank_begin = erb.ctypes.data
+    info = np.zeros(4, dtype=np.int64)
+    send = np.zeros(nranks, dtype=np.int64)
+    recv = np.zeros(nranks, dtype=np.int64)
+    rc = lib().lor_xframe_dry_run(C.byref(a), info.ctypes.data, send.ctypes.data, recv.ctypes.data)
     if rc:
         raise LorError(rc, lib().lor_last_error(None).decode())
     return info, send, recv

@@ -1,0 +1,77 @@
+"""NCCL path on >= 2 GPUs (skipped with fewer): one process per GPU, ncclUniqueId broadcast over
+torch.distributed.  Each rank's owned rows against the oracle's rank-major matrix:
+  * H1 and RT: single-pass extended frame with the ghost layer (no partial-row exchange);
+  * ND: element + merge passes with the interface partial rows over grouped ncclSend/ncclRecv;
+  * after lor_update_coordinates with new (jittered) coordinates, whose ghost layer is refreshed from
+    the peers over NCCL, the re-assembly matches the oracle on the moved mesh."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    errs = []
+    try:
+        from oracle import oracle as O
+        from paper_2210_12253_b200 import meshgen as mg
+        from paper_2210_12253_b200.lor import LOR, nccl_unique_id
+        from tests.parity import compare_csr_arrays
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ma = mg.box_mesh(3, (3, 3, 2 * world), 4, kershaw=0.3, nranks=world)
+        mb = mg.box_mesh(3, (3, 3, 2 * world), 4, jitter=True, nranks=world)
+        for space in ("h1", "nd", "rt"):
+            ctx = LOR(ma, rank=rank, nranks=world, nccl_id=obj[0], device=rank)
+            qq = ctx.query(space)
+            out = ctx.assemble(space, 1.3, 0.7, "vertex")
+            ctx.sync()
+            ref = O.assemble(ma, space, "vertex", 1.3, 0.7)
+            try:
+                compare_csr_arrays(*(t.cpu().numpy() for t in out), ref, qq["row_begin"], qq["n_local"],
+                                   f"{space} rank {rank}")
+            except AssertionError as e:
+                errs.append(str(e))
+            e0, e1 = int(mb.elem_rank_begin[rank]), int(mb.elem_rank_begin[rank + 1])
+            ctx.update_coordinates(torch.from_numpy(np.ascontiguousarray(mb.X[e0:e1])).cuda())
+            ctx.reassemble(space, 1.3, 0.7, "vertex", out=out)
+            ctx.sync()
+            refb = O.assemble(mb, space, "vertex", 1.3, 0.7)
+            try:
+                compare_csr_arrays(*(t.cpu().numpy() for t in out), refb, qq["row_begin"], qq["n_local"],
+                                   f"{space} moved rank {rank}")
+            except AssertionError as e:
+                errs.append(str(e))
+            ctx.close()
+    except Exception as e:  # noqa: BLE001
+        errs.append(repr(e))
+    finally:
+        dist.destroy_process_group()
+    q.put((rank, errs))
+
+
+def test_nccl_two_gpus():
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, errs in res:
+        assert not errs, f"rank {rank}: {errs}"

@@ -114,6 +114,9 @@ def test_multirank_emulated(torch_cuda, oracle_lib, space, nranks):
         c.sync()
     ref = oracle_lib.assemble(m, space, "vertex", 1.0, 1.0)
     for r, c in enumerate(ctxs):
+        # H1 and RT keep the single-pass extended frame on every rank (ghost layer of neighbour
+        # coordinates, no partial-row exchange); ND takes the element + merge passes + exchange
+        assert c.fill_path(space) == (0 if space == "nd" else 1)
         q = c.query(space)
         rp, col, val = (to_host(t) for t in outs[r])
         compare_full(rp, col, val, ref, q["row_begin"], q["n_local"], f"{space} rank {r}/{nranks}")
@@ -198,3 +201,25 @@ def test_full_size_c4_c5_row_sampled(torch_cuda, oracle_lib, cfg, space):
     same_row = np.diff(np.repeat(np.arange(q["n_local"]), d)) == 0
     assert (np.diff(col.astype(np.int64))[same_row] > 0).all()
     ctx.close()
+
+
+@pytest.mark.parametrize("space,p,shape", [("h1", 4, (4, 3, 6)), ("h1", 8, (2, 2, 4)), ("rt", 4, (3, 4, 6)),
+                                           ("h1", 2, (3, 3, 8))])
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_multirank_xframe_kershaw(torch_cuda, oracle_lib, space, p, shape, nranks):
+    """extended frame on several ranks (ghost layer of neighbour coordinates from the global
+    E-vector at setup): each rank's owned rows, Kershaw slabs, equal the oracle's"""
+    from paper_2210_12253_b200.lor import LOR
+    if shape[2] % nranks:
+        pytest.skip("slabs")
+    m = mg.box_mesh(3, shape, p, kershaw=0.3, nranks=nranks)
+    ref = oracle_lib.assemble(m, space, "vertex", 1.3, 0.7)
+    for r in range(nranks):
+        c = LOR(m, rank=r, nranks=nranks)
+        assert c.fill_path(space) == 1
+        q = c.query(space)
+        rp, col, val = c.assemble(space, 1.3, 0.7, "vertex")
+        c.sync()
+        compare_full(to_host(rp), to_host(col), to_host(val), ref, q["row_begin"], q["n_local"],
+                     f"{space} xframe rank {r}/{nranks}")
+        c.close()
