@@ -407,8 +407,8 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.ownbase = S.ownbase;
   a.ownpos = S.ownpos;
   a.dbg = c->dbg;
-  a.emap = S.emap;
-  a.esgn = S.esgn;
+  a.emap = c->nranks == 1 ? S.emap : nullptr;
+  a.esgn = c->nranks == 1 ? S.esgn : nullptr;
   CUDA_TRY(c, launch_assemble(c->dim, s, c->p, (int)quad, a, c->stream, nullptr));
   if (c->nel_local > 0) c->launches++;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
@@ -935,9 +935,10 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     a.ownpos = S.ownpos;
     if (launch_assemble(A.dim, s, A.p, 0, a, c->stream, nullptr) != cudaSuccess) return bail(LOR_ERR_CUDA, "own-row positions");
   }
-  // one rank: the element restriction of every space, computed once (k_dofmap) and read by the
-  // element pass instead of rebuilding its block table per call (LOR_EMAP=0: off)
-  if (c->nranks == 1 && c->nel_local > 0 && !(getenv("LOR_EMAP") && !atoi(getenv("LOR_EMAP")))) {
+  // the element restriction of every space, computed once (k_dofmap): read by the discrete
+  // operators, and on one rank by the element pass instead of rebuilding its block table per call
+  // (LOR_EMAP=0: off)
+  if (c->nel_local > 0 && !(getenv("LOR_EMAP") && !atoi(getenv("LOR_EMAP")))) {
     for (int s = 0; s < 3; ++s) {
       SpaceDev &S = c->sp[s];
       if (!S.valid) continue;
@@ -1181,17 +1182,23 @@ lor_status lor_discrete_grad(lor_ctx c, lor_csr *out) {
   const SpaceDev &R = c->sp[SP_ND];
   if (out->cap_nnz < 2 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 2 n_rows");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  DiscArgs a;
-  a.p = c->p;
-  a.nel_local = c->nel_local;
-  a.topo = c->topo;
-  fill_base(R, a.base_row);
-  fill_base(c->sp[SP_H1], a.base_col);
-  a.row_begin = R.row_begin;
-  a.col = out->col;
-  a.val = out->val;
   CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 2, c->stream));
-  CUDA_TRY(c, launch_discrete(0, a, c->stream));
+  const SpaceDev &Cs = c->sp[SP_H1];
+  if (R.emap && Cs.emap) {
+    DiscMapArgs m{c->p, c->nel_local, c->topo, R.emap, R.esgn, Cs.emap, Cs.esgn, R.row_begin, out->col, out->val};
+    CUDA_TRY(c, launch_discrete_map(0, m, c->stream));
+  } else {
+    DiscArgs a;
+    a.p = c->p;
+    a.nel_local = c->nel_local;
+    a.topo = c->topo;
+    fill_base(R, a.base_row);
+    fill_base(c->sp[SP_H1], a.base_col);
+    a.row_begin = R.row_begin;
+    a.col = out->col;
+    a.val = out->val;
+    CUDA_TRY(c, launch_discrete(0, a, c->stream));
+  }
   c->launches += 2;
   return LOR_OK;
 }
@@ -1202,17 +1209,23 @@ lor_status lor_discrete_curl(lor_ctx c, lor_csr *out) {
   const SpaceDev &R = c->sp[SP_RT];
   if (out->cap_nnz < 4 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 4 n_rows");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  DiscArgs a;
-  a.p = c->p;
-  a.nel_local = c->nel_local;
-  a.topo = c->topo;
-  fill_base(R, a.base_row);
-  fill_base(c->sp[SP_ND], a.base_col);
-  a.row_begin = R.row_begin;
-  a.col = out->col;
-  a.val = out->val;
   CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 4, c->stream));
-  CUDA_TRY(c, launch_discrete(1, a, c->stream));
+  const SpaceDev &Cs = c->sp[SP_ND];
+  if (R.emap && Cs.emap) {
+    DiscMapArgs m{c->p, c->nel_local, c->topo, R.emap, R.esgn, Cs.emap, Cs.esgn, R.row_begin, out->col, out->val};
+    CUDA_TRY(c, launch_discrete_map(1, m, c->stream));
+  } else {
+    DiscArgs a;
+    a.p = c->p;
+    a.nel_local = c->nel_local;
+    a.topo = c->topo;
+    fill_base(R, a.base_row);
+    fill_base(c->sp[SP_ND], a.base_col);
+    a.row_begin = R.row_begin;
+    a.col = out->col;
+    a.val = out->val;
+    CUDA_TRY(c, launch_discrete(1, a, c->stream));
+  }
   c->launches += 2;
   return LOR_OK;
 }

@@ -543,6 +543,87 @@ __global__ void __launch_bounds__(128) k_discrete(DiscArgs A) {
   }
 }
 
+// G and C from the setup element restrictions (the reused HO element restriction): one
+// CTA per element, one thread per local row dof in local order (consecutive threads -> consecutive
+// rows of a coarse entity), the column restriction of the element staged in shared memory; the
+// owning element (minimal element containing the row's entity, this rank) writes the row's 2 / 4
+// entries with one vector store each (row_ptr[i] = 2i / 4i keeps them 8 / 16-byte aligned).  Reads
+// exactly the map bytes of SURVEY d.3's B_G / B_C.
+template <int WHICH>
+__global__ void __launch_bounds__(128) k_discrete_map(DiscMapArgs A) {
+  constexpr int RSP = WHICH == 0 ? SP_ND : SP_RT;
+  __shared__ uint8_t flags[27];
+  extern __shared__ int32_t cmap[];  // [ndpe_col] ids, then (curl) [ndpe_col] signs as int8
+  const int64_t el = blockIdx.x;
+  if (el >= A.nel_local) return;
+  const int p = A.p;
+  const int ndr = WHICH == 0 ? 3 * p * (p + 1) * (p + 1) : 3 * p * p * (p + 1);
+  const int ndc = WHICH == 0 ? (p + 1) * (p + 1) * (p + 1) : 3 * p * (p + 1) * (p + 1);
+  int8_t *csg = reinterpret_cast<int8_t *>(cmap + ndc);
+  if (threadIdx.x < 27) flags[threadIdx.x] = A.topo[el].flags[threadIdx.x];
+  for (int i = threadIdx.x; i < ndc; i += blockDim.x) {
+    cmap[i] = __ldg(A.cmap + el * ndc + i);
+    if (WHICH == 1) csg[i] = __ldg(A.csgn + el * ndc + i);
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < ndr; l += blockDim.x) {
+    int s, x[3];
+    decode_local<3, RSP>(p, l, s, x);
+    const int tr = row_tau<3, RSP>(p, s, x);
+    if ((flags[tr] & (TF_OWNED | TF_MIN)) != (TF_OWNED | TF_MIN)) continue;
+    const int64_t row = (int64_t)__ldg(A.rmap + el * ndr + l) - A.row_begin;
+    const double sg = (double)__ldg(A.rsgn + el * ndr + l);
+    if (WHICH == 0) {
+      const int lt = x[0] + (p + 1) * (x[1] + (p + 1) * x[2]);
+      const int lh = lt + (s == 0 ? 1 : (s == 1 ? p + 1 : (p + 1) * (p + 1)));
+      const int gt = cmap[lt], gh = cmap[lh];
+      const bool sw = gh < gt;
+      reinterpret_cast<int2 *>(A.col)[row] = sw ? make_int2(gh, gt) : make_int2(gt, gh);
+      reinterpret_cast<double2 *>(A.val)[row] = sw ? make_double2(sg, -sg) : make_double2(-sg, sg);
+    } else {
+      // face (s, x): cyclic in-face axes (u', v') = (s+1, s+2) mod 3; edges u'-edge at v'=0 (+1),
+      // v'-edge at u'=1 (+1), u'-edge at v'=1 (-1), v'-edge at u'=0 (-1) (App. A.5, reading P-15)
+      const int up = (s + 1) % 3, vp = (s + 2) % 3;
+      int c[4];
+      double v[4];
+      const int eax[4] = {up, vp, up, vp};
+      const int eoff[4] = {0, 1, 1, 0};
+      const double es[4] = {1.0, 1.0, -1.0, -1.0};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int y[3] = {x[0], x[1], x[2]};
+        const int other = (eax[q] == up) ? vp : up;
+        y[other] += eoff[q];
+        const int a = eax[q];
+        const int e0 = a == 0 ? p : p + 1, e1 = a == 1 ? p : p + 1;
+        const int le = a * p * (p + 1) * (p + 1) + y[0] + e0 * (y[1] + e1 * y[2]);
+        c[q] = cmap[le];
+        v[q] = es[q] * sg * (double)csg[le];
+      }
+#define CSWAP(i, j)                                   \
+  if (c[j] < c[i]) {                                  \
+    int tc = c[i]; c[i] = c[j]; c[j] = tc;            \
+    double tv = v[i]; v[i] = v[j]; v[j] = tv;         \
+  }
+      CSWAP(0, 1) CSWAP(2, 3) CSWAP(0, 2) CSWAP(1, 3) CSWAP(1, 2)
+#undef CSWAP
+      reinterpret_cast<int4 *>(A.col)[row] = make_int4(c[0], c[1], c[2], c[3]);
+      reinterpret_cast<double2 *>(A.val)[2 * row] = make_double2(v[0], v[1]);
+      reinterpret_cast<double2 *>(A.val)[2 * row + 1] = make_double2(v[2], v[3]);
+    }
+  }
+}
+
+cudaError_t launch_discrete_map(int which, const DiscMapArgs &a, cudaStream_t st) {
+  if (a.nel_local <= 0) return cudaSuccess;
+  const int p = a.p;
+  const int ndc = which == 0 ? (p + 1) * (p + 1) * (p + 1) : 3 * p * (p + 1) * (p + 1);
+  const size_t smem = (size_t)ndc * (which == 0 ? 4 : 5);
+  if (which == 0) k_discrete_map<0><<<(unsigned)a.nel_local, 128, smem, st>>>(a);
+  else k_discrete_map<1><<<(unsigned)a.nel_local, 128, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <int DIM, int SP>
 __global__ void __launch_bounds__(128) k_dofmap(DofmapArgs A) {
   __shared__ ElemTopo T;

@@ -149,6 +149,20 @@ struct DiscArgs {
   double *val;
 };
 
+// discrete gradient / curl from the element restrictions (rows: ND / RT, columns: H1 / ND)
+struct DiscMapArgs {
+  int p;
+  int64_t nel_local;
+  const ElemTopo *topo;
+  const int32_t *rmap;  // [nel_local][ndpe_row]
+  const int8_t *rsgn;
+  const int32_t *cmap;  // [nel_local][ndpe_col]
+  const int8_t *csgn;   // curl only
+  int64_t row_begin;
+  int32_t *col;
+  double *val;
+};
+
 struct DofmapArgs {
   int p, ndpe;
   int64_t nel_local;
@@ -173,6 +187,7 @@ cudaError_t launch_finalize_list(const FinArgs &f, cudaStream_t st);
 cudaError_t launch_plan_merge(const PlanArgs &a, int n_ose, cudaStream_t st);
 cudaError_t launch_merge_rows(const MergeArgs &a, cudaStream_t st);
 cudaError_t launch_discrete(int which, const DiscArgs &a, cudaStream_t st);
+cudaError_t launch_discrete_map(int which, const DiscMapArgs &a, cudaStream_t st);
 cudaError_t launch_rowptr_stride(int64_t *row_ptr, int64_t n, int w, cudaStream_t st);
 cudaError_t launch_gather_rows(const double *X, int64_t stride, const int32_t *idx, int64_t n, double *buf, cudaStream_t st);
 cudaError_t launch_dofmap(int dim, int space, const DofmapArgs &a, cudaStream_t st);

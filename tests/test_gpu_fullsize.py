@@ -110,3 +110,20 @@ def test_discrete_per_rank(torch_cuda, oracle_lib, which):
 def test_gauss2_every_p(torch_cuda, oracle_lib, space, p):
     m = mg.box_mesh(3, (3, 2, 2) if p <= 4 else (2, 2, 2), p, jitter=True, scramble=True)
     full_case(oracle_lib, m, dict(space=space, alpha=1.3, beta=0.7, quad="gauss2"), f"{space} gauss2 p={p}")
+
+
+@pytest.mark.parametrize("which", ["grad", "curl"])
+def test_discrete_map_path_equals_block_path(torch_cuda, monkeypatch, which):
+    """G / C from the setup element restrictions (k_discrete_map, default) and from the per-element
+    affine blocks (k_discrete, LOR_EMAP=0): bit-identical arrays"""
+    from paper_2210_12253_b200.lor import LOR
+    m = mg.box_mesh(3, (3, 3, 2), 3, jitter=True, scramble=True)
+    outs = []
+    for emap in ("1", "0"):
+        monkeypatch.setenv("LOR_EMAP", emap)
+        ctx = LOR(m)
+        outs.append([to_host(t).copy() for t in ctx.discrete(which)])
+        ctx.sync()
+        ctx.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
