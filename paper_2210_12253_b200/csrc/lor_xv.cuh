@@ -59,13 +59,18 @@ struct XvCfg {
   // rows processed per group of GZ z-layers: all of them at once for RT with resident cells (short
   // rows: per-layer barriers would dominate), one layer otherwise
   static constexpr int GZ = (ONE && SP == SP_RT) ? P + 1 : 1;
-  static constexpr int MAXG = GZ * MAXR;
+  // rows of a group in family-major segments, each starting at a warp boundary (a warp then runs
+  // one family's code: no divergence between the families' unrolled row kernels)
+  static constexpr int NF2 = GZ * NRF2, NF0 = GZ * NRF0;
+  static constexpr int B0 = (NF2 + 31) / 32 * 32, B1 = B0 + (NF0 + 31) / 32 * 32;
+  static constexpr int MAXG = B1 + NF0;
   static constexpr int RPT = (MAXG + 127) / 128;
   static constexpr int NSLOT = ONE ? NB : 2;
   static constexpr int OFF_CM = 3 * NPB * 8;                       // E-vector box [3][NPB]
   static constexpr int OFF_ST = OFF_CM + NSLOT * NE * NCP * 8;     // cell layers [NSLOT][NE][NCP]
-  static constexpr int OFF_SC = OFF_ST + MAXG * W * 8;             // staged values [MAXG][W]
-  static constexpr int OFF_XV = OFF_SC + MAXG * W * 4;             // staged columns [MAXG][W]
+  static constexpr int NROWS = NF2 + 2 * NF0;                      // rows of a group (staging capacity)
+  static constexpr int OFF_SC = OFF_ST + NROWS * W * 8;            // staged values [NROWS][W]
+  static constexpr int OFF_XV = OFF_SC + NROWS * W * 4;            // staged columns [NROWS][W]
   static constexpr int OFF_MO = (OFF_XV + 3 * NVF * 4 + 15) / 16 * 16;  // restriction [3][NVF]
   static constexpr int SMEM = OFF_MO + 16 * RPT;                   // per (rr, warp): staged entries
 };
@@ -126,6 +131,33 @@ __device__ __forceinline__ bool layer_row(int z, int t, int &s, int x[3]) {
   x[1] = t / n0;
   x[2] = z;
   return SP == SP_ND ? true : z < P;
+}
+
+// row t of the group of GZ layers starting at z0 (family-major warp-aligned segments, see XvCfg)
+template <int P, int SP, int GZ, int B0, int B1, int NF2, int NF0>
+__device__ __forceinline__ bool group_row(int z0, int t, int &s, int x[3]) {
+  constexpr int NRF2 = SP == SP_ND ? (P + 1) * (P + 1) : P * P, NRF0 = P * (P + 1);
+  int k, nr;
+  if (t < B0) {
+    if (t >= NF2) return false;
+    k = t;
+    nr = NRF2;
+    s = 2;
+  } else if (t < B1) {
+    k = t - B0;
+    if (k >= NF0) return false;
+    nr = NRF0;
+    s = 0;
+  } else {
+    k = t - B1;
+    if (k >= NF0) return false;
+    nr = NRF0;
+    s = 1;
+  }
+  const int z = z0 + k / nr, kk = k % nr;
+  if (z > P) return false;
+  const int tt = s == 2 ? kk : (s == 0 ? NRF2 + kk : NRF2 + NRF0 + kk);
+  return layer_row<P, SP>(z, tt, s, x);
 }
 
 // coarse entity slot (element-local classes) of the dof of family s at x
@@ -496,14 +528,15 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
   auto load_layer = [&](int zg) {  // rows of the group starting at layer zg
 #pragma unroll
     for (int rr = 0; rr < CF::RPT; ++rr) {
-      const int tg = tid + 128 * rr, zz = zg + tg / CF::MAXR, t = tg % CF::MAXR;
+      const int tg = tid + 128 * rr;
       ns[rr] = -1;
       nn[rr] = 0;
       nout[rr] = -1;
 #pragma unroll
       for (int q = 0; q < CF::PW; ++q) npw[rr][q] = 0xffffffffu;
       int sf = 0, xx[3] = {0, 0, 0};
-      if (tg < CF::MAXG && zz <= P && layer_row<P, SP>(zz, t, sf, xx) && ((own >> dof_tau<P, SP>(sf, xx)) & 1)) {
+      if (tg < CF::MAXG && group_row<P, SP, CF::GZ, CF::B0, CF::B1, CF::NF2, CF::NF0>(zg, tg, sf, xx) &&
+          ((own >> dof_tau<P, SP>(sf, xx)) & 1)) {
         const int u[3] = {xx[0] - clo[0], xx[1] - clo[1], xx[2] - clo[2]};
         const int idx = sf == 0 ? fidx<SP, NB>(0, u) : (sf == 1 ? fidx<SP, NB>(1, u) : fidx<SP, NB>(2, u));
         const int64_t r = (int64_t)(__ldg(A.xvmap + bs * 3 * CF::NVF + sf * CF::NVF + idx) & 0x7fffffffu) - A.row_begin;
