@@ -22,6 +22,9 @@
 #include "lor_xdev.cuh"
 #include "lor_xframe.h"
 
+#ifndef XPFENCE
+#define XPFENCE 2  // persistent fill: corners per fence in the cell phase
+#endif
 #ifndef XMINB
 #define XMINB 5  // CTAs per SM of the one-chunk fill kernels (p <= 4): 96 registers
 #endif
@@ -323,7 +326,7 @@ __host__ __device__ constexpr bool first_touch(int q, int a, int b) {
   return true;
 }
 
-template <int XN, int XR, int XS>
+template <int XN, int XR, int XS, int FENCE = 1>
 __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, double a8, double b8, double *__restrict__ o) {
   auto X = [&](int v, int k) -> double { return XE[k * XN + pb + (v & 1) + XR * ((v >> 1) & 1) + XS * ((v >> 2) & 1)]; };
   // accumulate in the cell's (thread-private) shared-memory row: the first corner touching an
@@ -341,8 +344,9 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
   for (int q = 0; q < 8; ++q) {
     // corners are evaluated one after the other (the fence keeps the compiler from hoisting every
     // corner's loads and arithmetic at once: ~200 registers otherwise; caching the eight points in
-    // registers instead spills at 128); the corner re-reads its four points from shared memory
-    asm volatile("" ::: "memory");
+    // registers instead spills at 128); the corner re-reads its four points from shared memory.
+    // FENCE = 2: two corners in flight (more ILP where the register budget allows)
+    if (q % FENCE == 0) asm volatile("" ::: "memory");
     double j[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -616,6 +620,250 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
 #undef XSTAMP
 }
 
+// ============================================================================== persistent fill
+// One-chunk configurations (p <= 4): a persistent CTA walks the elements bs = blockIdx.x + k gridDim.x
+// and loads the NEXT element's prologue (extended restriction, gather list, own E-vector, neighbour
+// points) with cp.async into a second shared-memory buffer while it computes the current one -- the
+// prologue (a quarter of a CTA's lifetime as one-shot CTAs: 5.5 K of 21 K cycles, C2) leaves the
+// critical path.  The staging of the rows sits in the cell storage (values + uint16 box points;
+// the current buffer's restriction gives the column at write-out).  Same arithmetic and output
+// as k_xh1_fill.
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int P, int NB>
+struct XPCfg {
+  using CF = XCfg<P, NB>;
+  static constexpr int NPT = (P + 1) * (P + 1) * (P + 1);
+  static constexpr int HC = CF::NPB - NPT;
+  static constexpr int OFF_XG = (CF::XEB + 15) / 16 * 16, OFF_HL = (OFF_XG + CF::NPB * 4 + 15) / 16 * 16;
+  static constexpr int BUF = (OFF_HL + HC * 8 + 15) / 16 * 16;  // XE | XG | gather list
+  static constexpr int OFF_CM = 2 * BUF;
+  static constexpr int CMB = CF::NSL * CF::CP * 8;
+  static constexpr int OFF_MT = OFF_CM + CMB;
+  static constexpr int OFF_SO = OFF_MT + 8 * CF::MAXROW;
+  static constexpr int OFF_INV = OFF_SO + 4 * CF::MAXROW;
+  static constexpr int SMEM = OFF_INV + 128;
+  static_assert(CF::ONE, "persistent fill: one-chunk configurations");
+  static_assert(CF::MAXROW * 27 * 10 <= CMB, "staging (values + uint16 points) must fit in the cell storage");
+  static_assert(OFF_HL + HC * 8 <= BUF, "buffer layout");
+};
+
+template <int P, int NB, int MINB, bool WCOL>
+__global__ void __launch_bounds__(128, MINB) k_xh1_fill_pers(XFillArgs A) {
+  using CF = XCfg<P, NB>;
+  using PC = XPCfg<P, NB>;
+  constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1, PB = CF::PB, NPB = CF::NPB, LAY = CF::LAY, CP = CF::CP;
+  constexpr int HC = PC::HC;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_bad;
+  double *cm = reinterpret_cast<double *>(smem + PC::OFF_CM);
+  int64_t *m_out = reinterpret_cast<int64_t *>(smem + PC::OFF_MT);
+  int32_t *m_n = reinterpret_cast<int32_t *>(smem + PC::OFF_SO);
+  uint8_t *s_inv = smem + PC::OFF_INV;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto XEb = [&](int b) { return reinterpret_cast<double *>(smem + b * PC::BUF); };
+  auto XGb = [&](int b) { return reinterpret_cast<int32_t *>(smem + b * PC::BUF + PC::OFF_XG); };
+  auto HLb = [&](int b) { return reinterpret_cast<int2 *>(smem + b * PC::BUF + PC::OFF_HL); };
+  // stage A of element e into buffer b: restriction and gather list (addresses from e alone)
+  auto stage_a = [&](int64_t e, int b) {
+    const int32_t *xm = A.xmap + e * NPB;
+    int32_t *xg = XGb(b);
+    if constexpr (NPB % 4 == 0) {  // element rows 16-byte aligned
+      for (int i = tid; i < NPB / 4; i += 128) cp_async16(xg + 4 * i, xm + 4 * i);
+    } else {
+      for (int i = tid; i < NPB; i += 128) cp_async4(xg + i, xm + i);
+    }
+    const int2 *hl = A.xhalo + e * HC;
+    int2 *hs = HLb(b);
+    for (int h = tid; h < HC; h += 128) cp_async8(hs + h, hl + h);
+    cp_commit();
+  };
+  // stage B of element e into buffer b: own E-vector and neighbour points (needs the element id, the
+  // box corner and this thread's gather-list entries of stage A)
+  auto stage_b = [&](int64_t e_el, int4 hwx, int b) {
+    const int c0 = (int8_t)(hwx.y & 255), c1 = (int8_t)((hwx.y >> 8) & 255), c2 = (int8_t)((hwx.y >> 16) & 255);
+    double *xe = XEb(b);
+    const double *xs = A.X + e_el * A.xstride;
+    for (int rr = tid; rr < 3 * NP1 * NP1; rr += 128) {
+      const int d = rr / (NP1 * NP1), x12 = rr - d * NP1 * NP1, x1 = x12 % NP1, x2 = x12 / NP1;
+      const double *src = xs + d * NPT + x12 * NP1;
+      double *dst = xe + d * CF::XN + (x1 - c1) * CF::XR + (x2 - c2) * CF::XS - c0;
+#pragma unroll
+      for (int i = 0; i < NP1; ++i) cp_async8(dst + i, src + i);
+    }
+    const int2 *hs = HLb(b);
+    for (int h = tid; h < HC; h += 128) {
+      const int2 hv = hs[h];  // written by this thread's own stage-A copy (waited for by the caller)
+      if (hv.x >= 0) {
+        const int q = hv.y % PB + CF::XR * ((hv.y / PB) % PB) + CF::XS * (hv.y / (PB * PB));
+        cp_async8(xe + q, A.X + hv.x);
+        cp_async8(xe + CF::XN + q, A.X + hv.x + NPT);
+        cp_async8(xe + 2 * CF::XN + q, A.X + hv.x + 2 * NPT);
+      }
+    }
+    cp_commit();
+  };
+  const int64_t stride = gridDim.x;
+  int64_t bs = blockIdx.x;
+  if (bs >= A.nel_local) return;
+  if (tid == 0) s_bad = 0;
+  if (tid < NB * NB * NB) s_inv[tid] = A.cinv[tid];
+  int4 hw = __ldg(reinterpret_cast<const int4 *>(A.xe + bs));
+  int64_t el = __ldg(&A.xe[bs].el);
+  stage_a(bs, 0);
+  cp_wait_all();
+  stage_b(el, hw, 0);
+  const double alpha = A.alpha, beta = A.beta;
+  for (int b = 0; bs < A.nel_local; bs += stride, b ^= 1) {
+    cp_wait_all();
+    __syncthreads();  // buffer b holds element bs; the previous element's write-out is done
+    double *XE = XEb(b);
+    const int32_t *XG = XGb(b);
+    const int64_t nbs = bs + stride;
+    int4 hwn = make_int4(0, 0, 0, 0);
+    int64_t eln = 0;
+    if (nbs < A.nel_local) {
+      hwn = __ldg(reinterpret_cast<const int4 *>(A.xe + nbs));
+      eln = __ldg(&A.xe[nbs].el);
+      stage_a(nbs, b ^ 1);
+    }
+    const int clo0 = (int8_t)(hw.y & 255), clo1 = (int8_t)((hw.y >> 8) & 255), clo2 = (int8_t)((hw.y >> 16) & 255);
+    const int ex0 = (int8_t)((hw.y >> 24) & 255) - clo0 + 1, ex1 = (int8_t)(hw.z & 255) - clo1 + 1,
+              ex2 = (int8_t)((hw.z >> 8) & 255) - clo2 + 1;
+    const int olo0 = (int8_t)((hw.z >> 16) & 255), olo1 = (int8_t)((hw.z >> 24) & 255), olo2 = (int8_t)(hw.w & 255);
+    const int ohi0 = (int8_t)((hw.w >> 8) & 255), ohi1 = (int8_t)((hw.w >> 16) & 255), ohi2 = (int8_t)((hw.w >> 24) & 255);
+    const uint32_t own = (uint32_t)hw.x;
+    const int pbase = -(clo0 + PB * (clo1 + PB * clo2));
+    // ---- cells: the whole box, thread -> cell by the bank-conflict-free permutation
+    {
+      const double a8 = 0.125 * alpha, b8 = 0.125 * beta;
+      const int cc = (int)A.cperm[tid];
+      if (cc < NB * LAY) {
+        const int ux = cc % NB, uy = (cc / NB) % NB, uz = cc / LAY;
+        if (ux < ex0 && uy < ex1 && uz < ex2) {
+          if (!cell_h1v<CF::XN, CF::XR, CF::XS, XPFENCE>(XE, ux + CF::XR * uy + CF::XS * uz, a8, b8, cm + tid * CP))
+            s_bad = 1 + (clo0 + ux + 1) + (P + 2) * ((clo1 + uy + 1) + (P + 2) * (clo2 + uz + 1));
+        }
+      }
+    }
+    __syncthreads();
+    if (s_bad && tid == 0) {  // map the extended-frame cell to (element, cell) of the element it lies in
+      const int bb = s_bad - 1, q[3] = {bb % (P + 2) - 1, (bb / (P + 2)) % (P + 2) - 1, bb / ((P + 2) * (P + 2)) - 1};
+      const int ni = (q[0] < 0 ? 0 : (q[0] >= P ? 2 : 1)) + 3 * (q[1] < 0 ? 0 : (q[1] >= P ? 2 : 1)) +
+                     9 * (q[2] < 0 ? 0 : (q[2] >= P ? 2 : 1));
+      int64_t ee = el;
+      int kc[3] = {q[0], q[1], q[2]};
+      if (ni != 13) {
+        const XNbr nb = A.xe[bs].nbr[ni];
+        ee = nb.el;
+        int y0[3] = {q[0], q[1], q[2]}, y1[3] = {q[0] + 1, q[1] + 1, q[2] + 1}, L0[3], L1[3];
+        x_to_local(P, nb.code, y0, L0);
+        x_to_local(P, nb.code, y1, L1);
+        for (int a = 0; a < 3; ++a) kc[a] = L0[a] < L1[a] ? L0[a] : L1[a];
+      }
+      xreport(A.err, 2, A.elem_begin + ee, kc[0] + P * (kc[1] + P * kc[2]));
+      s_bad = 0;
+    }
+    // next element, stage B (its gather-list entries are this thread's own stage-A copies)
+    if (nbs < A.nel_local) {
+      cp_wait_all();
+      stage_b(eln, hwn, b ^ 1);
+    }
+    // ---- rows: one thread per owned row
+    const int rnx = ohi0 - olo0 + 1, rny = ohi1 - olo1 + 1;
+    const int nrow = rnx * rny * (ohi2 - olo2 + 1);
+    double acc[27];
+    uint32_t pw[8];
+    int px = 0, nrw = 0;
+    int64_t out = 0;
+    bool hasrow = false;
+    if (tid < nrow) {
+      const int t = tid / rnx;
+      const int x0 = olo0 + tid - t * rnx, x1 = olo1 + t % rny, x2 = olo2 + t / rny;
+      hasrow = (own >> (lcls(x0, P) + 3 * lcls(x1, P) + 9 * lcls(x2, P))) & 1;
+      if (hasrow) {
+        px = pbase + x0 + PB * (x1 + PB * x2);
+        const int64_t r = (int64_t)XG[px] - A.row_begin;
+        out = __ldg(A.row_ptr + r);
+        nrw = (int)(__ldg(A.row_ptr + r + 1) - out);
+        const uint4 *pp = reinterpret_cast<const uint4 *>(A.pos + r * 8);
+        const uint4 pa = __ldcs(pp), pv = __ldcs(pp + 1);
+        pw[0] = pa.x; pw[1] = pa.y; pw[2] = pa.z; pw[3] = pa.w;
+        pw[4] = pv.x; pw[5] = pv.y; pw[6] = pv.z; pw[7] = pv.w;
+#pragma unroll
+        for (int jj = 0; jj < 27; ++jj) acc[jj] = 0.0;
+        const int u0 = x0 - clo0, u1 = x1 - clo1, u2 = x2 - clo2;
+#pragma unroll
+        for (int o = 0; o < 8; ++o) {
+          const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+          const int cx = u0 - ox, cy = u1 - oy, cz = u2 - oz;
+          if (cx < 0 || cx >= ex0 || cy < 0 || cy >= ex1 || cz < 0 || cz >= ex2) continue;
+          const double *ce = cm + (int)s_inv[cz * LAY + cy * NB + cx] * CP;
+#pragma unroll
+          for (int jc = 0; jc < 8; ++jc) {
+            if (body_diag(o, jc)) continue;
+            const int dx = (jc & 1) - ox, dy = ((jc >> 1) & 1) - oy, dz = ((jc >> 2) & 1) - oz;
+            acc[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)] += ce[cidx(o, jc)];
+          }
+          asm volatile("" ::: "memory");
+        }
+      }
+    }
+    __syncthreads();  // every row has read the cells: stage over the cell storage
+    double *stage_v = cm;
+    uint16_t *stage_p = reinterpret_cast<uint16_t *>(cm + CF::MAXROW * 27);
+    if (hasrow) {
+      const int so = tid * 27;
+#pragma unroll
+      for (int jj = 0; jj < 27; ++jj) {
+        const int ps = (int)((pw[jj >> 2] >> (8 * (jj & 3))) & 255u);
+        if (ps != 255) {
+          stage_v[so + ps] = acc[jj];
+          stage_p[so + ps] = (uint16_t)(px + (jj % 3 - 1) + PB * ((jj / 3) % 3 - 1) + PB * PB * (jj / 9 - 1));
+        }
+      }
+    }
+    if (tid < CF::MAXROW) {
+      m_out[tid] = hasrow ? out : -1;
+      m_n[tid] = hasrow ? nrw : 0;
+    }
+    __syncthreads();
+    for (int t = warp; t < nrow; t += 8) {
+      const int t2 = t + 4;
+      const int64_t o = m_out[t], o2 = t2 < nrow ? m_out[t2] : -1;
+      const int n = m_n[t], n2 = t2 < nrow ? m_n[t2] : 0;
+      const bool w1 = o >= 0 && lane < n, w2 = o2 >= 0 && lane < n2;
+      int32_t c1 = 0, c2 = 0;
+      double v1 = 0.0, v2 = 0.0;
+      if (w1) { c1 = XG[stage_p[t * 27 + lane]]; v1 = stage_v[t * 27 + lane]; }
+      if (w2) { c2 = XG[stage_p[t2 * 27 + lane]]; v2 = stage_v[t2 * 27 + lane]; }
+      if (w1) {
+        if (WCOL) __stcs(A.col + o + lane, c1);
+        __stcs(A.val + o + lane, v1);
+      }
+      if (w2) {
+        if (WCOL) __stcs(A.col + o2 + lane, c2);
+        __stcs(A.val + o2 + lane, v2);
+      }
+    }
+    hw = hwn;
+    el = eln;
+  }
+}
+
 // ============================================================================== launchers
 // Proper edge colouring of the bipartite multigraph (L[i], R[i]) (classes < 16) with `colors`
 // colours (Koenig: possible when no class has more than `colors` edges), by alternating-path
@@ -667,34 +915,10 @@ static cudaError_t xh1_setup_p(const XSetupArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// thread -> cell permutation of the one-chunk / ring cell phases (cached per instantiation)
 template <int P, int NB>
-static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_out) {
+static void cell_perm(uint8_t *perm_out, uint8_t *inv_out) {
   using CF = XCfg<P, NB>;
-  constexpr int smem = CF::SMEM;
-  if (smem_out) { *smem_out = smem; return cudaSuccess; }
-  if (a.nel_local <= 0) return cudaSuccess;
-  constexpr int MINB = ((smem + 1024) * 5 <= 228 * 1024) ? XMINB : 3;  // 228 KB shared memory per SM
-  auto k = a.values_only ? k_xh1_fill<P, NB, MINB, false> : k_xh1_fill<P, NB, MINB, true>;
-  static bool attr = false;
-  if (!attr) {
-    for (auto kk : {k_xh1_fill<P, NB, MINB, false>, k_xh1_fill<P, NB, MINB, true>}) {
-      cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(kk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    }
-    attr = true;
-  }
-  // L2 prefetch distance = resident CTAs of the grid (cached per instantiation; LOR_XPF=0: off)
-  static int64_t resident = -1;
-  if (resident < 0) {
-    int dev = 0, nsm = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, smem);
-    const char *e = getenv("LOR_XPF");
-    resident = (e && !atoi(e)) ? 0 : (int64_t)nsm * occ;
-  }
-  XFillArgs b = a;
-  b.pf_dist = resident;
   // one chunk: thread -> cell permutation.  The 64-bit E-vector loads of a half-warp are conflict
   // free when its 16 cells have distinct (ux + XR uy + XS uz) mod 16: the i-th cell of every residue
   // class goes to half-warp i.  Used when every class has NB^3/16 rounded down or up members, so
@@ -747,8 +971,73 @@ static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_ou
     }
     pinit = true;
   }
-  memcpy(b.cperm, perm, 128);
-  memcpy(b.cinv, inv, 128);
+  memcpy(perm_out, perm, 128);
+  memcpy(inv_out, inv, 128);
+}
+
+template <int P, int NB>
+static cudaError_t xh1_fill_pers(const XFillArgs &a, cudaStream_t st) {
+  using PC = XPCfg<P, NB>;
+  constexpr int smem = PC::SMEM;
+  constexpr int MINB = (smem + 1024) * 4 <= 228 * 1024 ? 4 : 3;
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, nsm = 0, occ = 0;
+    for (auto k : {k_xh1_fill_pers<P, NB, MINB, false>, k_xh1_fill_pers<P, NB, MINB, true>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xh1_fill_pers<P, NB, MINB, true>, 128, smem);
+    grid = nsm * (occ > 0 ? occ : 1);
+  }
+  if (a.nel_local <= 0) return cudaSuccess;
+  XFillArgs b = a;
+  cell_perm<P, NB>(b.cperm, b.cinv);
+  const unsigned g = (unsigned)std::min<int64_t>(a.nel_local, grid);
+  if (a.values_only) k_xh1_fill_pers<P, NB, MINB, false><<<g, 128, smem, st>>>(b);
+  else k_xh1_fill_pers<P, NB, MINB, true><<<g, 128, smem, st>>>(b);
+  return cudaGetLastError();
+}
+
+template <int P, int NB>
+static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_out) {
+  using CF = XCfg<P, NB>;
+  constexpr int smem = CF::SMEM;
+  if (smem_out) { *smem_out = smem; return cudaSuccess; }
+  if (a.nel_local <= 0) return cudaSuccess;
+  constexpr int MINB = ((smem + 1024) * 5 <= 228 * 1024) ? XMINB : 3;  // 228 KB shared memory per SM
+  if constexpr (CF::ONE) {
+    static int pers = -1;
+    if (pers < 0) {
+      const char *e = getenv("LOR_XPERS");
+      pers = (e && !atoi(e)) ? 0 : 1;
+    }
+    if (pers) return xh1_fill_pers<P, NB>(a, st);
+  }
+  auto k = a.values_only ? k_xh1_fill<P, NB, MINB, false> : k_xh1_fill<P, NB, MINB, true>;
+  static bool attr = false;
+  if (!attr) {
+    for (auto kk : {k_xh1_fill<P, NB, MINB, false>, k_xh1_fill<P, NB, MINB, true>}) {
+      cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(kk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    attr = true;
+  }
+  // L2 prefetch distance = resident CTAs of the grid (cached per instantiation; LOR_XPF=0: off)
+  static int64_t resident = -1;
+  if (resident < 0) {
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, smem);
+    const char *e = getenv("LOR_XPF");
+    resident = (e && !atoi(e)) ? 0 : (int64_t)nsm * occ;
+  }
+  XFillArgs b = a;
+  b.pf_dist = resident;
+  cell_perm<P, NB>(b.cperm, b.cinv);
   k<<<(unsigned)a.nel_local, 128, smem, st>>>(b);
   return cudaGetLastError();
 }
