@@ -26,6 +26,10 @@
 #include "lor_xdev.cuh"
 #include "lor_xframe.h"
 
+#ifndef XV_ND_ONE_KB
+#define XV_ND_ONE_KB 80  // ND: all cell layers resident up to this size (p <= 4: 78 KB, 2 CTAs/SM)
+#endif
+
 namespace lorb {
 
 using namespace xdev;
@@ -55,7 +59,7 @@ struct XvCfg {
   static constexpr int NCP = LAY | 1;  // cells per entry plane (odd pitch)
   // all cell layers resident when they fit next to the rest (then every cell is computed in one
   // phase by all threads), else a ring of the two layers a row layer needs
-  static constexpr bool ONE = NB * NE * NCP * 8 <= 40 * 1024;
+  static constexpr bool ONE = NB * NE * NCP * 8 <= (SP == SP_ND ? XV_ND_ONE_KB : 40) * 1024;
   // rows processed per group of GZ z-layers: all of them at once for RT with resident cells (short
   // rows: per-layer barriers would dominate), one layer otherwise
   static constexpr int GZ = (ONE && SP == SP_RT) ? P + 1 : 1;
@@ -350,9 +354,14 @@ __global__ void __launch_bounds__(128) k_xv_sym(XvArgs A) {
   const int chi[3] = {(int8_t)((hw.y >> 24) & 255), (int8_t)(hw.z & 255), (int8_t)((hw.z >> 8) & 255)};
   const uint32_t own = (uint32_t)hw.x;
   __syncthreads();
-  for (int i = tid; i < (P + 1) * CF::MAXR; i += 128) {
+  // all rows of the element in family-major warp-aligned segments (no divergence between the
+  // families' unrolled code paths within a warp)
+  constexpr int NRF2 = CF::NRF2, NRF0 = CF::NRF0;
+  constexpr int NF2 = (P + 1) * NRF2, NF0 = (P + 1) * NRF0;
+  constexpr int B0 = (NF2 + 31) / 32 * 32, B1 = B0 + (NF0 + 31) / 32 * 32, NT = B1 + NF0;
+  for (int i = tid; i < NT; i += 128) {
     int s, x[3];
-    if (!layer_row<P, SP>(i / CF::MAXR, i % CF::MAXR, s, x)) continue;
+    if (!group_row<P, SP, P + 1, B0, B1, NF2, NF0>(0, i, s, x)) continue;
     if (!((own >> dof_tau<P, SP>(s, x)) & 1)) continue;
     if (s == 0) sym_row<P, NB, SP, 0>(A, x, clo, chi, XV, s_pos + tid * 36);
     else if (s == 1) sym_row<P, NB, SP, 1>(A, x, clo, chi, XV, s_pos + tid * 36);
@@ -720,7 +729,7 @@ static cudaError_t fill_nb(const XvArgs &a, cudaStream_t st) {
     constexpr int smem = CF::SMEM;
     // CTAs per SM the shared memory allows (at most 5: >= 96 registers per thread)
     constexpr int MINB = (smem + 1024) * 5 <= 228 * 1024 ? 5 : ((smem + 1024) * 4 <= 228 * 1024 ? 4 :
-                         ((smem + 1024) * 4 <= 228 * 1024 ? 4 : ((smem + 1024) * 3 <= 228 * 1024 ? 3 : 1)));
+                         ((smem + 1024) * 3 <= 228 * 1024 ? 3 : ((smem + 1024) * 2 <= 228 * 1024 ? 2 : 1)));
     static bool attr = false;
     if (!attr) {
       for (auto k : {k_xv_fill<P, NB, SP, MINB, false>, k_xv_fill<P, NB, SP, MINB, true>}) {
