@@ -192,6 +192,80 @@ lor_status lor_xframe_dry_run(const lor_setup_args *args, int64_t *info, int64_t
  * (0 on error / cap too small). */
 int64_t lor_debug_dump(lor_ctx ctx, int what, lor_space space, void *host_out, int64_t cap_bytes);
 
+/* ---- Steps A3 (layout) and A4 after the local assembly --------------------
+ * hypre-style parallel CSR of an assembled operator ("Each rank has a diagonal
+ * block, which contains the nonzeros for which both the row and column indices are owned by
+ * itself, and an off-diagonal block, which contains the nonzeros for which the column indices are
+ * owned by another rank").  Rows: this rank's owned rows.  diag: int32 column ids LOCAL to the
+ * rank's column range; for the square operators (H1, ND, RT) the diagonal entry comes first in
+ * every row and the others follow in ascending order (hypre's ParCSR convention, DESIGN.md reading
+ * P-26); for G and C all ascending.  offd: int32 indices into col_map_offd, which lists the
+ * distinct off-rank global columns in ascending order (int64).  All DEVICE, caller-owned. */
+typedef struct {
+  int64_t *diag_row_ptr; /* [n_rows_local + 1] */
+  int32_t *diag_col;
+  double *diag_val;
+  int64_t cap_diag;      /* capacity of diag_col / diag_val (entries)                           */
+  int64_t *offd_row_ptr; /* [n_rows_local + 1] */
+  int32_t *offd_col;
+  double *offd_val;
+  int64_t cap_offd;
+  int64_t *col_map_offd;
+  int64_t cap_col_map;
+} lor_parcsr;
+
+/* Operators for lor_parcsr_*: 0 = H1, 1 = ND, 2 = RT (the matrices of lor_assemble_*), 3 = discrete
+ * gradient (rows ND, columns H1), 4 = discrete curl (rows RT, columns ND). */
+enum { LOR_OP_H1 = 0, LOR_OP_ND = 1, LOR_OP_RT = 2, LOR_OP_GRAD = 3, LOR_OP_CURL = 4 };
+
+/* Symbolic part of the split of the assembled operator A (row_ptr / col as written by the
+ * assembly call, DEVICE): per-row diag / offd counts and their scans, the off-rank column set and,
+ * for square operators on several ranks, the marker-exchange plan of lor_eliminate_bc.
+ * SYNCHRONOUS (waits on the context stream); returns the sizes the caller allocates.  Errors:
+ * UNSUPPORTED (operator not available, nranks > 32), INVALID_ARGUMENT (a square operator's row
+ * lacks its diagonal), OUT_OF_MEMORY, CUDA.  The workspaces stay in the context for _fill and
+ * lor_eliminate_bc of the same operator. */
+lor_status lor_parcsr_prepare(lor_ctx ctx, int op, const lor_csr *A, int64_t *nnz_diag, int64_t *nnz_offd,
+                              int64_t *n_col_offd);
+/* Numeric part: copies A's values into the diag / offd blocks (enqueued on the context stream).
+ * A must hold the same pattern as at lor_parcsr_prepare.  BUFFER_TOO_SMALL if a capacity is below
+ * the prepared size (nothing written). */
+lor_status lor_parcsr_fill(lor_ctx ctx, int op, const lor_csr *A, lor_parcsr *out);
+
+/* The owned essential dofs of a trace condition on the whole domain boundary: local rows
+ * (ascending) of the dofs of every coarse entity on a boundary facet (a face -- an edge in 2D --
+ * of exactly one element): H1 all trace dofs, ND tangential edge dofs, RT normal face dofs
+ * ("rows and columns corresponding to each essential degree of freedom").
+ * *n = count; rows = DEVICE int32[cap] or NULL (count only); BUFFER_TOO_SMALL if cap < *n. */
+lor_status lor_boundary_dofs(lor_ctx ctx, lor_space space, int32_t *rows, int64_t cap, int64_t *n);
+
+/* Step A4, elimination of essential boundary conditions on the ParCSR M of
+ * operator `space` (filled by lor_parcsr_fill): for every essential dof j (ess = DEVICE int32 local
+ * rows of this rank, duplicates allowed) row j becomes the unit row (diagonal 1, every other stored
+ * entry 0 in diag and offd) and column j becomes 0 in every other row of every rank; the pattern is
+ * kept (explicit zeros).  On several ranks the markers of the owned essential dofs are sent to the
+ * ranks whose offd blocks hold those columns (grouped ncclSend/ncclRecv on a side stream, started
+ * before the diag / offd-row elimination and overlapped with it, l.383-386), then the offd columns
+ * are zeroed from the received markers (l.386-387).  Collective over the ranks (NCCL mode).  In
+ * LOR_EXCHANGE_MANUAL mode the call stops before the offd columns: the caller moves the markers
+ * with lor_bc_exchange_copy(dst, src, space) for every pair and completes with
+ * lor_eliminate_bc_finish.  ess entries outside [0, n_rows_local) are skipped and reported by the
+ * next lor_sync as INVALID_ARGUMENT. */
+lor_status lor_eliminate_bc(lor_ctx ctx, lor_space space, const int32_t *ess, int64_t n_ess, lor_parcsr *M);
+lor_status lor_bc_exchange_copy(lor_ctx dst, lor_ctx src, lor_space space);
+lor_status lor_eliminate_bc_finish(lor_ctx ctx, lor_space space, lor_parcsr *M);
+/* Marker-exchange plan of a prepared square operator: per peer, markers sent / received
+ * (host arrays [nranks], NULL allowed).  The plan is symmetric by construction; tests check
+ * send_counts[q] on rank r == recv_counts[r] on rank q. */
+lor_status lor_parcsr_exchange_counts(lor_ctx ctx, lor_space space, int64_t *send_counts, int64_t *recv_counts);
+
+/* LOR mesh vertex coordinate vectors for AMS / ADS: the
+ * coordinates of every owned H1 dof (= LOR vertex) deduplicated from the coordinate E-vector through
+ * the element restriction, one thread per deduplicated dof, no communication.  xyz = DEVICE
+ * double[dim][n_rows_local(H1)] (x of all owned vertices, then y, then z -- hypre's separate
+ * coordinate vectors), caller-owned; enqueued on the context stream.  Bit-exact copies. */
+lor_status lor_coordinates(lor_ctx ctx, double *xyz);
+
 /* Rank 0 creates the NCCL unique id (128 bytes) that the caller broadcasts to all ranks. */
 lor_status lor_nccl_get_unique_id(void *out128);
 

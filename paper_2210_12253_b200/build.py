@@ -65,21 +65,31 @@ def _gen_units(plist):
     return units
 
 
-def _headers_hash() -> str:
+def _deps(path, seen=None) -> list:
+    """Local headers a translation unit includes (transitively), from its #include "..." lines."""
+    import re
+    seen = set() if seen is None else seen
+    for inc in re.findall(r'#include\s+"([^"]+)"', open(path).read()):
+        cand = os.path.normpath(os.path.join(os.path.dirname(path), inc))
+        if not os.path.exists(cand):
+            cand = os.path.join(CSRC, os.path.basename(inc))
+        if os.path.exists(cand) and cand not in seen:
+            seen.add(cand)
+            _deps(cand, seen)
+    return sorted(seen)
+
+
+def _unit_key(src) -> str:
     h = hashlib.sha256()
-    for name in sorted(os.listdir(CSRC)):
-        if name.endswith((".cuh", ".h")):
-            with open(os.path.join(CSRC, name), "rb") as f:
-                h.update(name.encode() + f.read())
-    with open(os.path.join(ROOT, "include", "lor.h"), "rb") as f:
-        h.update(f.read())
+    for name in [src] + _deps(src):
+        with open(name, "rb") as f:
+            h.update(os.path.basename(name).encode() + f.read())
     h.update(" ".join(FLAGS + ARCH).encode())
-    return h.hexdigest()
+    return h.hexdigest()[:16]
 
 
-def _compile(src, obj, hkey, extra=()):
-    with open(src, "rb") as f:
-        key = hashlib.sha256(f.read() + hkey.encode()).hexdigest()[:16]
+def _compile(src, obj, extra=()):
+    key = _unit_key(src)
     kfile = obj + ".key"
     if os.path.exists(obj) and os.path.exists(kfile) and open(kfile).read() == key:
         return obj, False
@@ -100,6 +110,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
         return LIB
     units = _gen_units(plist)
     jobs = [(os.path.join(CSRC, "lor_kernels.cu"), os.path.join(BUILD, "lor_kernels.o")),
+            (os.path.join(CSRC, "lor_parcsr.cu"), os.path.join(BUILD, "lor_parcsr.o")),
             (os.path.join(CSRC, "lor_capi.cu"), os.path.join(BUILD, "lor_capi.o")),
             (os.path.join(CSRC, "lor_plan.cpp"), os.path.join(BUILD, "lor_plan.o")),
             (os.path.join(CSRC, "lor_xframe.cpp"), os.path.join(BUILD, "lor_xframe.o")),
@@ -113,9 +124,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
     nw = max(1, min(len(jobs), os.cpu_count() or 4))
     if verbose:
         print(f"[lor build] {len(jobs)} translation units on {nw} workers (p in {plist})", flush=True)
-    hkey = _headers_hash()
     with cf.ThreadPoolExecutor(nw) as ex:
-        futs = [ex.submit(_compile, s, o, hkey) for s, o in jobs]
+        futs = [ex.submit(_compile, s, o) for s, o in jobs]
         res = [f.result() for f in futs]
     objs = [o for o, _ in res]
     if verbose:

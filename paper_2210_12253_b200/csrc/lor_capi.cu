@@ -15,6 +15,7 @@
 #include "../../include/lor.h"
 #include "lor_internal.h"
 #include "lor_kernels.h"
+#include "lor_parcsr.h"
 #include "lor_plan.h"
 #include "lor_xframe.h"
 
@@ -109,6 +110,32 @@ struct SpaceDev {
   uint32_t *xvpos = nullptr;
   int64_t n_tr = 0;             // entries of the dof transpose (local elements x owned local dofs)
   int32_t *trmap = nullptr;     // element restriction workspace of lor_dof_transpose (nranks > 1)
+  std::vector<int64_t> rank_off;  // [nranks+1] row ranges of the ranks (column ownership)
+  int64_t *droff = nullptr;       // device copy
+  std::vector<int32_t> bnd;       // owned boundary rows (local, ascending; lor_boundary_dofs)
+};
+
+// ParCSR split (A3 layout) and essential-BC elimination (A4, l.376-388) of one
+// operator (H1, ND, RT, discrete gradient, discrete curl): workspaces of lor_parcsr_prepare, reused
+// by lor_parcsr_fill and lor_eliminate_bc.
+struct PcState {
+  bool ready = false;
+  int64_t n = 0, cb = 0, ce = 0, row_begin = 0, ncols = 0, nw = 0;
+  int64_t nnz_d = 0, nnz_o = 0, n_col_offd = 0;
+  int square = 0;
+  const int64_t *croff = nullptr;
+  uint32_t *bitmap = nullptr, *rowmask = nullptr;
+  int32_t *pc = nullptr, *cnt_d = nullptr, *cnt_o = nullptr, *flag = nullptr;
+  int64_t *wpre = nullptr, *drp = nullptr, *orp = nullptr, *pos = nullptr;
+  unsigned long long *status = nullptr;
+  unsigned int *tile_ctr = nullptr;
+  // marker exchange (square operators): rows whose markers each peer needs (ascending local rows,
+  // peer-major), and each peer's segment of col_map_offd (ascending: the same order on both sides)
+  std::vector<int64_t> send_off, send_cnt, recv_lo;
+  int32_t *send_list = nullptr;
+  uint8_t *marker = nullptr, *sbuf = nullptr, *omark = nullptr;
+  int64_t cap_send = 0, cap_send_b = 0, cap_omark = 0;
+  int pending = 0;  // manual mode: offd columns wait for lor_eliminate_bc_finish
 };
 
 }  // namespace
@@ -141,6 +168,9 @@ struct lor_ctx_s {
   int fin_smem = 0;
   int dbg = 0;  // LOR_DBG at setup (dev experiments; 0 in production)
   std::vector<void *> allocs;
+  PcState pc[5];                     // lor_parcsr_* / lor_eliminate_bc per operator
+  cudaStream_t side = nullptr;       // marker exchange stream (overlap)
+  cudaEvent_t ev_pack = nullptr, ev_xchg = nullptr;
 };
 
 namespace {
@@ -793,6 +823,9 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     S.recv_count = P.recv_count;
     S.send_begin = P.send_begin;
     S.send_count = P.send_count;
+    S.rank_off = P.rank_off;
+    if (dev_upload(c, &S.droff, P.rank_off.data(), P.rank_off.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "rank_off");
+    plan.boundary_rows(s, S.bnd);
     int smem = 0;
     AsmArgs dummy{};
     launch_assemble(A.dim, s, A.p, 0, dummy, c->stream, &smem);
@@ -1065,6 +1098,9 @@ lor_status lor_destroy(lor_ctx c) {
   if (!c) return LOR_OK;
   cudaSetDevice(c->device);
   if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_xchg) cudaEventDestroy(c->ev_xchg);
   for (void *p : c->allocs) cudaFree(p);
   for (int i = 0; i < 8; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
@@ -1078,6 +1114,10 @@ lor_status lor_sync(lor_ctx c) {
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   int err[4];
   CUDA_TRY(c, cudaMemcpy(err, c->err, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err[3]) {
+    cudaMemset(c->err, 0, sizeof(err));
+    return fail(c, LOR_ERR_INVALID_ARGUMENT, "lor_eliminate_bc: essential dof outside [0, n_rows_local)");
+  }
   if (err[0]) {
     cudaMemset(c->err, 0, sizeof(err));
     char buf[160];
@@ -1288,6 +1328,25 @@ lor_status lor_dof_transpose(lor_ctx c, lor_space space, int64_t *offsets, int32
   return LOR_OK;
 }
 
+lor_status lor_coordinates(lor_ctx c, double *xyz) {
+  if (!c || !xyz) return LOR_ERR_INVALID_ARGUMENT;
+  const SpaceDev &S = c->sp[SP_H1];
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CoordArgs a;
+  a.p = c->p;
+  a.nel_local = c->nel_local;
+  a.topo = c->topo;
+  fill_base(S, a.base);
+  a.X = c->X;
+  a.xstride = c->xstride;
+  a.row_begin = S.row_begin;
+  a.n_local = S.n_local;
+  a.out = xyz;
+  CUDA_TRY(c, launch_coords(c->dim, a, c->stream));
+  if (c->nel_local > 0) c->launches++;
+  return LOR_OK;
+}
+
 lor_status lor_query_elements(lor_ctx c, int64_t *elem_begin, int64_t *n_elem_local, int *nh1, int *nnd, int *nrt) {
   if (!c) return LOR_ERR_INVALID_ARGUMENT;
   if (elem_begin) *elem_begin = c->elem_begin;
@@ -1330,6 +1389,282 @@ int lor_last_phase_ms(lor_ctx c, float *ms, int cap) {
     ms[n++] = t;
   }
   return n;
+}
+
+}  // extern "C"
+// ------------------------------------------------------------------ ParCSR split + BC elimination
+namespace {
+
+// rows / columns of operator op: 0..2 the space's matrix (square), 3 discrete gradient (ND x H1),
+// 4 discrete curl (RT x ND)
+bool op_spaces(lor_ctx c, int op, int &rs, int &cs) {
+  if (op >= 0 && op <= 2) { rs = cs = op; }
+  else if (op == 3) { rs = SP_ND; cs = SP_H1; }
+  else if (op == 4) { rs = SP_RT; cs = SP_ND; }
+  else return false;
+  return c->sp[rs].valid && c->sp[cs].valid && (op <= 2 || c->dim == 3);
+}
+
+template <class T>
+cudaError_t grow(lor_ctx c, T **p, int64_t &cap, int64_t need) {
+  if (*p && cap >= need) return cudaSuccess;
+  if (*p) {
+    c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void *)*p));
+    cudaFree(*p);
+    *p = nullptr;
+  }
+  cap = std::max<int64_t>(need, 1);
+  cudaError_t e = cudaMalloc((void **)p, sizeof(T) * cap);
+  if (e == cudaSuccess) c->allocs.push_back(*p);
+  return e;
+}
+
+lor_status side_stream(lor_ctx c) {
+  if (c->side) return LOR_OK;
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_xchg, cudaEventDisableTiming));
+  return LOR_OK;
+}
+
+PcArgs pc_args(lor_ctx c, PcState &P, const lor_csr *A) {
+  PcArgs a{};
+  a.n = P.n;
+  a.rp = A->row_ptr;
+  a.col = A->col;
+  a.val = A->val;
+  a.cb = P.cb;
+  a.ce = P.ce;
+  a.row_begin = P.row_begin;
+  a.square = P.square;
+  a.croff = P.croff;
+  a.nranks = c->nranks;
+  a.ncols = P.ncols;
+  a.bitmap = P.bitmap;
+  a.wpre = P.wpre;
+  a.cnt_d = P.cnt_d;
+  a.cnt_o = P.cnt_o;
+  a.rowmask = P.rowmask;
+  a.err = c->err + 3;
+  return a;
+}
+
+}  // namespace
+extern "C" {
+
+lor_status lor_parcsr_prepare(lor_ctx c, int op, const lor_csr *A, int64_t *nnz_diag, int64_t *nnz_offd,
+                              int64_t *n_col_offd) {
+  int rs, cs;
+  if (!c || !A || !A->row_ptr) return LOR_ERR_INVALID_ARGUMENT;
+  if (!op_spaces(c, op, rs, cs)) return fail(c, LOR_ERR_UNSUPPORTED, "operator not available for this mesh");
+  if (c->nranks > 32) return fail(c, LOR_ERR_UNSUPPORTED, "ParCSR split: nranks > 32");
+  const SpaceDev &R = c->sp[rs], &C = c->sp[cs];
+  PcState &P = c->pc[op];
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  P.ready = false;
+  P.pending = 0;
+  P.n = R.n_local;
+  P.row_begin = R.row_begin;
+  P.cb = C.row_begin;
+  P.ce = C.row_begin + C.n_local;
+  P.square = op <= 2;
+  P.croff = C.droff;
+  P.ncols = C.n_global;
+  P.nw = (C.n_global + 31) / 32;
+  const int64_t n1 = P.n + 1;
+  if (!P.bitmap) {  // sizes are topological: allocated once per operator
+    if (dev_alloc(c, &P.bitmap, P.nw + 1) || dev_alloc(c, &P.rowmask, n1) || dev_alloc(c, &P.cnt_d, n1) ||
+        dev_alloc(c, &P.cnt_o, n1) || dev_alloc(c, &P.flag, n1) || dev_alloc(c, &P.pc, P.nw + 1) ||
+        dev_alloc(c, &P.wpre, P.nw + 2) || dev_alloc(c, &P.drp, n1) || dev_alloc(c, &P.orp, n1) ||
+        dev_alloc(c, &P.pos, std::max(n1, P.nw + 2)) ||
+        dev_alloc(c, &P.status, scan_status_words(std::max(P.n, P.nw))) || dev_alloc(c, &P.tile_ctr, 1) ||
+        (P.square && dev_alloc(c, &P.marker, n1)))
+      return fail(c, LOR_ERR_OUT_OF_MEMORY, "parcsr workspace");
+  }
+  CUDA_TRY(c, cudaMemsetAsync(P.bitmap, 0, sizeof(uint32_t) * (P.nw + 1), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->err + 3, 0, sizeof(int), c->stream));
+  PcArgs a = pc_args(c, P, A);
+  CUDA_TRY(c, launch_pc_count(a, c->stream));
+  CUDA_TRY(c, launch_scan(P.cnt_d, P.drp, P.n, P.status, P.tile_ctr, c->stream));
+  CUDA_TRY(c, launch_scan(P.cnt_o, P.orp, P.n, P.status, P.tile_ctr, c->stream));
+  CUDA_TRY(c, launch_pc_popc(P.bitmap, P.nw, P.pc, c->stream));
+  CUDA_TRY(c, launch_scan(P.pc, P.wpre, P.nw, P.status, P.tile_ctr, c->stream));
+  c->launches += 5;
+  int64_t tot[3] = {0, 0, 0};
+  CUDA_TRY(c, cudaMemcpyAsync(&tot[0], P.drp + P.n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&tot[1], P.orp + P.n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&tot[2], P.wpre + P.nw, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  int bad = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&bad, c->err + 3, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (bad == 1) return fail(c, LOR_ERR_INVALID_ARGUMENT, "ParCSR split: a row of a square operator lacks its diagonal");
+  if (bad) return fail(c, LOR_ERR_INVALID_ARGUMENT, "ParCSR split: column id outside [0, n_cols_global)");
+  P.nnz_d = tot[0];
+  P.nnz_o = tot[1];
+  P.n_col_offd = tot[2];
+  // marker exchange plan (square operators on several ranks): peer q's segment of col_map_offd and
+  // the owned rows whose offd columns q owns -- by structural symmetry exactly the rows q's
+  // col_map_offd holds from this rank, in the same (ascending) order
+  P.send_off.assign(c->nranks + 1, 0);
+  P.send_cnt.assign(c->nranks, 0);
+  P.recv_lo.assign(c->nranks + 1, 0);
+  if (P.square && c->nranks > 1) {
+    CUDA_TRY(c, launch_pc_peer_lo(P.bitmap, P.wpre, P.nw, P.croff, c->nranks, P.pos, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(P.recv_lo.data(), P.pos, sizeof(int64_t) * (c->nranks + 1), cudaMemcpyDeviceToHost,
+                                c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (int pass = 0; pass < 2; ++pass) {  // 0: counts per peer, 1: the lists
+      for (int q = 0; q < c->nranks; ++q) {
+        if (q == c->rank) continue;
+        CUDA_TRY(c, launch_pc_flag(P.rowmask, P.n, q, P.flag, c->stream));
+        CUDA_TRY(c, launch_scan(P.flag, P.pos, P.n, P.status, P.tile_ctr, c->stream));
+        c->launches += 2;
+        if (pass == 0) {
+          CUDA_TRY(c, cudaMemcpyAsync(&P.send_cnt[q], P.pos + P.n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+        } else if (P.send_cnt[q] > 0) {
+          CUDA_TRY(c, launch_pc_scatter(P.rowmask, P.pos, P.n, q, P.send_list + P.send_off[q], c->stream));
+          c->launches++;
+        }
+      }
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      if (pass == 0) {
+        for (int q = 0; q < c->nranks; ++q) P.send_off[q + 1] = P.send_off[q] + P.send_cnt[q];
+        if (P.send_off[c->nranks] > P.cap_send) {
+          if (grow(c, &P.send_list, P.cap_send, P.send_off[c->nranks]) ||
+              grow(c, &P.sbuf, P.cap_send_b, P.send_off[c->nranks]))
+            return fail(c, LOR_ERR_OUT_OF_MEMORY, "parcsr send lists");
+        }
+      }
+    }
+  }
+  if (P.square && grow(c, &P.omark, P.cap_omark, P.n_col_offd + 1)) return fail(c, LOR_ERR_OUT_OF_MEMORY, "parcsr markers");
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  P.ready = true;
+  if (nnz_diag) *nnz_diag = P.nnz_d;
+  if (nnz_offd) *nnz_offd = P.nnz_o;
+  if (n_col_offd) *n_col_offd = P.n_col_offd;
+  return LOR_OK;
+}
+
+lor_status lor_parcsr_fill(lor_ctx c, int op, const lor_csr *A, lor_parcsr *M) {
+  int rs, cs;
+  if (!c || !A || !M || !A->row_ptr) return LOR_ERR_INVALID_ARGUMENT;
+  if (!op_spaces(c, op, rs, cs)) return fail(c, LOR_ERR_UNSUPPORTED, "operator not available for this mesh");
+  PcState &P = c->pc[op];
+  if (!P.ready) return fail(c, LOR_ERR_INVALID_ARGUMENT, "lor_parcsr_fill before lor_parcsr_prepare");
+  if (!M->diag_row_ptr || !M->offd_row_ptr || (P.nnz_d > 0 && (!M->diag_col || !M->diag_val)) ||
+      (P.nnz_o > 0 && (!M->offd_col || !M->offd_val)) || (P.n_col_offd > 0 && !M->col_map_offd))
+    return fail(c, LOR_ERR_INVALID_ARGUMENT, "null ParCSR buffer");
+  if (M->cap_diag < P.nnz_d || M->cap_offd < P.nnz_o || M->cap_col_map < P.n_col_offd)
+    return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "ParCSR buffers smaller than lor_parcsr_prepare's sizes");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpyAsync(M->diag_row_ptr, P.drp, sizeof(int64_t) * (P.n + 1), cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(M->offd_row_ptr, P.orp, sizeof(int64_t) * (P.n + 1), cudaMemcpyDeviceToDevice, c->stream));
+  PcArgs a = pc_args(c, P, A);
+  PcOut o{P.drp, P.orp, M->diag_col, M->offd_col, M->diag_val, M->offd_val};
+  CUDA_TRY(c, launch_pc_fill(a, o, P.nnz_o > 0, c->stream));
+  c->launches += P.nnz_o > 0 ? 2 : 1;
+  if (P.n_col_offd > 0) {
+    CUDA_TRY(c, launch_pc_colmap(P.bitmap, P.wpre, P.nw, M->col_map_offd, c->stream));
+    c->launches++;
+  }
+  return LOR_OK;
+}
+
+lor_status lor_boundary_dofs(lor_ctx c, lor_space space, int32_t *rows, int64_t cap, int64_t *n) {
+  if (!c || space < 0 || space > 2 || !n) return LOR_ERR_INVALID_ARGUMENT;
+  const SpaceDev &S = c->sp[space];
+  if (!S.valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
+  *n = (int64_t)S.bnd.size();
+  if (!rows) return LOR_OK;
+  if (cap < *n) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap < number of boundary dofs");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (*n > 0) CUDA_TRY(c, cudaMemcpy(rows, S.bnd.data(), sizeof(int32_t) * *n, cudaMemcpyHostToDevice));
+  return LOR_OK;
+}
+
+lor_status lor_eliminate_bc(lor_ctx c, lor_space space, const int32_t *ess, int64_t n_ess, lor_parcsr *M) {
+  if (!c || space < 0 || space > 2 || !M || (n_ess > 0 && !ess) || n_ess < 0) return LOR_ERR_INVALID_ARGUMENT;
+  PcState &P = c->pc[space];
+  if (!P.ready) return fail(c, LOR_ERR_INVALID_ARGUMENT, "lor_eliminate_bc before lor_parcsr_prepare/fill");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemsetAsync(P.marker, 0, P.n + 1, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->err + 3, 0, sizeof(int), c->stream));
+  CUDA_TRY(c, launch_bc_mark(ess, n_ess, P.n, P.marker, c->err + 3, c->stream));
+  c->launches++;
+  const int64_t nsend = P.send_off.empty() ? 0 : P.send_off[c->nranks];
+  const bool remote = c->nranks > 1 && P.n_col_offd > 0;
+  if (c->nranks > 1) {
+    CUDA_TRY(c, launch_bc_pack(P.marker, P.send_list, nsend, P.sbuf, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(P.omark, 0, P.n_col_offd + 1, c->stream));
+    if (nsend > 0) c->launches++;
+  }
+  const bool use_nccl = c->nranks > 1 && c->exchange_mode == 0;
+  if (use_nccl) {  // the marker exchange starts first and overlaps the diag / offd-row elimination
+    lor_status st = side_stream(c);
+    if (st) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev_pack, c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_pack, 0));
+    if (g_nccl.GroupStart() != ncclSuccess) return fail(c, LOR_ERR_NCCL, "ncclGroupStart");
+    for (int q = 0; q < c->nranks; ++q) {
+      if (q == c->rank) continue;
+      ncclResult_t r = ncclSuccess;
+      if (P.send_cnt[q] > 0)
+        r = g_nccl.Send(P.sbuf + P.send_off[q], P.send_cnt[q], ncclUint8, q, c->comm, c->side);
+      if (r == ncclSuccess && P.recv_lo[q + 1] > P.recv_lo[q])
+        r = g_nccl.Recv(P.omark + P.recv_lo[q], P.recv_lo[q + 1] - P.recv_lo[q], ncclUint8, q, c->comm, c->side);
+      if (r != ncclSuccess) { g_nccl.GroupEnd(); return fail(c, LOR_ERR_NCCL, g_nccl.GetErrorString(r)); }
+    }
+    if (g_nccl.GroupEnd() != ncclSuccess) return fail(c, LOR_ERR_NCCL, "ncclGroupEnd");
+    CUDA_TRY(c, cudaEventRecord(c->ev_xchg, c->side));
+  }
+  BcArgs b{P.n, M->diag_row_ptr, M->offd_row_ptr, M->diag_col, M->diag_val, M->offd_val};
+  CUDA_TRY(c, launch_bc_rows(ess, n_ess, b, c->stream));
+  if (n_ess > 0) c->launches++;
+  if (!remote) return LOR_OK;
+  if (!use_nccl) {
+    P.pending = 1;
+    return LOR_OK;
+  }
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_xchg, 0));
+  CUDA_TRY(c, launch_bc_offd_cols(M->offd_col, P.nnz_o, P.omark, M->offd_val, c->stream));
+  if (P.nnz_o > 0) c->launches++;
+  return LOR_OK;
+}
+
+lor_status lor_bc_exchange_copy(lor_ctx dst, lor_ctx src, lor_space space) {
+  if (!dst || !src || space < 0 || space > 2) return LOR_ERR_INVALID_ARGUMENT;
+  PcState &D = dst->pc[space], &S = src->pc[space];
+  if (!D.ready || !S.ready) return fail(dst, LOR_ERR_INVALID_ARGUMENT, "ParCSR not prepared");
+  const int q = src->rank, r = dst->rank;
+  const int64_t want = D.recv_lo[q + 1] - D.recv_lo[q];
+  if (want != S.send_cnt[r]) return fail(dst, LOR_ERR_INVALID_ARGUMENT, "marker exchange plan mismatch");
+  if (want == 0) return LOR_OK;
+  CUDA_TRY(dst, cudaStreamSynchronize(src->stream));
+  CUDA_TRY(dst, cudaMemcpyAsync(D.omark + D.recv_lo[q], S.sbuf + S.send_off[r], want, cudaMemcpyDeviceToDevice,
+                                dst->stream));
+  return LOR_OK;
+}
+
+lor_status lor_eliminate_bc_finish(lor_ctx c, lor_space space, lor_parcsr *M) {
+  if (!c || space < 0 || space > 2 || !M) return LOR_ERR_INVALID_ARGUMENT;
+  PcState &P = c->pc[space];
+  if (!P.pending) return LOR_OK;
+  P.pending = 0;
+  CUDA_TRY(c, launch_bc_offd_cols(M->offd_col, P.nnz_o, P.omark, M->offd_val, c->stream));
+  if (P.nnz_o > 0) c->launches++;
+  return LOR_OK;
+}
+
+lor_status lor_parcsr_exchange_counts(lor_ctx c, lor_space space, int64_t *send_counts, int64_t *recv_counts) {
+  if (!c || space < 0 || space > 2) return LOR_ERR_INVALID_ARGUMENT;
+  const PcState &P = c->pc[space];
+  if (!P.ready) return fail(c, LOR_ERR_INVALID_ARGUMENT, "ParCSR not prepared");
+  for (int q = 0; q < c->nranks; ++q) {
+    if (send_counts) send_counts[q] = P.send_cnt.empty() ? 0 : P.send_cnt[q];
+    if (recv_counts) recv_counts[q] = P.recv_lo.empty() ? 0 : P.recv_lo[q + 1] - P.recv_lo[q];
+  }
+  return LOR_OK;
 }
 
 }  // extern "C"

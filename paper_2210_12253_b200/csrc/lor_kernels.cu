@@ -17,6 +17,7 @@
 //   k_finalize_deferred  interface rows whose partial rows came over NCCL (A3 replacement).
 //   k_grad / k_curl      discrete gradient (Algorithm 1, l.417-438) / curl (l.440-445).
 //   k_dofmap    element restriction (for parity tests of the numbering).
+//   k_coords    LOR vertex coordinate vectors: E-vector -> owned H1 dofs.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -651,6 +652,52 @@ __global__ void __launch_bounds__(128) k_dofmap(DofmapArgs A) {
     A.map[el * A.ndpe + l] = B.g0 + B.str[0] * x[0] + B.str[1] * x[1] + B.str[2] * x[2];
     if (A.sign) A.sign[el * A.ndpe + l] = B.sigma;
   }
+}
+
+// ================================================================================ coordinate vectors
+// The LOR mesh vertex coordinates AMS/ADS need: "Deduplicating this vector is
+// performed efficiently using the element restriction degree of freedom index mappings ... with
+// one thread per deduplicated DOF without requiring any MPI communication."  The E-vector at the
+// GLL points holds exactly the LOR vertex coordinates (the GLL interpolation of the HO nodes is the
+// identity for nodes given at the GLL points, reading P-27); each owned H1 dof is written once, by
+// the minimal element containing its coarse entity (the same rule as A2, l.352) -- one thread per
+// deduplicated dof, its index mapping from the element's affine blocks.
+template <int DIM>
+__global__ void __launch_bounds__(128) k_coords(CoordArgs A) {
+  __shared__ ElemTopo T;
+  __shared__ Blk blk[27];
+  const int64_t el = blockIdx.x;
+  if (el >= A.nel_local) return;
+  {
+    const int4 *src = reinterpret_cast<const int4 *>(A.topo + el);
+    int4 *dst = reinterpret_cast<int4 *>(&T);
+    for (int i = threadIdx.x; i < (int)(sizeof(ElemTopo) / 16); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < 27) {
+    if (DIM == 2 && threadIdx.x >= 9) blk[threadIdx.x].size = 0;
+    else block_affine<DIM, SP_H1>(A.p, 0, threadIdx.x, T, A.base, blk[threadIdx.x]);
+  }
+  __syncthreads();
+  const int np = DIM == 3 ? (A.p + 1) * (A.p + 1) * (A.p + 1) : (A.p + 1) * (A.p + 1);
+  const double *xe = A.X + el * A.xstride;
+  for (int l = threadIdx.x; l < np; l += blockDim.x) {
+    int s, x[3];
+    decode_local<DIM, SP_H1>(A.p, l, s, x);
+    const int tr = row_tau<DIM, SP_H1>(A.p, s, x);
+    if ((T.flags[tr] & (TF_MIN | TF_OWNED)) != (TF_MIN | TF_OWNED)) continue;
+    const Blk &B = blk[tr];
+    const int64_t r = (int64_t)(B.g0 + B.str[0] * x[0] + B.str[1] * x[1] + B.str[2] * x[2]) - A.row_begin;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) __stcs(A.out + d * A.n_local + r, __ldcs(xe + d * np + l));
+  }
+}
+
+cudaError_t launch_coords(int dim, const CoordArgs &a, cudaStream_t st) {
+  if (a.nel_local <= 0) return cudaSuccess;
+  if (dim == 2) k_coords<2><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  else k_coords<3><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 // ================================================================================ dof transpose

@@ -172,6 +172,19 @@ struct DofmapArgs {
   int8_t *sign;
 };
 
+// LOR vertex coordinate vectors: E-vector -> owned H1 dofs
+struct CoordArgs {
+  int p;
+  int64_t nel_local;
+  const ElemTopo *topo;
+  const int32_t *base[4];
+  const double *X;   // E-vector [local element][dim][(p+1)^dim], element stride xstride
+  int64_t xstride;
+  int64_t row_begin, n_local;
+  double *out;       // [dim][n_local]
+};
+cudaError_t launch_coords(int dim, const CoordArgs &a, cudaStream_t st);
+
 cudaError_t launch_count(int dim, int space, const CountArgs &a, cudaStream_t st);
 // table sizes (entries) and builder
 int64_t tab_slot_entries(int dim, int space);

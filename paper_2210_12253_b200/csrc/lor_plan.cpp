@@ -121,6 +121,50 @@ void slot_entity(int dim, int tau, int &type, int &lidx) {
 
 // topology record of any element e (entity ids, orientation codes, valences, TF_MIN / TF_OWNED
 // for this rank); valid after build()
+void HostPlan::boundary_rows(int s, std::vector<int32_t> &out) const {
+  out.clear();
+  const SpacePlan &S = sp[s];
+  if (!S.valid) return;
+  int64_t nd[4];
+  entity_ndofs(dim, p, s, nd);
+  const int nc = 1 << dim, nle = (dim == 3) ? 12 : 4, nslot = (dim == 3) ? 27 : 9, ft = dim - 1;
+  std::vector<char> bnd[3];
+  for (int t = 0; t < 3; ++t) bnd[t].assign(n_ent[t], 0);
+  auto ent_id = [&](int64_t e, int type, int lidx) -> int64_t {
+    if (type == 0) return EVp[e * nc + lidx];
+    if (type == 1) return el_edge[e * nle + lidx];
+    return el_face[e * 6 + lidx];
+  };
+  for (int64_t e = 0; e < nel; ++e)
+    for (int tau = 0; tau < nslot; ++tau) {
+      int type, lidx;
+      slot_entity(dim, tau, type, lidx);
+      if (type != ft) continue;
+      const int64_t id = ent_id(e, type, lidx);
+      if (inc_off[type][id + 1] - inc_off[type][id] != 1) continue;  // shared facet: interior
+      const int cls[3] = {tau % 3, (tau / 3) % 3, tau / 9};
+      int n = 0;
+      while (cls[n] == 1) ++n;  // the facet's normal axis (its one non-interior class)
+      for (int t2 = 0; t2 < nslot; ++t2) {
+        const int c2[3] = {t2 % 3, (t2 / 3) % 3, t2 / 9};
+        if (c2[n] != cls[n]) continue;  // not on this facet
+        int ty2, l2;
+        slot_entity(dim, t2, ty2, l2);
+        if (ty2 < 3) bnd[ty2][ent_id(e, ty2, l2)] = 1;
+      }
+    }
+  for (int t = 0; t < 3; ++t) {
+    if (nd[t] == 0) continue;
+    for (int64_t id = 0; id < n_ent[t]; ++id) {
+      if (!bnd[t][id]) continue;
+      const int64_t g = S.base[t][id];
+      if (g < S.row_begin || g >= S.row_begin + S.n_local) continue;
+      for (int64_t k = 0; k < nd[t]; ++k) out.push_back((int32_t)(g - S.row_begin + k));
+    }
+  }
+  std::sort(out.begin(), out.end());
+}
+
 ElemTopo HostPlan::topo_of(int64_t e) const {
   const int nc = 1 << dim, nle = (dim == 3) ? 12 : 4;
   const int nslot = (dim == 3) ? 27 : 9;

@@ -49,6 +49,10 @@ struct HostPlan {
 
   void build(const PlanInput &in);
   ElemTopo topo_of(int64_t e) const;
+  // local rows (ascending) of the owned dofs of space s on the domain boundary: the dofs of every
+  // coarse entity lying on a boundary facet (a face -- an edge in 2D -- of exactly one element);
+  // the essential dofs of a Dirichlet / tangential / normal trace condition.
+  void boundary_rows(int s, std::vector<int32_t> &out) const;
 };
 
 int maxl_of(int dim, int space);

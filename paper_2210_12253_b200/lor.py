@@ -38,6 +38,16 @@ class _Csr(C.Structure):
     _fields_ = [("row_ptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p), ("cap_nnz", C.c_int64)]
 
 
+class _ParCsr(C.Structure):
+    _fields_ = [("diag_row_ptr", C.c_void_p), ("diag_col", C.c_void_p), ("diag_val", C.c_void_p),
+                ("cap_diag", C.c_int64), ("offd_row_ptr", C.c_void_p), ("offd_col", C.c_void_p),
+                ("offd_val", C.c_void_p), ("cap_offd", C.c_int64), ("col_map_offd", C.c_void_p),
+                ("cap_col_map", C.c_int64)]
+
+
+OPS = {"h1": 0, "nd": 1, "rt": 2, "grad": 3, "curl": 4}
+
+
 _lib = None
 
 
@@ -78,6 +88,14 @@ def lib():
         L.lor_fill_path.argtypes = [C.c_void_p, C.c_int]
         L.lor_query_transpose.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int64)]
         L.lor_dof_transpose.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64]
+        L.lor_parcsr_prepare.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Csr)] + [C.POINTER(C.c_int64)] * 3
+        L.lor_parcsr_fill.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Csr), C.POINTER(_ParCsr)]
+        L.lor_boundary_dofs.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.lor_eliminate_bc.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(_ParCsr)]
+        L.lor_bc_exchange_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        L.lor_eliminate_bc_finish.argtypes = [C.c_void_p, C.c_int, C.POINTER(_ParCsr)]
+        L.lor_parcsr_exchange_counts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.lor_coordinates.argtypes = [C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -301,3 +319,74 @@ class LOR:
         s = t.empty((self.n_elem_local, n), dtype=t.int8, device=self.device)
         self._check(lib().lor_dof_map(self.h, sp, C.c_void_p(m.data_ptr()), C.c_void_p(s.data_ptr())))
         return m, s
+
+    # ------------------------------------------------------------------ A3 layout / A4 (NEXT-1)
+    def parcsr(self, op, A, out=None):
+        """hypre-style split of the assembled operator ``A`` = (row_ptr, col, val) of ``op`` ("h1", "nd",
+        "rt", "grad", "curl"): lor_parcsr_prepare (synchronous sizes) + lor_parcsr_fill.  Returns a
+        dict of device tensors diag_row_ptr, diag_col, diag_val, offd_row_ptr, offd_col, offd_val,
+        col_map_offd (``out`` = such a dict to reuse)."""
+        t = self.torch
+        o = OPS.get(op, op)
+        v = [C.c_int64() for _ in range(3)]
+        a = self._csr(*A)
+        self._check(lib().lor_parcsr_prepare(self.h, o, C.byref(a), *[C.byref(x) for x in v]))
+        nd, no, nc = (x.value for x in v)
+        n = A[0].numel() - 1
+        if out is None:
+            out = dict(diag_row_ptr=t.empty(n + 1, dtype=t.int64, device=self.device),
+                       diag_col=t.empty(max(nd, 1), dtype=t.int32, device=self.device),
+                       diag_val=t.empty(max(nd, 1), dtype=t.float64, device=self.device),
+                       offd_row_ptr=t.empty(n + 1, dtype=t.int64, device=self.device),
+                       offd_col=t.empty(max(no, 1), dtype=t.int32, device=self.device),
+                       offd_val=t.empty(max(no, 1), dtype=t.float64, device=self.device),
+                       col_map_offd=t.empty(max(nc, 1), dtype=t.int64, device=self.device))
+        out["sizes"] = (nd, no, nc)
+        self._check(lib().lor_parcsr_fill(self.h, o, C.byref(a), C.byref(self._pcsr(out))))
+        return out
+
+    @staticmethod
+    def _pcsr(M):
+        m = _ParCsr()
+        m.diag_row_ptr, m.diag_col, m.diag_val = (M[k].data_ptr() for k in ("diag_row_ptr", "diag_col", "diag_val"))
+        m.offd_row_ptr, m.offd_col, m.offd_val = (M[k].data_ptr() for k in ("offd_row_ptr", "offd_col", "offd_val"))
+        m.col_map_offd = M["col_map_offd"].data_ptr()
+        m.cap_diag, m.cap_offd, m.cap_col_map = M["diag_col"].numel(), M["offd_col"].numel(), M["col_map_offd"].numel()
+        return m
+
+    def boundary_dofs(self, space="h1"):
+        """int32 device tensor: local rows of the owned dofs on the domain boundary (lor_boundary_dofs)."""
+        t = self.torch
+        sp = SPACES.get(space, space)
+        n = C.c_int64()
+        self._check(lib().lor_boundary_dofs(self.h, sp, None, 0, C.byref(n)))
+        rows = t.empty(max(n.value, 1), dtype=t.int32, device=self.device)
+        self._check(lib().lor_boundary_dofs(self.h, sp, C.c_void_p(rows.data_ptr()), C.c_int64(rows.numel()),
+                                            C.byref(n)))
+        return rows[:n.value]
+
+    def eliminate_bc(self, space, ess, M):
+        """Step A4 on the ParCSR ``M`` of ``space`` (lor_eliminate_bc); ``ess`` = int32 device tensor."""
+        self._check(lib().lor_eliminate_bc(self.h, SPACES.get(space, space), C.c_void_p(ess.data_ptr()),
+                                           C.c_int64(ess.numel()), C.byref(self._pcsr(M))))
+
+    def bc_exchange_copy_from(self, src: "LOR", space):
+        self._check(lib().lor_bc_exchange_copy(self.h, src.h, SPACES.get(space, space)))
+
+    def eliminate_bc_finish(self, space, M):
+        self._check(lib().lor_eliminate_bc_finish(self.h, SPACES.get(space, space), C.byref(self._pcsr(M))))
+
+    def parcsr_exchange_counts(self, space):
+        s = np.zeros(self.nranks, dtype=np.int64)
+        r = np.zeros(self.nranks, dtype=np.int64)
+        self._check(lib().lor_parcsr_exchange_counts(self.h, SPACES.get(space, space), s.ctypes.data, r.ctypes.data))
+        return s, r
+
+    def coordinates(self, out=None):
+        """LOR vertex coordinate vectors of the owned H1 dofs: device tensor [dim, n_local] (lor_coordinates)."""
+        t = self.torch
+        q = self.query("h1")
+        if out is None:
+            out = t.empty((self.dim, max(q["n_local"], 1)), dtype=t.float64, device=self.device)
+        self._check(lib().lor_coordinates(self.h, C.c_void_p(out.data_ptr())))
+        return out[:, :q["n_local"]]
