@@ -42,8 +42,14 @@ WORKLOADS = {
     "C5-J": "C5-J: C5 with jittered interior vertices (seed 12253)",
     "C4-G": "C4-G: discrete gradient (ND rows x H1 cols) on the C4 mesh, 32^3 hex per GPU, p=4",
     "C5-C": "C5-C: discrete curl (RT rows x ND cols) on the C5 mesh, 32^3 hex per GPU, p=4",
+    "C2-A4": "C2-A4: ParCSR split + A4 boundary elimination of the assembled C2 matrix (NEXT-1)",
+    "C4-A4": "C4-A4: ParCSR split + A4 boundary elimination of the assembled C4 (ND) matrix (NEXT-1)",
+    "C5-A4": "C5-A4: ParCSR split + A4 boundary elimination of the assembled C5 (RT) matrix (NEXT-1)",
+    "C2-X": "C2-X: LOR vertex coordinate vectors of the C2 mesh (E-vector -> owned H1 dofs, NEXT-2)",
 }
 DISCRETE = {"C4-G": ("C4", "grad"), "C5-C": ("C5", "curl")}
+# steps after the assembly: A3 layout + A4, coordinate vectors (l.400-404)
+AUX = {"C2-A4": ("C2", "a4"), "C4-A4": ("C4", "a4"), "C5-A4": ("C5", "a4"), "C2-X": ("C2", "coords")}
 # the paper's own numbers for the discrete operators (context only; 1 V100)
 PAPER_DISCRETE_GDOFS = {"grad": 12.0, "curl": 4.5}
 
@@ -139,13 +145,27 @@ def host_info():
 
 ORACLE_SNIPPET = r"""
 import json, sys, time
+import numpy as np
 sys.path.insert(0, {root!r})
 from oracle import oracle as O
 from paper_2210_12253_b200 import meshgen as mg
 O.build()
 m, form = mg.config_mesh({cfg!r}, n={n})
 t0 = time.perf_counter()
-if {which!r}:
+if {aux!r} == "coords":
+    from oracle import bc
+    t0 = time.perf_counter()
+    xyz = bc.coordinates(m)
+    A = O.Csr(row_ptr=np.zeros(xyz.shape[1] + 1, dtype=np.int64), row_id=None, col=np.zeros(0), val=None, n_cols=0)
+elif {aux!r} == "a4":
+    from oracle import bc
+    A0 = O.assemble(m, form["space"], form["quad"], form["alpha"], form["beta"])
+    t0 = time.perf_counter()
+    ess = bc.boundary_dofs(m, form["space"])
+    n0 = A0.row_ptr.shape[0] - 1
+    P = bc.parcsr_split(bc.eliminate(A0, ess), 0, n0, 0, n0)
+    A = A0
+elif {which!r}:
     A = O.discrete(m, {which!r})
 else:
     A = O.assemble(m, form["space"], form["quad"], form["alpha"], form["beta"])
@@ -158,7 +178,10 @@ def cpu_baseline(cfg, n):
     """The oracle as it stands (single-threaded C, test infrastructure), pinned to core 0
     (taskset -c 0), on the workload's recipe at n^3 elements (n = 32: the full C2/C4/C5 mesh)."""
     base, which = DISCRETE.get(cfg, (cfg, ""))
-    code = ORACLE_SNIPPET.format(root=ROOT, cfg=base, n=n, which=which)
+    base, aux = AUX.get(cfg, (base, ""))
+    if aux:
+        n = min(n, 8 if aux == "a4" else 16)
+    code = ORACLE_SNIPPET.format(root=ROOT, cfg=base, n=n, which=which, aux=aux)
     cmd = [sys.executable, "-c", code]
     pinned = False
     try:
@@ -174,7 +197,8 @@ def cpu_baseline(cfg, n):
     return {"value": d["rows"] / d["seconds"] / 1e6, "unit": "MDOF/s", "cores": 1, "kind": "oracle",
             "pinned": "taskset -c 0" if pinned else "unpinned",
             "sample": f"{base} recipe at {n}^3 elements{' (the full workload)' if n == 32 and base != 'C3' else ''}: "
-                      f"{d['rows']} rows, {d['nnz']} nnz, {'discrete ' + which if which else 'full oracle assembly'} "
+                      f"{d['rows']} rows, {d['nnz']} nnz, "
+                      f"{'discrete ' + which if which else ('oracle/bc ' + aux) if aux else 'full oracle assembly'} "
                       f"in {d['seconds']:.2f} s",
             "host": host_info()}
 
@@ -274,6 +298,7 @@ def main():
 
     cfg = args.config.upper()
     base, which = DISCRETE.get(cfg, (cfg, ""))
+    base, aux = AUX.get(cfg, (base, ""))
     mesh, form = mg.config_mesh(base, gpus=world)
     nid = None
     if world > 1:
@@ -289,7 +314,36 @@ def main():
     nel_local = ctx.n_elem_local
     ndpe = (ctx.ndpe[0], ctx.ndpe[1], ctx.ndpe[2])
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    if which:
+    aux_bytes = None
+    if aux:
+        # the post-assembly step on the assembled operator: the matrix is assembled once (untimed), the
+        # symbolic split (lor_parcsr_prepare, synchronous) is setup; a step = the numeric split + A4
+        q = ctx.query(space)
+        ng = q["n_global"]
+        if aux == "coords":
+            qh = ctx.query("h1")
+            q = dict(n_local=qh["n_local"], nnz=0, n_global=qh["n_global"])
+            xyz = torch.empty((mesh.dim, qh["n_local"]), dtype=torch.float64, device=dev)
+
+            def step():
+                ctx.coordinates(out=xyz)
+            aux_bytes = 16 * mesh.dim * qh["n_local"] + 192 * nel_local
+        else:
+            A = ctx.assemble(space, form["alpha"], form["beta"], form["quad"])
+            ctx.sync()
+            P = ctx.parcsr(space, A)
+            ess = ctx.boundary_dofs(space)
+            ctx.sync()
+            ep = A[0].cpu()
+            ess_h = ess.cpu().long()
+            nnz_e = int((ep[ess_h + 1] - ep[ess_h]).sum()) if ess_h.numel() else 0
+
+            def step():
+                ctx.parcsr(space, A, out=P, prepared=True)
+                ctx.eliminate_bc(space, ess, P)
+            aux_bytes = (24 * q["nnz"] + 32 * (q["n_local"] + 1) + q["n_local"] + 4 * ess.numel() + 24 * nnz_e)
+        q = dict(n_local=q["n_local"], nnz=q["nnz"], n_global=q["n_global"])
+    elif which:
         q = ctx.query_discrete(which)
         ng = q["n_local"]
         if world > 1:
@@ -327,7 +381,12 @@ def main():
     torch.cuda.synchronize()
     launches = ctx.launches() - l0
     t_ms = statistics.mean(step_ms)
-    if which:
+    if aux:
+        fill_ms = t_ms
+        kernel = ("k_coords (E-vector -> owned H1 dofs)" if aux == "coords" else
+                  "ParCSR fill (k_pc_fill_flat) + A4 (k_bc_mark, k_bc_rows)")
+        B = aux_bytes
+    elif which:
         fill_ms = t_ms  # the discrete call: row_ptr stride kernel + k_discrete
         kernel = f"discrete {which} (k_discrete, a{8 if which == 'grad' else 9})"
         B = discrete_bytes(which, nel_local, ndpe, q["n_local"])
@@ -355,7 +414,7 @@ def main():
 
     # ---- numeric-only re-assembly (pattern reuse), same buffers ---------------------------------
     reasm = None
-    if not which and not args.no_reassembly:
+    if not which and not aux and not args.no_reassembly:
         def restep():
             ctx.reassemble(space, form["alpha"], form["beta"], form["quad"], out=out)
         for _ in range(3):
@@ -374,7 +433,7 @@ def main():
 
     # ---- e2e: pinned host E-vector H2D + the same call + CSR D2H, same public API ---------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not aux:
         e0, e1 = ctx.elem_begin, ctx.elem_begin + nel_local
         Xh = torch.from_numpy(mesh.X[e0:e1].copy()).pin_memory()
         hrp = torch.empty(q["n_local"] + 1, dtype=torch.int64).pin_memory()
@@ -410,14 +469,18 @@ def main():
                        "nnz_per_gpu": q["nnz"], "elements_per_gpu": nel_local, "p": mesh.p,
                        "space": which or space, "l2": "flushed (512 MiB write) before every timed step",
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
-                       "step": ("lor_discrete_" + which) if which else
-                               "lor_assemble_" + space + ": symbolic pass + scan + fill (full call, SURVEY P-24)"},
+                       "step": ("lor_coordinates" if aux == "coords" else
+                                "lor_parcsr_fill + lor_eliminate_bc (boundary dofs of the whole domain)" if aux else
+                                ("lor_discrete_" + which) if which else
+                                "lor_assemble_" + space + ": symbolic pass + scan + fill (full call, SURVEY P-24)")},
             "hbm_gbs": B / (t_ms * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "algorithmic_bytes_per_launch": B, "avg_launch_ms": fill_ms,
-                         "bytes_model": "SURVEY 8(d) d.3 (" + ("B_G" if which == "grad" else "B_C" if which else "B_asm") + ")"},
-            "phases_ms": ({} if which else dict(zip(["symbolic+scan", "fill (element pass)", "merge pass",
+                         "bytes_model": ("DESIGN.md 4 (B_X = 16 dim n_H1 + 192 nel)" if aux == "coords" else
+                                         "DESIGN.md 4 (B_A4 = 24 nnz + 32 (n+1) + n + 4 n_ess + 24 nnz_ess)" if aux else
+                                         "SURVEY 8(d) d.3 (" + ("B_G" if which == "grad" else "B_C" if which else "B_asm") + ")")},
+            "phases_ms": ({} if which or aux else dict(zip(["symbolic+scan", "fill (element pass)", "merge pass",
                                                      "exchange+finalize"], ph))),
             "setup_ms": setup_ms,
             "reassembly": reasm,

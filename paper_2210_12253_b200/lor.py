@@ -321,15 +321,18 @@ class LOR:
         return m, s
 
     # ------------------------------------------------------------------ A3 layout / A4 (NEXT-1)
-    def parcsr(self, op, A, out=None):
+    def parcsr(self, op, A, out=None, prepared=False):
         """hypre-style split of the assembled operator ``A`` = (row_ptr, col, val) of ``op`` ("h1", "nd",
         "rt", "grad", "curl"): lor_parcsr_prepare (synchronous sizes) + lor_parcsr_fill.  Returns a
         dict of device tensors diag_row_ptr, diag_col, diag_val, offd_row_ptr, offd_col, offd_val,
         col_map_offd (``out`` = such a dict to reuse)."""
         t = self.torch
         o = OPS.get(op, op)
-        v = [C.c_int64() for _ in range(3)]
         a = self._csr(*A)
+        if prepared and out is not None:  # numeric part only (same operator, same pattern)
+            self._check(lib().lor_parcsr_fill(self.h, o, C.byref(a), C.byref(self._pcsr(out))))
+            return out
+        v = [C.c_int64() for _ in range(3)]
         self._check(lib().lor_parcsr_prepare(self.h, o, C.byref(a), *[C.byref(x) for x in v]))
         nd, no, nc = (x.value for x in v)
         n = A[0].numel() - 1

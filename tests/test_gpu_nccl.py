@@ -3,7 +3,9 @@ torch.distributed.  Each rank's owned rows against the oracle's rank-major matri
   * H1 and RT: single-pass extended frame with the ghost layer (no partial-row exchange);
   * ND: element + merge passes with the interface partial rows over grouped ncclSend/ncclRecv;
   * after lor_update_coordinates with new (jittered) coordinates, whose ghost layer is refreshed from
-    the peers over NCCL, the re-assembly matches the oracle on the moved mesh."""
+    the peers over NCCL, the re-assembly matches the oracle on the moved mesh;
+  * ParCSR split + A4 elimination with the boundary markers exchanged over NCCL on the side stream:
+    structure bit-exact against oracle/bc.py, eliminated entries exactly 0 / 1."""
 import os
 
 import numpy as np
@@ -50,6 +52,23 @@ def _worker(rank, world, port, q):
                                    f"{space} moved rank {rank}")
             except AssertionError as e:
                 errs.append(str(e))
+            # A4 over NCCL: the boundary markers of the peers zero this rank's offd columns
+            from oracle import bc
+            P = ctx.parcsr(space, out)
+            ess = ctx.boundary_dofs(space)
+            ctx.eliminate_bc(space, ess, P)
+            ctx.sync()
+            essg = bc.boundary_dofs(mb, space, world)
+            R = bc.parcsr_split(bc.eliminate(refb, essg), qq["row_begin"], qq["n_local"], qq["row_begin"],
+                                qq["row_begin"] + qq["n_local"])
+            for k in ("diag_row_ptr", "diag_col", "offd_row_ptr", "offd_col", "col_map_offd"):
+                n = len(R[k])
+                if not np.array_equal(P[k].cpu().numpy()[:n], R[k]):
+                    errs.append(f"{space} rank {rank}: parcsr {k}")
+            ov = P["offd_val"].cpu().numpy()[:len(R["offd_val"])]
+            zero = R["offd_val"] == 0.0
+            if not np.array_equal(ov[zero], R["offd_val"][zero]):
+                errs.append(f"{space} rank {rank}: eliminated offd columns")
             ctx.close()
     except Exception as e:  # noqa: BLE001
         errs.append(repr(e))
