@@ -46,6 +46,8 @@ WORKLOADS = {
     "C4-A4": "C4-A4: ParCSR split + A4 boundary elimination of the assembled C4 (ND) matrix (NEXT-1)",
     "C5-A4": "C5-A4: ParCSR split + A4 boundary elimination of the assembled C5 (RT) matrix (NEXT-1)",
     "C2-X": "C2-X: LOR vertex coordinate vectors of the C2 mesh (E-vector -> owned H1 dofs, NEXT-2)",
+    "C2-V": "C2-V: C2 with variable coefficients alpha a(x), beta b(x) given as E-vectors at the LOR vertices (NEXT-3)",
+    "C4-V": "C4-V: C4 (ND) with variable coefficients a(x), b(x) at the LOR vertices (NEXT-3)",
 }
 DISCRETE = {"C4-G": ("C4", "grad"), "C5-C": ("C5", "curl")}
 # steps after the assembly: A3 layout + A4, coordinate vectors (l.400-404)
@@ -167,6 +169,12 @@ elif {aux!r} == "a4":
     A = A0
 elif {which!r}:
     A = O.discrete(m, {which!r})
+elif {vc!r}:
+    xs = [m.X[:, d, :] for d in range(m.dim)]
+    ca = 1.0 + 0.5 * np.sin(3.0 * xs[0]) * np.cos(2.0 * xs[1]) + xs[2] * xs[2]
+    cb = 2.0 + np.cos(xs[0] + xs[1] + xs[2])
+    t0 = time.perf_counter()
+    A = O.assemble(m, form["space"], form["quad"], form["alpha"], form["beta"], coef=(ca, cb))
 else:
     A = O.assemble(m, form["space"], form["quad"], form["alpha"], form["beta"])
 dt = time.perf_counter() - t0
@@ -179,9 +187,12 @@ def cpu_baseline(cfg, n):
     (taskset -c 0), on the workload's recipe at n^3 elements (n = 32: the full C2/C4/C5 mesh)."""
     base, which = DISCRETE.get(cfg, (cfg, ""))
     base, aux = AUX.get(cfg, (base, ""))
+    vc = cfg.endswith("-V")
+    if vc:
+        base = cfg[:-2]
     if aux:
         n = min(n, 8 if aux == "a4" else 16)
-    code = ORACLE_SNIPPET.format(root=ROOT, cfg=base, n=n, which=which, aux=aux)
+    code = ORACLE_SNIPPET.format(root=ROOT, cfg=base, n=n, which=which, aux=aux, vc=vc)
     cmd = [sys.executable, "-c", code]
     pinned = False
     try:
@@ -280,6 +291,7 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(self_launch(args))
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -299,6 +311,9 @@ def main():
     cfg = args.config.upper()
     base, which = DISCRETE.get(cfg, (cfg, ""))
     base, aux = AUX.get(cfg, (base, ""))
+    varcoef = cfg.endswith("-V")
+    if varcoef:
+        base = cfg[:-2]
     mesh, form = mg.config_mesh(base, gpus=world)
     nid = None
     if world > 1:
@@ -312,6 +327,12 @@ def main():
     setup_ms = (time.perf_counter() - t0) * 1e3
     space = form["space"]
     nel_local = ctx.n_elem_local
+    if varcoef:  # smooth coefficient fields sampled at the LOR vertices (the E-vector points)
+        e0, e1 = ctx.elem_begin, ctx.elem_begin + nel_local
+        xs = [mesh.X[e0:e1, d, :] for d in range(mesh.dim)]
+        ca = 1.0 + 0.5 * np.sin(3.0 * xs[0]) * np.cos(2.0 * xs[1]) + xs[2] * xs[2]
+        cb = 2.0 + np.cos(xs[0] + xs[1] + xs[2])
+        ctx.set_coefficients(ca, cb)
     ndpe = (ctx.ndpe[0], ctx.ndpe[1], ctx.ndpe[2])
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     aux_bytes = None
@@ -396,6 +417,8 @@ def main():
         kernel = ("fill step a6 = k_xh1_fill" if ctx.fill_path(space) == 1 else
                   "fill step a6 = k_assemble + k_merge_rows")
         B = algorithmic_bytes(q, mesh.dim, mesh.p, nel_local, ndpe[{"h1": 0, "nd": 1, "rt": 2}[space]], space)
+        if varcoef:  # + the two coefficient E-vectors
+            B += 2 * 8 * (mesh.p + 1) ** mesh.dim * nel_local
     if world > 1:
         tt = torch.tensor([t_ms, fill_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

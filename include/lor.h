@@ -161,6 +161,17 @@ lor_status lor_query_elements(lor_ctx ctx, int64_t *elem_begin, int64_t *n_elem_
  * call it).  In LOR_EXCHANGE_MANUAL mode the ghost layer keeps the coordinates given at setup. */
 lor_status lor_update_coordinates(lor_ctx ctx, const double *elem_nodes);
 
+/* Variable coefficients ("definite Helmholtz", l.546 "time-dependent
+ * variable coefficients"; reading P-28): alpha_e / beta_e = coefficient E-vectors
+ * [n_elem_local][(p+1)^dim] at the GLL points (= the LOR vertices, the layout of elem_nodes), HOST or
+ * DEVICE, copied on the context stream.  Subsequent lor_assemble_* / lor_reassemble_* integrate
+ * alpha * a(x) (grad | curl | div part) and beta * b(x) (mass part), a and b sampled at the LOR
+ * vertices: the corner value under the vertex rule, the multilinear interpolant of the cell's corner
+ * values at the Gauss points under Gauss-2.  Both NULL: back to constant coefficients.  With
+ * variable coefficients every space takes the element + merge passes (lor_fill_path returns 0).
+ * INVALID_ARGUMENT if exactly one pointer is NULL. */
+lor_status lor_set_coefficients(lor_ctx ctx, const double *alpha_e, const double *beta_e);
+
 /* Exchange mode for nranks > 1 (A3 replacement).  LOR_EXCHANGE_NCCL (0, default when
  * nccl_unique_id was given): ncclSend/ncclRecv of interface partial rows inside the assembly call.
  * LOR_EXCHANGE_MANUAL (1, default without a unique id): single-process emulation of several ranks

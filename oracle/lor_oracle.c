@@ -46,6 +46,8 @@ typedef struct {
   const double *X;      /* [nel][dim][(p+1)^dim] coordinate E-vector (GLL points) */
   int nranks;
   const int64_t *erb;   /* [nranks+1] contiguous element slabs (NULL: 1 rank)    */
+  const double *ca, *cb; /* [nel][(p+1)^dim] coefficient E-vectors a(x), b(x) at the GLL points
+                           (variable coefficients, reading P-28), or NULL: constants */
 } orc_mesh;
 
 typedef struct {
@@ -204,9 +206,31 @@ static int local_ndof(int dim, int space) {
   return 6;
 }
 
-/* A (n x n, row major) = local matrix of alpha*(grad|curl|div) + beta*(mass) on one cell. */
+/* A (n x n, row major) = local matrix of alpha*a(x)*(grad|curl|div) + beta*b(x)*(mass) on one cell;
+ * a, b = the multilinear interpolants of the corner values ca8 / cb8 (vertex order), evaluated at each
+ * quadrature point (reading P-28: coefficients sampled at the LOR vertices);
+ * ca8 == cb8 == NULL: a = b = 1. */
+int orc_local_matrix_vc(int dim, int space, int quad, double alpha, double beta, const double *corners,
+                        const double *ca8, const double *cb8, double *A);
 int orc_local_matrix(int dim, int space, int quad, double alpha, double beta, const double *corners,
                      double *A) {
+  return orc_local_matrix_vc(dim, space, quad, alpha, beta, corners, NULL, NULL, A);
+}
+
+/* value at reference point x of the multilinear interpolant of the 2^dim corner values c (NULL: 1) */
+static double corner_interp(int dim, const double *c, const double *x) {
+  if (!c) return 1.0;
+  double s = 0.0;
+  for (int v = 0; v < (1 << dim); ++v) {
+    double N, g[3];
+    q1_basis(dim, x, v, &N, g);
+    s += N * c[v];
+  }
+  return s;
+}
+
+int orc_local_matrix_vc(int dim, int space, int quad, double alpha, double beta, const double *corners,
+                        const double *ca8, const double *cb8, double *A) {
   if (!(dim == 2 || dim == 3) || (dim == 2 && space != ORC_H1)) return ORC_ERR_ARG;
   int n = local_ndof(dim, space);
   for (int i = 0; i < n * n; ++i) A[i] = 0.0;
@@ -217,6 +241,7 @@ int orc_local_matrix(int dim, int space, int quad, double alpha, double beta, co
     jacobian(dim, corners, pts[q], J);
     double det = inverse(dim, J, Ji);
     if (!(det > 0.0)) return ORC_ERR_DEGENERATE;
+    const double aq = alpha * corner_interp(dim, ca8, pts[q]), bq = beta * corner_interp(dim, cb8, pts[q]);
     if (space == ORC_H1) {
       double N[8], g[8][3];
       for (int i = 0; i < n; ++i) {
@@ -231,7 +256,7 @@ int orc_local_matrix(int dim, int space, int quad, double alpha, double beta, co
         for (int j = 0; j < n; ++j) {
           double gg = 0.0;
           for (int k = 0; k < dim; ++k) gg += g[i][k] * g[j][k];
-          A[i * n + j] += w * (alpha * gg + beta * N[i] * N[j]) * det;
+          A[i * n + j] += w * (aq * gg + bq * N[i] * N[j]) * det;
         }
     } else if (space == ORC_ND) {
       double phi[12][3], cu[12][3];
@@ -255,7 +280,7 @@ int orc_local_matrix(int dim, int space, int quad, double alpha, double beta, co
             cc += cu[i][k] * cu[j][k];
             pp += phi[i][k] * phi[j][k];
           }
-          A[i * 12 + j] += w * (alpha * cc + beta * pp) * det;
+          A[i * 12 + j] += w * (aq * cc + bq * pp) * det;
         }
     } else {
       double phi[6][3], dv[6];
@@ -273,7 +298,7 @@ int orc_local_matrix(int dim, int space, int quad, double alpha, double beta, co
         for (int j = 0; j < 6; ++j) {
           double pp = 0.0;
           for (int k = 0; k < 3; ++k) pp += phi[i][k] * phi[j][k];
-          A[i * 6 + j] += w * (alpha * dv[i] * dv[j] + beta * pp) * det;
+          A[i * 6 + j] += w * (aq * dv[i] * dv[j] + bq * pp) * det;
         }
     }
   }
@@ -734,6 +759,19 @@ static void cell_corners(const orc_mesh *m, int64_t e, const int *k, double *cor
   }
 }
 
+/* the 2^d corner values of LOR cell k of element e of a scalar E-vector c [nel][(p+1)^dim] (NULL:
+ * returns NULL -- constant coefficients) */
+static const double *cell_coefs(const orc_mesh *m, const double *c, int64_t e, const int *k, double *out) {
+  if (!c) return NULL;
+  int p = m->p, dim = m->dim;
+  int64_t np = ipow(p + 1, dim);
+  for (int v = 0; v < (1 << dim); ++v) {
+    int a = v & 1, b = (v >> 1) & 1, cc = (v >> 2) & 1;
+    out[v] = c[e * np + h1_lidx(dim, p, k[0] + a, k[1] + b, dim == 3 ? k[2] + cc : 0)];
+  }
+  return out;
+}
+
 /* ======================================================================================
  * O5/O6: triplets and sort-and-sum into CSR.
  * ==================================================================================== */
@@ -819,14 +857,15 @@ int orc_assemble(const orc_mesh *m, int space, int quad, double alpha, double be
   trip_t *T = (trip_t *)malloc(sizeof(trip_t) * nt);
   if (!T) { topo_free(&t); numbering_free(&nb); return ORC_ERR_MEM; }
   int64_t it = 0;
-  double A[144], corners[24];
+  double A[144], corners[24], ca8[8], cb8[8];
   int ldof[12];
   for (int64_t e = 0; e < m->nel; ++e)
     for (int ic = 0; ic < nc; ++ic) {
       int k[3];
       cell_index(m->p, m->dim, ic, k);
       cell_corners(m, e, k, corners);
-      if (orc_local_matrix(m->dim, space, quad, alpha, beta, corners, A)) {
+      if (orc_local_matrix_vc(m->dim, space, quad, alpha, beta, corners, cell_coefs(m, m->ca, e, k, ca8),
+                              cell_coefs(m, m->cb, e, k, cb8), A)) {
         snprintf(g_err, sizeof g_err, "degenerate-geometry(e=%lld, kx=%d, ky=%d, kz=%d)", (long long)e, k[0],
                  k[1], k[2]);
         free(T); topo_free(&t); numbering_free(&nb);
@@ -871,7 +910,7 @@ int orc_assemble_rows(const orc_mesh *m, int space, int quad, double alpha, doub
   int nloc = local_ndof(m->dim, space), nc = ncells_dim(m->p, m->dim);
   int64_t cap = 1024, nt = 0;
   trip_t *T = (trip_t *)malloc(sizeof(trip_t) * cap);
-  double A[144], corners[24];
+  double A[144], corners[24], ca8[8], cb8[8];
   int ldof[12];
   for (int64_t q = 0; q < nreq; ++q) {
     int64_t g = rows[q];
@@ -888,7 +927,8 @@ int orc_assemble_rows(const orc_mesh *m, int space, int quad, double alpha, doub
         for (int i = 0; i < nloc; ++i) if (ldof[i] == l) li = i;
         if (li < 0) continue;
         cell_corners(m, e, k, corners);
-        if (orc_local_matrix(m->dim, space, quad, alpha, beta, corners, A)) { rc = ORC_ERR_DEGENERATE; break; }
+        if (orc_local_matrix_vc(m->dim, space, quad, alpha, beta, corners, cell_coefs(m, m->ca, e, k, ca8),
+                                cell_coefs(m, m->cb, e, k, cb8), A)) { rc = ORC_ERR_DEGENERATE; break; }
         for (int j = 0; j < nloc; ++j) {
           if (nt == cap) { cap *= 2; T = (trip_t *)realloc(T, sizeof(trip_t) * cap); }
           int64_t gj = nb.map[e * nb.ndpe + ldof[j]];

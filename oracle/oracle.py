@@ -38,7 +38,7 @@ def build(force: bool = False) -> str:
 class _Mesh(C.Structure):
     _fields_ = [("dim", C.c_int), ("p", C.c_int), ("nv", C.c_int64), ("nel", C.c_int64),
                 ("elem", C.POINTER(C.c_int64)), ("X", C.POINTER(C.c_double)), ("nranks", C.c_int),
-                ("erb", C.POINTER(C.c_int64))]
+                ("erb", C.POINTER(C.c_int64)), ("ca", C.POINTER(C.c_double)), ("cb", C.POINTER(C.c_double))]
 
 
 class _Csr(C.Structure):
@@ -91,7 +91,7 @@ def _check(rc):
 class OracleMesh:
     """Keeps numpy buffers alive while the C struct points into them."""
 
-    def __init__(self, mesh, nranks: int | None = None):
+    def __init__(self, mesh, nranks: int | None = None, coef=None):
         self.dim = mesh.dim
         self.p = mesh.p
         self.elem = np.ascontiguousarray(mesh.elem, dtype=np.int64)
@@ -101,9 +101,14 @@ class OracleMesh:
             erb = np.array([0, mesh.nel])
         self.erb = np.ascontiguousarray(erb, dtype=np.int64)
         self.nranks = len(self.erb) - 1
+        # variable coefficients: (a, b) E-vectors [nel][(p+1)^dim] (reading P-28), None = constants
+        self.coef = None if coef is None else tuple(np.ascontiguousarray(c, dtype=np.float64) for c in coef)
+        ptr = (lambda a: a.ctypes.data_as(C.POINTER(C.c_double))) if coef is not None else None
         self.s = _Mesh(mesh.dim, mesh.p, mesh.nv, mesh.nel, self.elem.ctypes.data_as(C.POINTER(C.c_int64)),
                        self.X.ctypes.data_as(C.POINTER(C.c_double)), self.nranks,
-                       self.erb.ctypes.data_as(C.POINTER(C.c_int64)))
+                       self.erb.ctypes.data_as(C.POINTER(C.c_int64)),
+                       ptr(self.coef[0]) if coef is not None else None,
+                       ptr(self.coef[1]) if coef is not None else None)
 
 
 def _take(c: _Csr) -> Csr:
@@ -116,18 +121,19 @@ def _take(c: _Csr) -> Csr:
     return out
 
 
-def assemble(mesh, space="h1", quad="vertex", alpha=1.0, beta=1.0, nranks=None) -> Csr:
-    """O2-O6: the full LOR matrix, all global rows, rank-major ids."""
-    om = OracleMesh(mesh, nranks)
+def assemble(mesh, space="h1", quad="vertex", alpha=1.0, beta=1.0, nranks=None, coef=None) -> Csr:
+    """O2-O6: the full LOR matrix, all global rows, rank-major ids.  coef = (a, b) coefficient
+    E-vectors (variable coefficients alpha a(x), beta b(x)) or None."""
+    om = OracleMesh(mesh, nranks, coef)
     c = _Csr()
     _check(lib().orc_assemble(C.byref(om.s), SPACES[space], QUADS[quad], C.c_double(alpha), C.c_double(beta),
                               C.byref(c)))
     return _take(c)
 
 
-def assemble_rows(mesh, rows, space="h1", quad="vertex", alpha=1.0, beta=1.0, nranks=None) -> Csr:
+def assemble_rows(mesh, rows, space="h1", quad="vertex", alpha=1.0, beta=1.0, nranks=None, coef=None) -> Csr:
     """O10: the requested global rows only (any size; cost ~ number of rows)."""
-    om = OracleMesh(mesh, nranks)
+    om = OracleMesh(mesh, nranks, coef)
     r = np.ascontiguousarray(np.unique(np.asarray(rows, dtype=np.int64)))
     c = _Csr()
     _check(lib().orc_assemble_rows(C.byref(om.s), SPACES[space], QUADS[quad], C.c_double(alpha), C.c_double(beta),
@@ -170,13 +176,18 @@ def topology_counts(mesh):
     return tuple(int(v) for v in cnt)
 
 
-def local_matrix(dim, space, quad, alpha, beta, corners) -> np.ndarray:
-    """O4 on one cell: corners [2^dim, dim] in local order a + 2b + 4c."""
+def local_matrix(dim, space, quad, alpha, beta, corners, ca8=None, cb8=None) -> np.ndarray:
+    """O4 on one cell: corners [2^dim, dim] in local order a + 2b + 4c; ca8 / cb8 = corner values of the
+    variable coefficients (None: constants)."""
     n = {"h1": 1 << dim, "nd": 12, "rt": 6}[space]
     A = np.zeros((n, n))
     cr = np.ascontiguousarray(corners, dtype=np.float64)
-    _check(lib().orc_local_matrix(C.c_int(dim), SPACES[space], QUADS[quad], C.c_double(alpha), C.c_double(beta),
-                                  cr.ctypes.data_as(C.POINTER(C.c_double)), A.ctypes.data_as(C.POINTER(C.c_double))))
+    ap = None if ca8 is None else np.ascontiguousarray(ca8, dtype=np.float64)
+    bp = None if cb8 is None else np.ascontiguousarray(cb8, dtype=np.float64)
+    dp = lambda a: None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    _check(lib().orc_local_matrix_vc(C.c_int(dim), SPACES[space], QUADS[quad], C.c_double(alpha), C.c_double(beta),
+                                     cr.ctypes.data_as(C.POINTER(C.c_double)), dp(ap), dp(bp),
+                                     A.ctypes.data_as(C.POINTER(C.c_double))))
     return A
 
 

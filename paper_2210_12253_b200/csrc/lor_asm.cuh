@@ -289,7 +289,8 @@ __device__ __forceinline__ void row_values(const double *__restrict__ cm, const 
 //   body diagonal = 0
 template <int P, int NC, int NRING_>
 __device__ __forceinline__ void cells_h1_corner(const double *__restrict__ X, double *__restrict__ cm, int k0, int ncell,
-                                                double alpha, double beta, int &bad) {
+                                                double alpha, double beta, int &bad, const double *ca = nullptr,
+                                                const double *cb = nullptr) {
   constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1;
   const int lane = threadIdx.x & 31;
   const int items = ncell * 8;
@@ -315,7 +316,9 @@ __device__ __forceinline__ void cells_h1_corner(const double *__restrict__ X, do
     cross3(j[0], j[1], r[2]);
     const double det = dot3(j[0], r[0]);
     if (act && !(det > 0.0)) bad = 1 + c;
-    const double sa = 0.125 * alpha / det;
+    // variable coefficients (NEXT-3): the element's coefficient E-vectors at this corner's point
+    const int lq = (cx + (q & 1)) + NP1 * ((cy + ((q >> 1) & 1)) + NP1 * (cz + ((q >> 2) & 1)));
+    const double sa = 0.125 * alpha * (ca ? __ldg(ca + lq) : 1.0) / det;
     double Q[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -326,7 +329,7 @@ __device__ __forceinline__ void cells_h1_corner(const double *__restrict__ X, do
     for (int d = 0; d < 3; ++d) sg[d] = ((q >> d) & 1) ? 1.0 : -1.0;
 #pragma unroll
     for (int d = 0; d < 3; ++d) Qs[d] = Q[d][0] * sg[0] + Q[d][1] * sg[1] + Q[d][2] * sg[2];
-    double diag = sg[0] * Qs[0] + sg[1] * Qs[1] + sg[2] * Qs[2] + 0.125 * beta * det;
+    double diag = sg[0] * Qs[0] + sg[1] * Qs[1] + sg[2] * Qs[2] + 0.125 * beta * (cb ? __ldg(cb + lq) : 1.0) * det;
     double edge[3], fdg[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -363,13 +366,28 @@ __device__ __forceinline__ void cells_h1_corner(const double *__restrict__ X, do
 
 template <int DIM, int SP, int P, int QUAD>
 __device__ __forceinline__ bool compute_cell(const double *__restrict__ X, int cx, int cy, int cz, double alpha,
-                                             double beta, double *__restrict__ out, int NC, int ci) {
+                                             double beta, double *__restrict__ out, int NC, int ci,
+                                             const double *ca = nullptr, const double *cb = nullptr) {
   constexpr int NP1 = P + 1;
+  // variable coefficients (NEXT-3): the cell's corner values from the element's coefficient E-vectors
+  double a8[8], b8[8];
+  const double *pa = nullptr, *pb = nullptr;
+  if (ca) {
+#pragma unroll
+    for (int q = 0; q < (DIM == 3 ? 8 : 4); ++q) {
+      const int l = DIM == 3 ? (cx + (q & 1)) + NP1 * ((cy + ((q >> 1) & 1)) + NP1 * (cz + ((q >> 2) & 1)))
+                             : (cx + (q & 1)) + NP1 * (cy + ((q >> 1) & 1));
+      a8[q] = __ldg(ca + l);
+      b8[q] = __ldg(cb + l);
+    }
+    pa = a8;
+    pb = b8;
+  }
   if (DIM == 3 && SP == SP_ND && QUAD == 0) {  // vertex rule: straight into the packed slots
     auto XF = [&](int v, int k) -> double {
       return X[k * ipow_c(NP1, 3) + (cx + (v & 1)) + NP1 * ((cy + ((v >> 1) & 1)) + NP1 * (cz + ((v >> 2) & 1)))];
     };
-    return cell_nd_vertex_to(XF, alpha, beta, out + ci, NC);
+    return cell_nd_vertex_to(XF, alpha, beta, out + ci, NC, pa, pb);
   }
   if (DIM == 3) {
     double C[8][3];
@@ -381,19 +399,19 @@ __device__ __forceinline__ bool compute_cell(const double *__restrict__ X, int c
     }
     if (SP == SP_H1) {
       double A[36];
-      bool ok = cell_h1_3d<QUAD>(C, alpha, beta, A);
+      bool ok = cell_h1_3d<QUAD>(C, alpha, beta, A, pa, pb);
 #pragma unroll
       for (int i = 0; i < 36; ++i) out[i * NC + ci] = A[i];
       return ok;
     } else if (SP == SP_ND) {
       double A[78];
-      bool ok = cell_nd<QUAD>(C, alpha, beta, A);
+      bool ok = cell_nd<QUAD>(C, alpha, beta, A, pa, pb);
 #pragma unroll
       for (int i = 0; i < 78; ++i) out[i * NC + ci] = A[i];
       return ok;
     } else {
       double A[21];
-      bool ok = cell_rt<QUAD>(C, alpha, beta, A);
+      bool ok = cell_rt<QUAD>(C, alpha, beta, A, pa, pb);
 #pragma unroll
       for (int i = 0; i < 21; ++i) out[i * NC + ci] = A[i];
       return ok;
@@ -407,7 +425,7 @@ __device__ __forceinline__ bool compute_cell(const double *__restrict__ X, int c
       for (int d = 0; d < 2; ++d) C[q][d] = X[d * NP1 * NP1 + l];
     }
     double A[10];
-    bool ok = cell_h1_2d<QUAD>(C, alpha, beta, A);
+    bool ok = cell_h1_2d<QUAD>(C, alpha, beta, A, pa, pb);
 #pragma unroll
     for (int i = 0; i < 10; ++i) out[i * NC + ci] = A[i];
     return ok;
@@ -656,6 +674,8 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
     }
   }
 
+  // variable coefficients (NEXT-3): this element's coefficient E-vectors, or null (constants)
+  const double *eca = A.ca ? A.ca + el * CF::NPTS : nullptr, *ecb = A.ca ? A.cb + el * CF::NPTS : nullptr;
   // ---- z-chunks of cell layers
   constexpr int NCHUNK = (DIM == 3) ? (P + KZ - 1) / KZ : 1;
   for (int ch = 0; ch < NCHUNK; ++ch) {
@@ -665,13 +685,14 @@ __global__ void __launch_bounds__(128, MINB) k_assemble(AsmArgs A) {
     if (ch > 0) __syncthreads();  // previous chunk's rows done before its ring slots are reused
     if (DIM == 3 && SP == SP_H1 && QUAD == 0) {
       int bad = 0;
-      cells_h1_corner<P, NC, CF::NRING>(X, cm, k0, ncell, A.alpha, A.beta, bad);
+      cells_h1_corner<P, NC, CF::NRING>(X, cm, k0, ncell, A.alpha, A.beta, bad, eca, ecb);
       if (bad) s_bad = bad;
     } else {
       for (int c = tid; c < ncell; c += blockDim.x) {
         const int cx = c % P, cy = (c / P) % P, cz = (DIM == 3) ? k0 + c / (P * P) : 0;
         const int ci = (DIM == 3) ? (((cz % CF::NRING) * P) + cy) * P + cx : cy * P + cx;
-        if (!compute_cell<DIM, SP, P, QUAD>(X, cx, cy, cz, A.alpha, A.beta, cm, NC, ci)) s_bad = 1 + cx + P * (cy + P * cz);
+        if (!compute_cell<DIM, SP, P, QUAD>(X, cx, cy, cz, A.alpha, A.beta, cm, NC, ci, eca, ecb))
+          s_bad = 1 + cx + P * (cy + P * cz);
       }
     }
     __syncthreads();

@@ -169,6 +169,8 @@ struct lor_ctx_s {
   int dbg = 0;  // LOR_DBG at setup (dev experiments; 0 in production)
   std::vector<void *> allocs;
   PcState pc[5];                     // lor_parcsr_* / lor_eliminate_bc per operator
+  double *ca = nullptr, *cb = nullptr;  // variable coefficient E-vectors (lor_set_coefficients)
+  bool vc = false;
   cudaStream_t side = nullptr;       // marker exchange stream (overlap)
   cudaEvent_t ev_pack = nullptr, ev_xchg = nullptr;
 };
@@ -354,7 +356,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   c->nphase = 0;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   lor_status st = LOR_OK;
-  if (S.xvok && quad == LOR_QUAD_VERTEX) {  // ND / RT extended-frame path: every owned row in one pass
+  if (S.xvok && quad == LOR_QUAD_VERTEX && !c->vc) {  // ND / RT extended-frame path: every owned row in one pass
     XvArgs x = xv_args(c, s);
     if (!reuse) {
       CUDA_TRY(c, launch_xv_sym(s, c->p, x, c->stream));
@@ -376,7 +378,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
     return LOR_OK;
   }
-  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX;
+  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX && !c->vc;  // variable coefficients: general path
   if (!reuse) {  // symbolic part (A2): row lengths per call, then the int64 scan
     if (xpath) {
       XFillArgs x = xfill_args(c, S);
@@ -439,6 +441,8 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.dbg = c->dbg;
   a.emap = c->nranks == 1 ? S.emap : nullptr;
   a.esgn = c->nranks == 1 ? S.esgn : nullptr;
+  a.ca = c->vc ? c->ca : nullptr;
+  a.cb = c->vc ? c->cb : nullptr;
   CUDA_TRY(c, launch_assemble(c->dim, s, c->p, (int)quad, a, c->stream, nullptr));
   if (c->nel_local > 0) c->launches++;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
@@ -1183,6 +1187,27 @@ lor_status lor_update_coordinates(lor_ctx c, const double *elem_nodes) {
   return exchange_ghost_coords(c);  // extended frame on several ranks: the ghost layer follows
 }
 
+lor_status lor_set_coefficients(lor_ctx c, const double *alpha_e, const double *beta_e) {
+  if (!c || (!alpha_e) != (!beta_e)) return LOR_ERR_INVALID_ARGUMENT;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (!alpha_e) {
+    c->vc = false;
+    return LOR_OK;
+  }
+  const int64_t np = (c->dim == 3) ? (int64_t)(c->p + 1) * (c->p + 1) * (c->p + 1) : (int64_t)(c->p + 1) * (c->p + 1);
+  const size_t bytes = sizeof(double) * std::max<int64_t>(1, c->nel_local * np);
+  if (!c->ca) {
+    if (dev_alloc(c, &c->ca, bytes / sizeof(double)) || dev_alloc(c, &c->cb, bytes / sizeof(double)))
+      return fail(c, LOR_ERR_OUT_OF_MEMORY, "coefficient E-vectors");
+  }
+  if (c->nel_local > 0) {
+    CUDA_TRY(c, cudaMemcpyAsync(c->ca, alpha_e, sizeof(double) * c->nel_local * np, cudaMemcpyDefault, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->cb, beta_e, sizeof(double) * c->nel_local * np, cudaMemcpyDefault, c->stream));
+  }
+  c->vc = true;
+  return LOR_OK;
+}
+
 lor_status lor_set_exchange(lor_ctx c, int mode) {
   if (!c || (mode != 0 && mode != 1)) return LOR_ERR_INVALID_ARGUMENT;
   if (mode == 0 && c->nranks > 1 && !c->comm) return fail(c, LOR_ERR_NCCL, "no NCCL communicator");
@@ -1377,7 +1402,7 @@ int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int
 
 int lor_fill_path(lor_ctx c, lor_space space) {
   if (!c || space < 0 || space > 2 || !c->sp[space].valid) return -1;
-  return (c->sp[space].xok || c->sp[space].xvok) ? 1 : 0;
+  return ((c->sp[space].xok || c->sp[space].xvok) && !c->vc) ? 1 : 0;
 }
 
 int lor_last_phase_ms(lor_ctx c, float *ms, int cap) {

@@ -101,9 +101,33 @@ __device__ __forceinline__ void jac_point(const double X[8][3], const double *t,
 
 __device__ __forceinline__ double gauss2_pt(int bit) { return bit ? 0.78867513459481288225 : 0.21132486540518711775; }
 
+// Variable coefficients ("time-dependent variable coefficients";
+// DESIGN.md reading P-28): the multiplier of alpha / beta at quadrature point q of a cell with corner
+// values c[NV] (vertex order a + 2b + 4c) -- the corner value under the vertex rule, the multilinear
+// interpolant at the Gauss point under Gauss-2.  c == nullptr: constant coefficients, multiplier
+// exactly 1.0 (x * 1.0 == x, so the constant-coefficient results are unchanged bit for bit).
+template <int QUAD, int NV>
+__device__ __forceinline__ double coef_q(const double *c, int q) {
+  if (!c) return 1.0;
+  if (QUAD == 0) return c[q];
+  double s = 0.0;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double f = 1.0;
+#pragma unroll
+    for (int a = 0; a < (NV == 8 ? 3 : 2); ++a) {
+      const double t = gauss2_pt((q >> a) & 1);
+      f *= ((v >> a) & 1) ? t : 1.0 - t;
+    }
+    s += f * c[v];
+  }
+  return s;
+}
+
 // ---------------------------------------------------------------------------- H1, 3D
 template <int QUAD>
-__device__ __forceinline__ bool cell_h1_3d(const double X[8][3], double alpha, double beta, double *A /*36*/) {
+__device__ __forceinline__ bool cell_h1_3d(const double X[8][3], double alpha, double beta, double *A /*36*/,
+                                           const double *ca = nullptr, const double *cb = nullptr) {
 #pragma unroll
   for (int i = 0; i < 36; ++i) A[i] = 0.0;
   const double w = 0.125;
@@ -114,7 +138,7 @@ __device__ __forceinline__ bool cell_h1_3d(const double X[8][3], double alpha, d
       Jac3 J;
       jac_corner(X, q, J);
       ok &= J.det > 0.0;
-      const double sa = w * alpha / J.det;
+      const double sa = w * alpha * coef_q<0, 8>(ca, q) / J.det;
       double Q[3][3];
 #pragma unroll
       for (int d = 0; d < 3; ++d)
@@ -125,7 +149,7 @@ __device__ __forceinline__ bool cell_h1_3d(const double X[8][3], double alpha, d
       for (int d = 0; d < 3; ++d) sg[d] = ((q >> d) & 1) ? 1.0 : -1.0;
 #pragma unroll
       for (int d = 0; d < 3; ++d) Qs[d] = Q[d][0] * sg[0] + Q[d][1] * sg[1] + Q[d][2] * sg[2];
-      A[tri(8, q, q)] += (sg[0] * Qs[0] + sg[1] * Qs[1] + sg[2] * Qs[2]) + w * beta * J.det;
+      A[tri(8, q, q)] += (sg[0] * Qs[0] + sg[1] * Qs[1] + sg[2] * Qs[2]) + w * beta * coef_q<0, 8>(cb, q) * J.det;
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         const int qd = q ^ (1 << d);
@@ -142,7 +166,7 @@ __device__ __forceinline__ bool cell_h1_3d(const double X[8][3], double alpha, d
       Jac3 J;
       jac_point(X, t, J);
       ok &= J.det > 0.0;
-      const double sa = w * alpha / J.det;
+      const double sa = w * alpha * coef_q<1, 8>(ca, pt) / J.det;
       double Q[3][3];
 #pragma unroll
       for (int d = 0; d < 3; ++d)
@@ -163,7 +187,7 @@ __device__ __forceinline__ bool cell_h1_3d(const double X[8][3], double alpha, d
         G[v][1] = f[0] * df[1] * f[2];
         G[v][2] = f[0] * f[1] * df[2];
       }
-      const double wb = w * beta * J.det;
+      const double wb = w * beta * coef_q<1, 8>(cb, pt) * J.det;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         double QG[3];
@@ -179,7 +203,8 @@ __device__ __forceinline__ bool cell_h1_3d(const double X[8][3], double alpha, d
 
 // ---------------------------------------------------------------------------- H1, 2D
 template <int QUAD>
-__device__ __forceinline__ bool cell_h1_2d(const double X[4][2], double alpha, double beta, double *A /*10*/) {
+__device__ __forceinline__ bool cell_h1_2d(const double X[4][2], double alpha, double beta, double *A /*10*/,
+                                           const double *ca = nullptr, const double *cb = nullptr) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) A[i] = 0.0;
   const double w = 0.25;
@@ -208,14 +233,15 @@ __device__ __forceinline__ bool cell_h1_2d(const double X[4][2], double alpha, d
     const double det = j0[0] * j1[1] - j0[1] * j1[0];
     ok &= det > 0.0;
     const double r0[2] = {j1[1], -j1[0]}, r1[2] = {-j0[1], j0[0]};  // rows of adj(J)
-    const double sa = w * alpha / det;
+    const double aq = coef_q<QUAD, 4>(ca, q), bq = coef_q<QUAD, 4>(cb, q);
+    const double sa = w * alpha * aq / det;
     const double Q00 = sa * (r0[0] * r0[0] + r0[1] * r0[1]);
     const double Q01 = sa * (r0[0] * r1[0] + r0[1] * r1[1]);
     const double Q11 = sa * (r1[0] * r1[0] + r1[1] * r1[1]);
     if (QUAD == 0) {
       const double s0 = (q & 1) ? 1.0 : -1.0, s1 = (q & 2) ? 1.0 : -1.0;
       const double Qs0 = Q00 * s0 + Q01 * s1, Qs1 = Q01 * s0 + Q11 * s1;
-      A[tri(4, q, q)] += s0 * Qs0 + s1 * Qs1 + w * beta * det;
+      A[tri(4, q, q)] += s0 * Qs0 + s1 * Qs1 + w * beta * bq * det;
       A[tri(4, q, q ^ 1)] += -s0 * Qs0;
       A[tri(4, q, q ^ 2)] += -s1 * Qs1;
       A[tri(4, q ^ 1, q ^ 1)] += Q00;
@@ -236,7 +262,7 @@ __device__ __forceinline__ bool cell_h1_2d(const double X[4][2], double alpha, d
 #pragma unroll
         for (int j = i; j < 4; ++j)
           A[tri(4, i, j)] += G[i][0] * (Q00 * G[j][0] + Q01 * G[j][1]) + G[i][1] * (Q01 * G[j][0] + Q11 * G[j][1]) +
-                             w * beta * det * N[i] * N[j];
+                             w * beta * bq * det * N[i] * N[j];
     }
   }
   return ok;
@@ -244,7 +270,8 @@ __device__ __forceinline__ bool cell_h1_2d(const double X[4][2], double alpha, d
 
 // ------------------------------------------------------------------------ ND (3D): 12 x 12
 template <int QUAD>
-__device__ __forceinline__ bool cell_nd(const double X[8][3], double alpha, double beta, double *A /*78*/) {
+__device__ __forceinline__ bool cell_nd(const double X[8][3], double alpha, double beta, double *A /*78*/,
+                                        const double *ca = nullptr, const double *cb = nullptr) {
 #pragma unroll
   for (int i = 0; i < 78; ++i) A[i] = 0.0;
   double M[21];  // 6x6 face "mass" with alpha: curl-curl = C^T M C
@@ -262,7 +289,7 @@ __device__ __forceinline__ bool cell_nd(const double X[8][3], double alpha, doub
       jac_point(X, t, J);
     }
     ok &= J.det > 0.0;
-    const double sm = w * beta / J.det, sc = w * alpha / J.det;
+    const double sm = w * beta * coef_q<QUAD, 8>(cb, q) / J.det, sc = w * alpha * coef_q<QUAD, 8>(ca, q) / J.det;
     double Qm[3][3], R[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -362,7 +389,8 @@ __device__ __forceinline__ void nd_curl_all(const double (&M)[21], double *__res
 }
 
 template <typename XF>
-__device__ __forceinline__ bool cell_nd_vertex_to(XF X, double alpha, double beta, double *__restrict__ out, int NC) {
+__device__ __forceinline__ bool cell_nd_vertex_to(XF X, double alpha, double beta, double *__restrict__ out, int NC,
+                                                  const double *ca = nullptr, const double *cb = nullptr) {
   double M[21];
 #pragma unroll
   for (int i = 0; i < 21; ++i) M[i] = 0.0;
@@ -380,7 +408,8 @@ __device__ __forceinline__ bool cell_nd_vertex_to(XF X, double alpha, double bet
     }
     finish_jac(J);
     ok &= J.det > 0.0;
-    const double rdet = 1.0 / J.det, sm = w * beta * rdet, sc = w * alpha * rdet;
+    const double rdet = 1.0 / J.det, sm = w * beta * coef_q<0, 8>(cb, q) * rdet,
+                 sc = w * alpha * coef_q<0, 8>(ca, q) * rdet;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
@@ -400,7 +429,8 @@ __device__ __forceinline__ bool cell_nd_vertex_to(XF X, double alpha, double bet
 
 // ------------------------------------------------------------------------ RT (3D): 6 x 6
 template <int QUAD>
-__device__ __forceinline__ bool cell_rt(const double X[8][3], double alpha, double beta, double *A /*21*/) {
+__device__ __forceinline__ bool cell_rt(const double X[8][3], double alpha, double beta, double *A /*21*/,
+                                        const double *ca = nullptr, const double *cb = nullptr) {
 #pragma unroll
   for (int i = 0; i < 21; ++i) A[i] = 0.0;
   const double w = 0.125;
@@ -416,8 +446,8 @@ __device__ __forceinline__ bool cell_rt(const double X[8][3], double alpha, doub
       jac_point(X, t, J);
     }
     ok &= J.det > 0.0;
-    const double sm = w * beta / J.det;
-    sdiv += w * alpha / J.det;
+    const double sm = w * beta * coef_q<QUAD, 8>(cb, q) / J.det;
+    sdiv += w * alpha * coef_q<QUAD, 8>(ca, q) / J.det;
     double R[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)

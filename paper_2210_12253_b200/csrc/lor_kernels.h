@@ -57,6 +57,7 @@ struct CountArgs {
 
 struct AsmArgs {
   int64_t nel_local, elem_begin;
+  const double *ca = nullptr, *cb = nullptr;  // variable coefficients: E-vectors [nel_local][(p+1)^dim] (NEXT-3)
   const int32_t *order;          // CTA -> local element (Morton order of element centroids), or NULL
   const ElemTopo *topo;
   const ElemSpace *esp;

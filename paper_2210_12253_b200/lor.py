@@ -96,6 +96,7 @@ def lib():
         L.lor_eliminate_bc_finish.argtypes = [C.c_void_p, C.c_int, C.POINTER(_ParCsr)]
         L.lor_parcsr_exchange_counts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.lor_coordinates.argtypes = [C.c_void_p, C.c_void_p]
+        L.lor_set_coefficients.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -393,3 +394,19 @@ class LOR:
             out = t.empty((self.dim, max(q["n_local"], 1)), dtype=t.float64, device=self.device)
         self._check(lib().lor_coordinates(self.h, C.c_void_p(out.data_ptr())))
         return out[:, :q["n_local"]]
+
+    # ------------------------------------------------------------------ variable coefficients (NEXT-3)
+    def set_coefficients(self, a=None, b=None):
+        """Coefficient E-vectors a(x), b(x) [n_elem_local, (p+1)^dim] of this rank's elements (numpy or
+        torch, host or device) multiplying alpha / beta in later assemblies; None, None = constants."""
+        if a is None and b is None:
+            self._check(lib().lor_set_coefficients(self.h, None, None))
+            self._coef = None
+            return
+        t = self.torch
+        conv = lambda x: (x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(x, dtype=np.float64))  # noqa: E731
+                          ).to(dtype=t.float64).contiguous()
+        a, b = conv(a), conv(b)
+        self._coef = (a, b)  # keep alive until the copy on the context stream has run
+        self._check(lib().lor_set_coefficients(self.h, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr())))
+        self.sync()
