@@ -46,6 +46,8 @@ WORKLOADS = {
     "C4-A4": "C4-A4: ParCSR split + A4 boundary elimination of the assembled C4 (ND) matrix (NEXT-1)",
     "C5-A4": "C5-A4: ParCSR split + A4 boundary elimination of the assembled C5 (RT) matrix (NEXT-1)",
     "C2-X": "C2-X: LOR vertex coordinate vectors of the C2 mesh (E-vector -> owned H1 dofs, NEXT-2)",
+    "C2-L": "C2-L: the unstructured (legacy) comparator on the C2 workload: LOR mesh as an arbitrary hex mesh, "
+            "dense 8x8 cell matrices, direct CSR assembly (PAPER.md l.593-606, NEXT-4)",
     "C2-V": "C2-V: C2 with variable coefficients alpha a(x), beta b(x) given as E-vectors at the LOR vertices (NEXT-3)",
     "C4-V": "C4-V: C4 (ND) with variable coefficients a(x), b(x) at the LOR vertices (NEXT-3)",
 }
@@ -188,7 +190,7 @@ def cpu_baseline(cfg, n):
     base, which = DISCRETE.get(cfg, (cfg, ""))
     base, aux = AUX.get(cfg, (base, ""))
     vc = cfg.endswith("-V")
-    if vc:
+    if vc or cfg.endswith("-L"):
         base = cfg[:-2]
     if aux:
         n = min(n, 8 if aux == "a4" else 16)
@@ -312,7 +314,8 @@ def main():
     base, which = DISCRETE.get(cfg, (cfg, ""))
     base, aux = AUX.get(cfg, (base, ""))
     varcoef = cfg.endswith("-V")
-    if varcoef:
+    legacy = cfg.endswith("-L")
+    if varcoef or legacy:
         base = cfg[:-2]
     mesh, form = mg.config_mesh(base, gpus=world)
     nid = None
@@ -376,6 +379,15 @@ def main():
 
         def step():
             ctx.discrete(which, out=out)
+    elif legacy:
+        q = ctx.query(space)
+        out = ctx.alloc(q["n_local"], q["nnz"])
+        t1 = time.perf_counter()
+        ctx.legacy_setup()
+        setup_ms += (time.perf_counter() - t1) * 1e3
+
+        def step():
+            ctx.legacy_assemble(form["alpha"], form["beta"], out=out)
     else:
         q = ctx.query(space)
         out = ctx.alloc(q["n_local"], q["nnz"])
@@ -411,6 +423,11 @@ def main():
         fill_ms = t_ms  # the discrete call: row_ptr stride kernel + k_discrete
         kernel = f"discrete {which} (k_discrete, a{8 if which == 'grad' else 9})"
         B = discrete_bytes(which, nel_local, ndpe, q["n_local"])
+    elif legacy:
+        fill_ms = t_ms
+        kernel = "legacy comparator: k_leg_ea + k_leg_rows (count) + k_scan + k_leg_rows (fill)"
+        ncell = nel_local * mesh.p ** 3  # broken LOR coordinates + LOR element restriction + CSR
+        B = 192 * ncell + 32 * ncell + 8 * (q["n_local"] + 1) + 12 * q["nnz"]
     else:
         # phases: [symbolic + scan, element pass / fill, merge pass, exchange + finalize]
         fill_ms = statistics.mean(p[1] + (p[2] if len(p) > 3 else 0.0) for p in phases)
@@ -437,7 +454,7 @@ def main():
 
     # ---- numeric-only re-assembly (pattern reuse), same buffers ---------------------------------
     reasm = None
-    if not which and not aux and not args.no_reassembly:
+    if not which and not aux and not legacy and not args.no_reassembly:
         def restep():
             ctx.reassemble(space, form["alpha"], form["beta"], form["quad"], out=out)
         for _ in range(3):
@@ -456,7 +473,7 @@ def main():
 
     # ---- e2e: pinned host E-vector H2D + the same call + CSR D2H, same public API ---------------
     e2e = None
-    if not args.no_e2e and not aux:
+    if not args.no_e2e and not aux and not legacy:
         e0, e1 = ctx.elem_begin, ctx.elem_begin + nel_local
         Xh = torch.from_numpy(mesh.X[e0:e1].copy()).pin_memory()
         hrp = torch.empty(q["n_local"] + 1, dtype=torch.int64).pin_memory()
@@ -492,7 +509,8 @@ def main():
                        "nnz_per_gpu": q["nnz"], "elements_per_gpu": nel_local, "p": mesh.p,
                        "space": which or space, "l2": "flushed (512 MiB write) before every timed step",
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
-                       "step": ("lor_coordinates" if aux == "coords" else
+                       "step": ("lor_legacy_assemble_h1 (unstructured comparator, full call)" if legacy else
+                                "lor_coordinates" if aux == "coords" else
                                 "lor_parcsr_fill + lor_eliminate_bc (boundary dofs of the whole domain)" if aux else
                                 ("lor_discrete_" + which) if which else
                                 "lor_assemble_" + space + ": symbolic pass + scan + fill (full call, SURVEY P-24)")},
@@ -500,10 +518,11 @@ def main():
             "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "algorithmic_bytes_per_launch": B, "avg_launch_ms": fill_ms,
-                         "bytes_model": ("DESIGN.md 4 (B_X = 16 dim n_H1 + 192 nel)" if aux == "coords" else
+                         "bytes_model": ("DESIGN.md 4 (B_L = 224 ncell + 8 (n+1) + 12 nnz)" if legacy else
+                                         "DESIGN.md 4 (B_X = 16 dim n_H1 + 192 nel)" if aux == "coords" else
                                          "DESIGN.md 4 (B_A4 = 24 nnz + 32 (n+1) + n + 4 n_ess + 24 nnz_ess)" if aux else
                                          "SURVEY 8(d) d.3 (" + ("B_G" if which == "grad" else "B_C" if which else "B_asm") + ")")},
-            "phases_ms": ({} if which or aux else dict(zip(["symbolic+scan", "fill (element pass)", "merge pass",
+            "phases_ms": ({} if which or aux or legacy else dict(zip(["symbolic+scan", "fill (element pass)", "merge pass",
                                                      "exchange+finalize"], ph))),
             "setup_ms": setup_ms,
             "reassembly": reasm,

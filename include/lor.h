@@ -172,6 +172,19 @@ lor_status lor_update_coordinates(lor_ctx ctx, const double *elem_nodes);
  * INVALID_ARGUMENT if exactly one pointer is NULL. */
 lor_status lor_set_coefficients(lor_ctx ctx, const double *alpha_e, const double *beta_e);
 
+/* Unstructured ("legacy") comparator -- NOT the product path:
+ * the LOR mesh treated as an arbitrary low-order hex mesh.  lor_legacy_setup builds the explicit LOR
+ * element restriction (8 global H1 ids per LOR cell), the LOR coordinates in broken per-cell format
+ * and the dof -> (cell, corner) transpose (the overhead l.604-606 says "can dominate"; synchronous).
+ * lor_legacy_assemble_h1 then, per call, computes the dense 8x8 matrix of every LOR cell (vertex rule,
+ * alpha grad.grad + beta mass) and assembles the global CSR directly from them: per row the 8 x 8
+ * candidate (column, value) pairs of its cells ranked by column, row lengths, scan, then columns
+ * ascending with duplicates summed -- the same matrix as lor_assemble_h1 (vertex rule) up to
+ * rounding.  3D, one rank; UNSUPPORTED otherwise.  Phases in lor_last_phase_ms: element matrices,
+ * count + scan, fill. */
+lor_status lor_legacy_setup(lor_ctx ctx);
+lor_status lor_legacy_assemble_h1(lor_ctx ctx, double alpha, double beta, lor_csr *out);
+
 /* Exchange mode for nranks > 1 (A3 replacement).  LOR_EXCHANGE_NCCL (0, default when
  * nccl_unique_id was given): ncclSend/ncclRecv of interface partial rows inside the assembly call.
  * LOR_EXCHANGE_MANUAL (1, default without a unique id): single-process emulation of several ranks

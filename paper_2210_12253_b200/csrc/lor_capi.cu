@@ -15,6 +15,7 @@
 #include "../../include/lor.h"
 #include "lor_internal.h"
 #include "lor_kernels.h"
+#include "lor_legacy.h"
 #include "lor_parcsr.h"
 #include "lor_plan.h"
 #include "lor_xframe.h"
@@ -170,6 +171,12 @@ struct lor_ctx_s {
   std::vector<void *> allocs;
   PcState pc[5];                     // lor_parcsr_* / lor_eliminate_bc per operator
   double *ca = nullptr, *cb = nullptr;  // variable coefficient E-vectors (lor_set_coefficients)
+  // unstructured comparator (lor_legacy_*): LOR element restriction, broken LOR coordinates, element
+  // matrices, dof -> (cell, corner) transpose
+  int64_t leg_ncell = 0;
+  int32_t *leg_lmap = nullptr, *leg_ent = nullptr;
+  double *leg_lx = nullptr, *leg_ea = nullptr;
+  int64_t *leg_off = nullptr;
   bool vc = false;
   cudaStream_t side = nullptr;       // marker exchange stream (overlap)
   cudaEvent_t ev_pack = nullptr, ev_xchg = nullptr;
@@ -1205,6 +1212,49 @@ lor_status lor_set_coefficients(lor_ctx c, const double *alpha_e, const double *
     CUDA_TRY(c, cudaMemcpyAsync(c->cb, beta_e, sizeof(double) * c->nel_local * np, cudaMemcpyDefault, c->stream));
   }
   c->vc = true;
+  return LOR_OK;
+}
+
+lor_status lor_legacy_setup(lor_ctx c) {
+  if (!c) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim != 3 || c->nranks != 1) return fail(c, LOR_ERR_UNSUPPORTED, "legacy comparator: 3D, one rank");
+  SpaceDev &S = c->sp[SP_H1];
+  if (!S.emap) return fail(c, LOR_ERR_UNSUPPORTED, "legacy comparator needs the H1 element restriction");
+  if (c->leg_lmap) return LOR_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const int64_t ncell = c->nel_local * (int64_t)c->p * c->p * c->p;
+  if (ncell * 8 >= (int64_t(1) << 31)) return fail(c, LOR_ERR_UNSUPPORTED, "legacy comparator: 8 ncell >= 2^31");
+  if (dev_alloc(c, &c->leg_lmap, ncell * 8) || dev_alloc(c, &c->leg_lx, ncell * 24) ||
+      dev_alloc(c, &c->leg_ea, ncell * 64) || dev_alloc(c, &c->leg_off, S.n_local + 1) ||
+      dev_alloc(c, &c->leg_ent, ncell * 8))
+    return fail(c, LOR_ERR_OUT_OF_MEMORY, "legacy comparator workspaces");
+  c->leg_ncell = ncell;
+  CUDA_TRY(c, launch_leg_mesh(c->p, c->nel_local, S.emap, c->X, c->xstride, c->leg_lmap, c->leg_lx, c->stream));
+  CUDA_TRY(c, launch_transpose(c->leg_lmap, ncell * 8, S.row_begin, S.n_local, S.cnt, c->leg_off, c->leg_ent,
+                               S.scan_status, S.tile_ctr, c->stream));
+  c->launches += 5;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return LOR_OK;
+}
+
+lor_status lor_legacy_assemble_h1(lor_ctx c, double alpha, double beta, lor_csr *out) {
+  if (!c || !out || !out->row_ptr) return LOR_ERR_INVALID_ARGUMENT;
+  if (!c->leg_lmap) return fail(c, LOR_ERR_INVALID_ARGUMENT, "lor_legacy_setup first");
+  SpaceDev &S = c->sp[SP_H1];
+  if (S.nnz_local > 0 && (!out->col || !out->val)) return fail(c, LOR_ERR_INVALID_ARGUMENT, "null output buffer");
+  if (out->cap_nnz < S.nnz_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < nnz_local");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  c->nphase = 0;
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  CUDA_TRY(c, launch_leg_ea(c->leg_ncell, c->leg_lx, alpha, beta, c->leg_ea, c->err, c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  LegArgs a{S.n_local, c->leg_off, c->leg_ent, c->leg_lmap, c->leg_ea, out->row_ptr, out->col, out->val, S.cnt};
+  CUDA_TRY(c, launch_leg_rows(a, false, c->stream));
+  CUDA_TRY(c, launch_scan(S.cnt, out->row_ptr, S.n_local, S.scan_status, S.tile_ctr, c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  CUDA_TRY(c, launch_leg_rows(a, true, c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  c->launches += 4;
   return LOR_OK;
 }
 

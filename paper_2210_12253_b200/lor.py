@@ -97,6 +97,8 @@ def lib():
         L.lor_parcsr_exchange_counts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.lor_coordinates.argtypes = [C.c_void_p, C.c_void_p]
         L.lor_set_coefficients.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lor_legacy_setup.argtypes = [C.c_void_p]
+        L.lor_legacy_assemble_h1.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(_Csr)]
         _lib = L
     return _lib
 
@@ -410,3 +412,16 @@ class LOR:
         self._coef = (a, b)  # keep alive until the copy on the context stream has run
         self._check(lib().lor_set_coefficients(self.h, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr())))
         self.sync()
+
+    # ------------------------------------------------------------------ unstructured comparator (NEXT-4)
+    def legacy_setup(self):
+        """LOR mesh as an unstructured mesh: element restriction, broken coordinates, transpose."""
+        self._check(lib().lor_legacy_setup(self.h))
+
+    def legacy_assemble(self, alpha=1.0, beta=1.0, out=None):
+        """The unstructured comparator's H1 assembly (lor_legacy_assemble_h1, vertex rule)."""
+        q = self.query("h1")
+        if out is None:
+            out = self.alloc(q["n_local"], q["nnz"])
+        self._check(lib().lor_legacy_assemble_h1(self.h, C.c_double(alpha), C.c_double(beta), C.byref(self._csr(*out))))
+        return out
