@@ -431,8 +431,8 @@ def main():
     else:
         # phases: [symbolic + scan, element pass / fill, merge pass, exchange + finalize]
         fill_ms = statistics.mean(p[1] + (p[2] if len(p) > 3 else 0.0) for p in phases)
-        kernel = ("fill step a6 = k_xh1_fill" if ctx.fill_path(space) == 1 else
-                  "fill step a6 = k_assemble + k_merge_rows")
+        kernel = (("fill step a6 = k_xh1_fill" if space == "h1" else "fill step a6 = k_xv_fill")
+                  if ctx.fill_path(space) == 1 else "fill step a6 = k_assemble + k_merge_rows")
         B = algorithmic_bytes(q, mesh.dim, mesh.p, nel_local, ndpe[{"h1": 0, "nd": 1, "rt": 2}[space]], space)
         if varcoef:  # + the two coefficient E-vectors
             B += 2 * 8 * (mesh.p + 1) ** mesh.dim * nel_local

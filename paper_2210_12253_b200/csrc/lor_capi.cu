@@ -1068,10 +1068,10 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
       // per-call symbolic pass == those of the general minimal-element count)
       for (int sv = SP_ND; S.xok && sv <= SP_RT; ++sv) {
         SpaceDev &V = c->sp[sv];
-        // ND stays on the element + merge passes unless LOR_XV_ND=1 (its extended-frame fill is
-        // still slower: DESIGN.md section 4); LOR_XV=0 turns the vector-space path off
+        // LOR_XV=0 turns the vector-space path off, LOR_XV_ND=0 for ND only (A/B against the
+        // element + merge passes)
         const char *xv_env = getenv("LOR_XV"), *xvnd_env = getenv("LOR_XV_ND");
-        if (!V.valid || (xv_env && !atoi(xv_env)) || (sv == SP_ND && !(xvnd_env && atoi(xvnd_env))) ||
+        if (!V.valid || (xv_env && !atoi(xv_env)) || (sv == SP_ND && xvnd_env && !atoi(xvnd_env)) ||
             !xv_supported(sv, A.p, S.xc))
           continue;
         if (dev_alloc(c, &V.xvmap, (size_t)c->nel_local * xv_map_words(sv, A.p, S.xc)) != cudaSuccess ||

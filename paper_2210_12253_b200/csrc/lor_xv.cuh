@@ -76,7 +76,9 @@ struct XvCfg {
   static constexpr int OFF_SC = OFF_ST + NROWS * W * 8;            // staged values [NROWS][W]
   static constexpr int OFF_XV = OFF_SC + NROWS * W * 4;            // staged columns [NROWS][W]
   static constexpr int OFF_MO = (OFF_XV + 3 * NVF * 4 + 15) / 16 * 16;  // restriction [3][NVF]
-  static constexpr int SMEM = OFF_MO + 16 * RPT;                   // per (rr, warp): staged entries
+  static constexpr int OFF_WE = (OFF_MO + 16 * RPT + 15) / 16 * 16;  // write-out: per warp 32 row ends
+  static constexpr int OFF_WD = OFF_WE + 4 * 32 * 4;                 //   and 32 destination offsets
+  static constexpr int SMEM = OFF_WD + 4 * 32 * 8;
 };
 
 // extent of family s along axis a in the box (cell-index axes: NB, point-index axes: NB + 1)
@@ -521,6 +523,8 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
   int32_t *stc = reinterpret_cast<int32_t *>(smem + CF::OFF_SC);
   uint32_t *XV = reinterpret_cast<uint32_t *>(smem + CF::OFF_XV);
   int32_t *m_wt = reinterpret_cast<int32_t *>(smem + CF::OFF_MO);  // per (rr, warp): staged entries
+  int32_t *w_end = reinterpret_cast<int32_t *>(smem + CF::OFF_WE);
+  int64_t *w_dst = reinterpret_cast<int64_t *>(smem + CF::OFF_WD);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bs = blockIdx.x;
   if (bs >= A.nel_local) return;
@@ -680,30 +684,24 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
       (void)t;
     }
     __syncthreads();
-    // write-out, each warp its own rows: maximal runs of consecutive rows whose CSR ranges are
-    // consecutive go out as one coalesced range with all 32 lanes
+    // write-out, each warp its own rows: the warp's staged range (its rows' entries, consecutive in
+    // staging) streamed with all 32 lanes; an entry's CSR position = its staged index + the
+    // destination offset of its row, found by a binary search over the warp's 32 staged row ends
 #pragma unroll
     for (int rr = 0; rr < CF::RPT; ++rr) {
-      const bool h = rs[rr] >= 0;
-      const int64_t o = rout[rr];
-      const int n = rn[rr], so = rso[rr];
-      const long long pend = __shfl_up_sync(0xffffffffu, (long long)(o + n), 1);
-      const bool ph = __shfl_up_sync(0xffffffffu, (int)h, 1) != 0;
-      const bool head = h && (lane == 0 || !ph || pend != o);
-      unsigned hb = __ballot_sync(0xffffffffu, head);
-      const unsigned brk = hb | ~__ballot_sync(0xffffffffu, h);
-      while (hb) {
-        const int h0 = __ffs(hb) - 1;
-        hb &= hb - 1;
-        const unsigned after = brk & (h0 == 31 ? 0u : (0xffffffffu << (h0 + 1)));
-        const int last = (after ? __ffs(after) - 1 : 32) - 1;
-        const int s0 = __shfl_sync(0xffffffffu, so, h0), s1 = __shfl_sync(0xffffffffu, so + n, last);
-        const long long o0 = __shfl_sync(0xffffffffu, (long long)o, h0);
-        for (int k = lane; k < s1 - s0; k += 32) {
-          if (WCOL) __stcs(A.col + o0 + k, stc[s0 + k]);
-          __stcs(A.val + o0 + k, stv[s0 + k]);
-        }
+      w_end[warp * 32 + lane] = rso[rr] + rn[rr];
+      w_dst[warp * 32 + lane] = rout[rr] - rso[rr];
+      __syncwarp();
+      const int S0 = __shfl_sync(0xffffffffu, rso[rr], 0), E0 = __shfl_sync(0xffffffffu, rso[rr] + rn[rr], 31);
+      for (int k = S0 + lane; k < E0; k += 32) {
+        int cur = 0;  // the entry's row: first of the warp's rows whose staged end exceeds k (5 steps)
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) cur += (w_end[warp * 32 + cur + st - 1] <= k) ? st : 0;
+        const int64_t d = w_dst[warp * 32 + cur] + k;
+        if (WCOL) __stcs(A.col + d, stc[k]);
+        __stcs(A.val + d, stv[k]);
       }
+      __syncwarp();
     }
     __syncthreads();
   }

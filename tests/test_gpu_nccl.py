@@ -1,7 +1,6 @@
 """NCCL path on >= 2 GPUs (skipped with fewer): one process per GPU, ncclUniqueId broadcast over
 torch.distributed.  Each rank's owned rows against the oracle's rank-major matrix:
-  * H1 and RT: single-pass extended frame with the ghost layer (no partial-row exchange);
-  * ND: element + merge passes with the interface partial rows over grouped ncclSend/ncclRecv;
+  * H1, ND and RT: single-pass extended frame with the ghost layer (no partial-row exchange);
   * after lor_update_coordinates with new (jittered) coordinates, whose ghost layer is refreshed from
     the peers over NCCL, the re-assembly matches the oracle on the moved mesh;
   * ParCSR split + A4 elimination with the boundary markers exchanged over NCCL on the side stream:

@@ -114,9 +114,9 @@ def test_multirank_emulated(torch_cuda, oracle_lib, space, nranks):
         c.sync()
     ref = oracle_lib.assemble(m, space, "vertex", 1.0, 1.0)
     for r, c in enumerate(ctxs):
-        # H1 and RT keep the single-pass extended frame on every rank (ghost layer of neighbour
-        # coordinates, no partial-row exchange); ND takes the element + merge passes + exchange
-        assert c.fill_path(space) == (0 if space == "nd" else 1)
+        # every space keeps the single-pass extended frame on every rank (ghost layer of neighbour
+        # coordinates, no partial-row exchange; the manual exchange calls are then no-ops)
+        assert c.fill_path(space) == 1
         q = c.query(space)
         rp, col, val = (to_host(t) for t in outs[r])
         compare_full(rp, col, val, ref, q["row_begin"], q["n_local"], f"{space} rank {r}/{nranks}")

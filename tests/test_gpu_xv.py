@@ -1,7 +1,8 @@
 """GPU parity of the extended-frame ("owner computes") path of the vector spaces (lor_xv.cuh,
 DESIGN.md section 4 "k_xv"): H(curl) Nedelec and H(div) Raviart-Thomas rows written complete by
 their owning element, the neighbour cells recomputed in its frame, orientation signs of the box
-dofs from the neighbours' restrictions.  RT takes this path by default; ND with LOR_XV_ND=1.  Both
+dofs from the neighbours' restrictions.  RT and ND take this path by default (LOR_XV=0 / LOR_XV_ND=0:
+the element + merge passes); ND at p >= 6 falls back to them when the frame does not fit.  Both
 are compared with the oracle element by element (bit-exact pattern, P-10b values), on meshes whose
 numbering is shuffled (ownership on every side of an element) and orientation-scrambled, for every
 p the instantiations cover."""
@@ -26,7 +27,8 @@ def torch_cuda():
 def run(O, m, space, expect_path, what):
     from paper_2210_12253_b200.lor import LOR
     ctx = LOR(m)
-    assert ctx.fill_path(space) == expect_path, what
+    if expect_path is not None:
+        assert ctx.fill_path(space) == expect_path, what
     q = ctx.query(space)
     rp, col, val = ctx.assemble(space, 1.3, 0.7, "vertex")
     ctx.sync()
@@ -50,17 +52,16 @@ def test_rt_xframe(torch_cuda, oracle_lib, p, kind):
     run(oracle_lib, m, "rt", 1, f"rt {kind} p={p}")
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("kind", ["scrambled", "shuffled", "kershaw"])
-def test_nd_xframe(torch_cuda, oracle_lib, monkeypatch, p, kind):
-    monkeypatch.setenv("LOR_XV_ND", "1")
+def test_nd_xframe(torch_cuda, oracle_lib, p, kind):
     if kind == "kershaw":
         m = mg.box_mesh(3, (6, 2, 2), p, kershaw=0.3)
     else:
         m = mg.box_mesh(3, (3, 3, 2), p, jitter=True, scramble=(kind == "scrambled"))
         if kind == "shuffled":
             m = shuffled(m, seed=10 + p)
-    run(oracle_lib, m, "nd", 1, f"nd {kind} p={p}")
+    run(oracle_lib, m, "nd", 1 if p <= 5 else None, f"nd {kind} p={p}")
 
 
 @pytest.mark.parametrize("space", ["rt", "nd"])
