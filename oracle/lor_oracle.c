@@ -202,6 +202,7 @@ static void rt_basis(const double *x, int f, double phi[3], double *div) {
 
 static int local_ndof(int dim, int space) {
   if (space == ORC_H1) return 1 << dim;
+  if (dim == 2) return 4;
   if (space == ORC_ND) return 12;
   return 6;
 }
@@ -231,7 +232,7 @@ static double corner_interp(int dim, const double *c, const double *x) {
 
 int orc_local_matrix_vc(int dim, int space, int quad, double alpha, double beta, const double *corners,
                         const double *ca8, const double *cb8, double *A) {
-  if (!(dim == 2 || dim == 3) || (dim == 2 && space != ORC_H1)) return ORC_ERR_ARG;
+  if (!(dim == 2 || dim == 3)) return ORC_ERR_ARG;
   int n = local_ndof(dim, space);
   for (int i = 0; i < n * n; ++i) A[i] = 0.0;
   double pts[8][3], w;
@@ -242,7 +243,30 @@ int orc_local_matrix_vc(int dim, int space, int quad, double alpha, double beta,
     double det = inverse(dim, J, Ji);
     if (!(det > 0.0)) return ORC_ERR_DEGENERATE;
     const double aq = alpha * corner_interp(dim, ca8, pts[q]), bq = beta * corner_interp(dim, cb8, pts[q]);
-    if (space == ORC_H1) {
+    if (dim == 2 && space != ORC_H1) { /* 2D lowest-order Nedelec / Raviart-Thomas on the quad */
+      double phi[4][2], sc[4];
+      for (int i = 0; i < 4; ++i) {
+        double ph[2], dv;
+        int fam = i / 2, off = i & 1;
+        if (space == ORC_ND) { /* x-edge at y = off: (f(y), 0); y-edge at x = off: (0, f(x)) */
+          int o = 1 - fam;
+          double f = off ? pts[q][o] : 1.0 - pts[q][o], df = off ? 1.0 : -1.0;
+          ph[fam] = f;
+          ph[o] = 0.0;
+          dv = fam == 0 ? -df : df; /* scalar curl = d phi_y/dx - d phi_x/dy */
+          for (int c = 0; c < 2; ++c) phi[i][c] = Ji[0][c] * ph[0] + Ji[1][c] * ph[1]; /* J^{-T} phi-hat */
+        } else { /* face normal e_fam at side off: e_fam (off ? x_fam : 1 - x_fam), div = off ? 1 : -1 */
+          ph[fam] = off ? pts[q][fam] : 1.0 - pts[q][fam];
+          ph[1 - fam] = 0.0;
+          dv = off ? 1.0 : -1.0;
+          for (int c = 0; c < 2; ++c) phi[i][c] = (J[c][0] * ph[0] + J[c][1] * ph[1]) / det; /* J phi-hat / det */
+        }
+        sc[i] = dv / det;
+      }
+      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j)
+          A[i * 4 + j] += w * (aq * sc[i] * sc[j] + bq * (phi[i][0] * phi[j][0] + phi[i][1] * phi[j][1])) * det;
+    } else if (space == ORC_H1) {
       double N[8], g[8][3];
       for (int i = 0; i < n; ++i) {
         double gr[3];
@@ -482,6 +506,7 @@ static int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e--) r *= b; retur
 
 static int64_t space_ndof_canonical(const topo_t *t, int space) {
   int p = t->p;
+  if (t->dim == 2 && space != ORC_H1) return t->ne * p + t->nel * 2 * (int64_t)p * (p - 1); /* 2D ND / RT */
   if (t->dim == 2) return t->nv + t->ne * (p - 1) + t->nel * (int64_t)(p - 1) * (p - 1);
   if (space == ORC_H1)
     return t->nv + t->ne * (p - 1) + t->nf * (int64_t)(p - 1) * (p - 1) + t->nel * ipow(p - 1, 3);
@@ -492,6 +517,7 @@ static int64_t space_ndof_canonical(const topo_t *t, int space) {
 
 static int ndof_per_el(int dim, int p, int space) {
   if (space == ORC_H1) return (int)ipow(p + 1, dim);
+  if (dim == 2) return 2 * p * (p + 1); /* 2D ND / RT: two families of lattice edges */
   if (space == ORC_ND) return 3 * p * (p + 1) * (p + 1);
   return 3 * p * p * (p + 1);
 }
@@ -549,6 +575,32 @@ static void canonical_dof(const orc_mesh *m, const topo_t *t, int space, int64_t
     int64_t lex = 0, stride = 1;
     for (int d = 0; d < dim; ++d) { lex += (x[d] - 1) * stride; stride *= (p - 1); }
     *gid = base + e * ipow(p - 1, dim) + lex;
+    return;
+  }
+  if (dim == 2) { /* 2D ND / RT (reading P-29): dofs on lattice edges */
+    int blk = p * (p + 1);
+    int d = l / blk, r = l % blk, o = 1 - d, x[2];
+    int ext0 = (space == ORC_ND) ? (d == 0 ? p : p + 1) : (d == 0 ? p + 1 : p);
+    x[0] = r % ext0;
+    x[1] = r / ext0;
+    /* ND family d: edges along d (cell index along d); RT family d: normal e_d, edges along o */
+    int along = (space == ORC_ND) ? d : o, across = 1 - along;
+    if (x[across] == 0 || x[across] == p) { /* on a coarse edge along `along` */
+      int le = 2 * along + (x[across] == p);
+      int tl, hd;
+      edge_corners(2, le, &tl, &hd);
+      int aligned = ev[tl] < ev[hd];
+      int k = aligned ? x[along] : p - 1 - x[along];
+      *gid = t->el_edge[e * 4 + le] * p + k;
+      /* ND: tangent in the global orientation; RT: global normal = the global tangent turned by
+       * +90 degrees, against the local normal +e_d (= the local +axis tangent turned: +1 for d = y,
+       * -1 for d = x) */
+      *sgn = (aligned ? 1 : -1) * ((space == ORC_RT && d == 0) ? -1 : 1);
+      return;
+    }
+    int lex = (space == ORC_ND) ? (d == 0 ? x[0] + p * (x[1] - 1) : (x[0] - 1) + (p - 1) * x[1])
+                                : (d == 0 ? (x[0] - 1) + (p - 1) * x[1] : x[0] + p * (x[1] - 1));
+    *gid = t->ne * p + e * 2 * (int64_t)p * (p - 1) + d * (int64_t)p * (p - 1) + lex;
     return;
   }
   if (space == ORC_ND) {
@@ -727,6 +779,16 @@ static int cell_dofs(int dim, int p, int space, const int *k, int *ldof) {
     }
     return 1 << dim;
   }
+  if (dim == 2) { /* ND: x-edges (b) -> b, y-edges (a) -> 2 + a; RT: faces 2d + side, normal +e_d */
+    for (int i = 0; i < 4; ++i) {
+      int fam = i / 2, off = i & 1, x[2] = {k[0], k[1]};
+      if (space == ORC_ND) x[1 - fam] += off;
+      else x[fam] += off;
+      int ext0 = (space == ORC_ND) ? (fam == 0 ? p : p + 1) : (fam == 0 ? p + 1 : p);
+      ldof[i] = fam * p * (p + 1) + x[0] + ext0 * x[1];
+    }
+    return 4;
+  }
   if (space == ORC_ND) {
     for (int eps = 0; eps < 12; ++eps) {
       int a = eps / 4, b1 = eps & 1, b2 = (eps >> 1) & 1;
@@ -836,10 +898,7 @@ static int check_mesh(const orc_mesh *m, int space) {
     snprintf(g_err, sizeof g_err, "invalid mesh");
     return ORC_ERR_ARG;
   }
-  if (m->dim == 2 && space != ORC_H1) {
-    snprintf(g_err, sizeof g_err, "2D supports H1 only");
-    return ORC_ERR_ARG;
-  }
+  (void)space;
   return ORC_OK;
 }
 
@@ -998,9 +1057,11 @@ int orc_topology_counts(const orc_mesh *m, int64_t *counts) {
  *            sigma_face * sigma_edge (App. A.5, reading P-15).
  * Every revisit of a row from another cell/element must produce the identical row.
  * ==================================================================================== */
+static int discrete_2d(const orc_mesh *m, int which, orc_csr *out);
 int orc_discrete(const orc_mesh *m, int which, orc_csr *out) {
   memset(out, 0, sizeof(*out));
-  if (!m || m->dim != 3 || m->p < 1) { snprintf(g_err, sizeof g_err, "3D only"); return ORC_ERR_ARG; }
+  if (m && m->dim == 2 && m->p >= 1 && (which == 0 || which == 2)) return discrete_2d(m, which, out);
+  if (!m || m->dim != 3 || m->p < 1 || which == 2) { snprintf(g_err, sizeof g_err, "3D only"); return ORC_ERR_ARG; }
   topo_t t;
   int rc = topo_build(m, &t);
   if (rc) return rc;
@@ -1084,6 +1145,81 @@ int orc_discrete(const orc_mesh *m, int which, orc_csr *out) {
       if (!done[r]) { rc = ORC_ERR_INCONSISTENT; snprintf(g_err, sizeof g_err, "row never visited"); }
     }
     for (int64_t i = 0; i < n * w; ++i) { out->col[i] = (int32_t)cols[i]; out->val[i] = vals[i]; }
+  }
+  free(cols); free(vals); free(done);
+  topo_free(&t); numbering_free(&nr); numbering_free(&ncn);
+  return rc;
+}
+
+/* 2D discrete gradient (which = 0: rows ND, Algorithm 1: -sigma at the LOR edge's tail, +sigma at its
+ * head) and rotated gradient (which = 2: rows RT; grad-perp = (-d/dy, d/dx): the
+ * flux of grad-perp u through an edge with normal n = tau turned by +90 degrees is u(head of tau) -
+ * u(tail of tau); the local normal +e_d has tau = +e_x for d = y and tau = -e_y for d = x), times the
+ * row's sign; columns sorted; every revisit of a row must give the identical row (reading P-29). */
+static int discrete_2d(const orc_mesh *m, int which, orc_csr *out) {
+  topo_t t;
+  int rc = topo_build(m, &t);
+  if (rc) return rc;
+  int rsp = which == 0 ? ORC_ND : ORC_RT;
+  numbering_t nr, ncn;
+  if ((rc = numbering_build(m, &t, rsp, &nr))) { topo_free(&t); return rc; }
+  if ((rc = numbering_build(m, &t, ORC_H1, &ncn))) { topo_free(&t); numbering_free(&nr); return rc; }
+  int64_t n = nr.n;
+  int64_t *cols = (int64_t *)malloc(sizeof(int64_t) * n * 2);
+  double *vals = (double *)malloc(sizeof(double) * n * 2);
+  char *done = (char *)calloc(n, 1);
+  int p = m->p, nc = ncells_dim(p, 2);
+  for (int64_t e = 0; e < m->nel && !rc; ++e)
+    for (int ic = 0; ic < nc && !rc; ++ic) {
+      int k[3];
+      cell_index(p, 2, ic, k);
+      int ldof[12];
+      cell_dofs(2, p, rsp, k, ldof);
+      for (int i = 0; i < 4; ++i) {
+        int64_t row = nr.map[e * nr.ndpe + ldof[i]];
+        double sr = nr.sign[e * nr.ndpe + ldof[i]];
+        int fam = i / 2, off = i & 1, ta[2], ha[2]; /* cell-local corners (x, y) of the edge's tail / head */
+        if (which == 0) { /* ND edge along fam at offset off across: tail lower end */
+          ta[fam] = 0; ha[fam] = 1; ta[1 - fam] = ha[1 - fam] = off;
+        } else if (fam == 1) { /* RT normal y: horizontal edge y = off, tau = +e_x */
+          ta[0] = 0; ha[0] = 1; ta[1] = ha[1] = off;
+        } else { /* RT normal x: vertical edge x = off, tau = -e_y */
+          ta[1] = 1; ha[1] = 0; ta[0] = ha[0] = off;
+        }
+        int64_t c[2] = {ncn.map[e * ncn.ndpe + h1_lidx(2, p, k[0] + ta[0], k[1] + ta[1], 0)],
+                        ncn.map[e * ncn.ndpe + h1_lidx(2, p, k[0] + ha[0], k[1] + ha[1], 0)]};
+        double v[2] = {-sr, sr};
+        if (c[1] < c[0]) {
+          int64_t tc = c[0]; c[0] = c[1]; c[1] = tc;
+          double tv = v[0]; v[0] = v[1]; v[1] = tv;
+        }
+        if (done[row]) {
+          for (int a = 0; a < 2; ++a)
+            if (cols[row * 2 + a] != c[a] || vals[row * 2 + a] != v[a]) {
+              snprintf(g_err, sizeof g_err, "inconsistent 2D %s row %lld", which ? "rotated gradient" : "G",
+                       (long long)row);
+              rc = ORC_ERR_INCONSISTENT;
+            }
+        } else {
+          done[row] = 1;
+          for (int a = 0; a < 2; ++a) { cols[row * 2 + a] = c[a]; vals[row * 2 + a] = v[a]; }
+        }
+      }
+    }
+  if (!rc) {
+    out->n_rows = n;
+    out->n_cols = ncn.n;
+    out->nnz = n * 2;
+    out->row_ptr = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+    out->row_id = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    out->col = (int32_t *)malloc(sizeof(int32_t) * n * 2);
+    out->val = (double *)malloc(sizeof(double) * n * 2);
+    for (int64_t r = 0; r <= n; ++r) out->row_ptr[r] = r * 2;
+    for (int64_t r = 0; r < n; ++r) {
+      out->row_id[r] = r;
+      if (!done[r]) { rc = ORC_ERR_INCONSISTENT; snprintf(g_err, sizeof g_err, "row never visited"); }
+    }
+    for (int64_t i = 0; i < n * 2; ++i) { out->col[i] = (int32_t)cols[i]; out->val[i] = vals[i]; }
   }
   free(cols); free(vals); free(done);
   topo_free(&t); numbering_free(&nr); numbering_free(&ncn);

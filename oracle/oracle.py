@@ -142,10 +142,10 @@ def assemble_rows(mesh, rows, space="h1", quad="vertex", alpha=1.0, beta=1.0, nr
 
 
 def discrete(mesh, which="grad", nranks=None) -> Csr:
-    """O7: discrete gradient (ND x H1) or curl (RT x ND), all rows."""
+    """O7: discrete gradient (ND x H1), curl (RT x ND, 3D) or 2D rotated gradient (RT x H1), all rows."""
     om = OracleMesh(mesh, nranks)
     c = _Csr()
-    _check(lib().orc_discrete(C.byref(om.s), 0 if which == "grad" else 1, C.byref(c)))
+    _check(lib().orc_discrete(C.byref(om.s), {"grad": 0, "curl": 1, "rotgrad": 2}[which], C.byref(c)))
     return _take(c)
 
 
@@ -179,7 +179,7 @@ def topology_counts(mesh):
 def local_matrix(dim, space, quad, alpha, beta, corners, ca8=None, cb8=None) -> np.ndarray:
     """O4 on one cell: corners [2^dim, dim] in local order a + 2b + 4c; ca8 / cb8 = corner values of the
     variable coefficients (None: constants)."""
-    n = {"h1": 1 << dim, "nd": 12, "rt": 6}[space]
+    n = {"h1": 1 << dim, "nd": 12 if dim == 3 else 4, "rt": 6 if dim == 3 else 4}[space]
     A = np.zeros((n, n))
     cr = np.ascontiguousarray(corners, dtype=np.float64)
     ap = None if ca8 is None else np.ascontiguousarray(ca8, dtype=np.float64)
