@@ -103,7 +103,8 @@ const char *lor_last_error(lor_ctx ctx);
 lor_status lor_query(lor_ctx ctx, lor_space space, int64_t *n_rows_local, int64_t *row_begin,
                      int64_t *n_rows_global, int64_t *nnz_local);
 /* which = 0: discrete gradient (rows: owned ND dofs, cols: global H1 dofs);
- * which = 1: discrete curl (rows: owned RT dofs, cols: global ND dofs; dim == 3). */
+ * which = 1: discrete curl (rows: owned RT dofs, cols: global ND dofs; dim == 3);
+ * which = 2: rotated gradient (rows: RT dofs, cols: H1 dofs; dim == 2, one rank). */
 lor_status lor_query_discrete(lor_ctx ctx, int which, int64_t *n_rows_local, int64_t *nnz_local,
                               int64_t *n_cols_global);
 
@@ -112,7 +113,9 @@ lor_status lor_query_discrete(lor_ctx ctx, int which, int64_t *n_rows_local, int
  * column/value fill (A2), and on nranks > 1 the interface exchange over NCCL that replaces the
  * P^T A P triple product (A3).  Forms: H1 alpha grad.grad + beta mass; ND alpha curl.curl +
  * beta mass; RT alpha div.div + beta mass (constant coefficients, reading P-2).
- * ND/RT with dim == 2 -> UNSUPPORTED.  Output: row_ptr[n_rows_local+1], col/val[nnz_local]. */
+ * ND/RT with dim == 2 (NEXT-2; reading P-29): one rank (UNSUPPORTED
+ * otherwise), lattice-edge dofs, scalar curl / divergence, assembled from the signed 4x4 cell
+ * matrices (lor_vec2d.cu).  Output: row_ptr[n_rows_local+1], col/val[nnz_local]. */
 lor_status lor_assemble_h1(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
 lor_status lor_assemble_nd(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
 lor_status lor_assemble_rt(lor_ctx ctx, double alpha, double beta, lor_quad quad, lor_csr *out);
@@ -134,6 +137,11 @@ lor_status lor_reassemble_rt(lor_ctx ctx, double alpha, double beta, lor_quad qu
  * orientation), columns sorted; row_ptr[f] = 4f.  No communication. */
 lor_status lor_discrete_grad(lor_ctx ctx, lor_csr *out);
 lor_status lor_discrete_curl(lor_ctx ctx, lor_csr *out);
+/* 2D rotated gradient grad-perp = (-d/dy, d/dx): H1 -> H(div) for grad-div problems with AMS (PAPER.md
+ * l.409-410): row of an RT dof = +-1 at the H1 ids of its lattice edge's end points, the flux of
+ * grad-perp u through the edge (u at the head minus u at the tail of the tangent that turns into the
+ * dof's normal by +90 degrees), times the dof's sign; row_ptr[f] = 2f.  dim == 2, one rank. */
+lor_status lor_discrete_rotgrad(lor_ctx ctx, lor_csr *out);
 
 /* Element restriction of `space` for this rank's elements:
  * elem_dofs[n_elem_local][ndof_per_el] global ids in the macro-element local order of

@@ -49,13 +49,13 @@ def _local_on_facet(dim, p, space, n, side):
             if x[n] == xn:
                 out.append(l)
         return out
-    # 3D vector spaces: family a, extents (ND: p along a, p+1 elsewhere; RT: p+1 along a, p elsewhere)
+    # vector spaces: family a, extents (ND: p along a, p+1 elsewhere; RT: p+1 along a, p elsewhere)
     off = 0
-    for a in range(3):
-        ext = [(p if b == a else p + 1) if space == "nd" else (p + 1 if b == a else p) for b in range(3)]
+    for a in range(dim):
+        ext = [(p if b == a else p + 1) if space == "nd" else (p + 1 if b == a else p) for b in range(dim)]
         tangential = (a != n) if space == "nd" else (a == n)
         for r in range(int(np.prod(ext))):
-            x = [r % ext[0], (r // ext[0]) % ext[1], r // (ext[0] * ext[1])]
+            x = [r % ext[0], (r // ext[0]) % ext[1]] + ([r // (ext[0] * ext[1])] if dim == 3 else [])
             if tangential and x[n] == xn:
                 out.append(off + r)
         off += int(np.prod(ext))

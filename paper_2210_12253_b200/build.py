@@ -112,6 +112,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     jobs = [(os.path.join(CSRC, "lor_kernels.cu"), os.path.join(BUILD, "lor_kernels.o")),
             (os.path.join(CSRC, "lor_parcsr.cu"), os.path.join(BUILD, "lor_parcsr.o")),
             (os.path.join(CSRC, "lor_legacy.cu"), os.path.join(BUILD, "lor_legacy.o")),
+            (os.path.join(CSRC, "lor_vec2d.cu"), os.path.join(BUILD, "lor_vec2d.o")),
             (os.path.join(CSRC, "lor_capi.cu"), os.path.join(BUILD, "lor_capi.o")),
             (os.path.join(CSRC, "lor_plan.cpp"), os.path.join(BUILD, "lor_plan.o")),
             (os.path.join(CSRC, "lor_xframe.cpp"), os.path.join(BUILD, "lor_xframe.o")),

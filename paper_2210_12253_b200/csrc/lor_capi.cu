@@ -18,6 +18,7 @@
 #include "lor_legacy.h"
 #include "lor_parcsr.h"
 #include "lor_plan.h"
+#include "lor_vec2d.h"
 #include "lor_xframe.h"
 
 // ---- minimal NCCL ABI (loaded with dlopen only when nranks > 1) ----------------------------------
@@ -114,6 +115,7 @@ struct SpaceDev {
   std::vector<int64_t> rank_off;  // [nranks+1] row ranges of the ranks (column ownership)
   int64_t *droff = nullptr;       // device copy
   std::vector<int32_t> bnd;       // owned boundary rows (local, ascending; lor_boundary_dofs)
+  int64_t key_lo = 0, key_hi = 0; // column-id range of the extended-frame restriction (sort keys)
 };
 
 // ParCSR split (A3 layout) and essential-BC elimination (A4, l.376-388) of one
@@ -177,6 +179,19 @@ struct lor_ctx_s {
   int32_t *leg_lmap = nullptr, *leg_ent = nullptr;
   double *leg_lx = nullptr, *leg_ea = nullptr;
   int64_t *leg_off = nullptr;
+  // 2D Nedelec / Raviart-Thomas (lor_vec2d.cu, one rank): per space the element restriction with
+  // signs, the row writers of the discrete operators, the LOR cells' signed dofs, the dof -> cell
+  // transpose, the cell matrices, sizes and the boundary dofs
+  struct Vec2 {
+    bool ok = false;
+    int64_t n = 0, nnz = 0, ncell = 0;
+    int32_t *map = nullptr, *cmap = nullptr, *ent = nullptr, *cnt = nullptr;
+    int8_t *sgn = nullptr, *csgn = nullptr;
+    uint8_t *writer = nullptr;
+    int64_t *off = nullptr, *rp = nullptr;
+    double *ea = nullptr;
+    std::vector<int32_t> bnd;
+  } v2[3];
   bool vc = false;
   cudaStream_t side = nullptr;       // marker exchange stream (overlap)
   cudaEvent_t ev_pack = nullptr, ev_xchg = nullptr;
@@ -314,7 +329,10 @@ XFillArgs xfill_args(lor_ctx c, const SpaceDev &S) {
   x.row_begin = S.row_begin;
   x.cnt = S.cnt;
   x.pos = S.xpos;
-  x.sort32 = (S.n_global < (int64_t(1) << 26) && !(c->dbg & 1)) ? 1 : 0;  // LOR_DBG bit 0: force the rank path
+  // keys relative to the lowest column id the rank's extended restriction references (setup)
+  const int64_t klo = S.key_lo, khi = S.key_hi;
+  x.key_base = (int)klo;
+  x.sort32 = (khi - klo < (int64_t(1) << 26) && !(c->dbg & 1)) ? 1 : 0;  // LOR_DBG bit 0: force the rank path
   x.ncx = S.xc[0];
   x.ncy = S.xc[1];
   x.ncz = S.xc[2];
@@ -344,15 +362,22 @@ XvArgs xv_args(lor_ctx c, int s) {
   x.ncz = H.xc[2];
   x.err = c->err;
   const int sb = s == SP_ND ? 6 : 4;  // slot bits of the packed sort keys
-  x.sort32 = (S.n_global < (int64_t(1) << (31 - sb)) && !(c->dbg & 1)) ? 1 : 0;
+  const int64_t klo = S.key_lo, khi = S.key_hi;
+  x.key_base = (int)klo;
+  x.sort32 = (khi - klo < (int64_t(1) << (31 - sb)) && !(c->dbg & 1)) ? 1 : 0;
   return x;
 }
 
 // reuse = true: numeric-only re-assembly into buffers holding the pattern of an earlier full call of
 // the same space (NEXT-3): no row lengths, no scan; the extended-frame path
 // stores values only.
+lor_status vec2d_assemble(lor_ctx c, int sp, double alpha, double beta, lor_quad quad, lor_csr *out);
 lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, lor_csr *out, bool reuse = false) {
   if (!c) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim == 2 && (s == SP_ND || s == SP_RT)) {  // 2D vector spaces (lor_vec2d.cu)
+    if (quad != LOR_QUAD_VERTEX && quad != LOR_QUAD_GAUSS2) return fail(c, LOR_ERR_INVALID_ARGUMENT, "bad quadrature");
+    return vec2d_assemble(c, s, alpha, beta, quad, out);
+  }
   if (s < 0 || s > 2 || !c->sp[s].valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available for this mesh");
   if (quad != LOR_QUAD_VERTEX && quad != LOR_QUAD_GAUSS2) return fail(c, LOR_ERR_INVALID_ARGUMENT, "bad quadrature");
   SpaceDev &S = c->sp[s];
@@ -568,6 +593,114 @@ lor_status exchange_ghost_coords(lor_ctx c) {
     }
   }
   if (g_nccl.GroupEnd() != ncclSuccess) return fail(c, LOR_ERR_NCCL, "ncclGroupEnd");
+  return LOR_OK;
+}
+
+// 2D Nedelec / Raviart-Thomas numbering (reading P-29, one rank): family d of the local
+// order holds the lattice edges along d (ND) / normal to d (RT); a dof on coarse edge E has id
+// E p + k with k the cell index along the edge's global orientation (min -> max vertex id) and sign
+// +-1 for ND by alignment, for RT by the global normal (global tangent turned by +90 degrees)
+// against the local normal +e_d; element interiors follow as ne p + el 2p(p-1) + d p(p-1) + lex.
+bool vec2d_setup(lor_ctx c, const HostPlan &plan, std::string &why) {
+  const int p = c->p, ndpe = 2 * p * (p + 1);
+  const int64_t nel = c->nel_local, ne = plan.n_ent[1], ncell = nel * p * p;
+  const SpaceDev &H = c->sp[SP_H1];
+  if (!H.emap) { why = "needs the H1 element restriction"; return false; }
+  for (int sp = SP_ND; sp <= SP_RT; ++sp) {
+    lor_ctx_s::Vec2 &V = c->v2[sp];
+    V.n = ne * p + nel * 2 * (int64_t)p * (p - 1);
+    V.ncell = ncell;
+    std::vector<int32_t> map((size_t)nel * ndpe);
+    std::vector<int8_t> sgn((size_t)nel * ndpe);
+    std::vector<uint8_t> wr((size_t)nel * ndpe);
+    for (int64_t e = 0; e < nel; ++e)
+      for (int l = 0; l < ndpe; ++l) {
+        const int d = l / (p * (p + 1)), r = l % (p * (p + 1));
+        const int ext0 = sp == SP_ND ? (d == 0 ? p : p + 1) : (d == 0 ? p + 1 : p);
+        const int x[2] = {r % ext0, r / ext0};
+        const int along = sp == SP_ND ? d : 1 - d, across = 1 - along;
+        int64_t g;
+        int sg = 1, w = 1;
+        if (x[across] == 0 || x[across] == p) {
+          const int le = 2 * along + (x[across] == p);
+          const int64_t E = plan.el_edge[e * 4 + le];
+          const bool aligned = !plan.el_edge_rev[e * 4 + le];
+          g = E * p + (aligned ? x[along] : p - 1 - x[along]);
+          sg = (aligned ? 1 : -1) * ((sp == SP_RT && d == 0) ? -1 : 1);
+          w = plan.inc_el[1][plan.inc_off[1][E]] == plan.elem_begin + e;
+        } else {
+          const int lex = sp == SP_ND ? (d == 0 ? x[0] + p * (x[1] - 1) : (x[0] - 1) + (p - 1) * x[1])
+                                      : (d == 0 ? (x[0] - 1) + (p - 1) * x[1] : x[0] + p * (x[1] - 1));
+          g = ne * p + e * 2 * (int64_t)p * (p - 1) + d * (int64_t)p * (p - 1) + lex;
+        }
+        map[e * ndpe + l] = (int32_t)g;
+        sgn[e * ndpe + l] = (int8_t)sg;
+        wr[e * ndpe + l] = (uint8_t)w;
+      }
+    V.bnd.clear();
+    for (int64_t E = 0; E < ne; ++E)
+      if (plan.inc_off[1][E + 1] - plan.inc_off[1][E] == 1)
+        for (int k = 0; k < p; ++k) V.bnd.push_back((int32_t)(E * p + k));
+    if (dev_upload(c, &V.map, map.data(), map.size()) || dev_upload(c, &V.sgn, sgn.data(), sgn.size()) ||
+        dev_upload(c, &V.writer, wr.data(), wr.size()) || dev_alloc(c, &V.cmap, ncell * 4) ||
+        dev_alloc(c, &V.csgn, ncell * 4) || dev_alloc(c, &V.ent, ncell * 4) || dev_alloc(c, &V.off, V.n + 1) ||
+        dev_alloc(c, &V.rp, V.n + 1) || dev_alloc(c, &V.cnt, V.n + 1) || dev_alloc(c, &V.ea, ncell * 16)) {
+      why = "out of memory";
+      return false;
+    }
+    if (launch_v2_cells(sp, p, nel, V.map, V.sgn, V.cmap, V.csgn, c->stream) != cudaSuccess ||
+        launch_transpose(V.cmap, ncell * 4, 0, V.n, V.cnt, V.off, V.ent, H.scan_status, H.tile_ctr, c->stream) !=
+            cudaSuccess) {
+      why = "cells / transpose";
+      return false;
+    }
+    // the pattern is topological: its size once, from the count pass
+    V2Rows r{V.n, V.off, V.ent, V.cmap, V.ea, V.rp, nullptr, nullptr, V.cnt};
+    if (launch_v2_rows(r, false, c->stream) != cudaSuccess ||
+        launch_scan(V.cnt, V.rp, V.n, H.scan_status, H.tile_ctr, c->stream) != cudaSuccess ||
+        cudaMemcpyAsync(&V.nnz, V.rp + V.n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess) {
+      why = "pattern size";
+      return false;
+    }
+    V.ok = true;
+  }
+  return true;
+}
+
+lor_status vec2d_assemble(lor_ctx c, int sp, double alpha, double beta, lor_quad quad, lor_csr *out) {
+  lor_ctx_s::Vec2 &V = c->v2[sp];
+  if (!V.ok) return fail(c, LOR_ERR_UNSUPPORTED, "2D ND / RT: one rank only");
+  if (!out || !out->row_ptr || (V.nnz > 0 && (!out->col || !out->val))) return fail(c, LOR_ERR_INVALID_ARGUMENT, "null output buffer");
+  if (out->cap_nnz < V.nnz) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < nnz_local");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  const SpaceDev &H = c->sp[SP_H1];
+  c->nphase = 0;
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  V2Args a{c->p, V.ncell, c->X, c->xstride, c->vc ? c->ca : nullptr, c->vc ? c->cb : nullptr, alpha, beta, V.csgn,
+           V.ea, c->err};
+  CUDA_TRY(c, launch_v2_ea(sp, (int)quad, a, c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  V2Rows r{V.n, V.off, V.ent, V.cmap, V.ea, out->row_ptr, out->col, out->val, V.cnt};
+  CUDA_TRY(c, launch_v2_rows(r, false, c->stream));
+  CUDA_TRY(c, launch_scan(V.cnt, out->row_ptr, V.n, H.scan_status, H.tile_ctr, c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  CUDA_TRY(c, launch_v2_rows(r, true, c->stream));
+  CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+  c->launches += 4;
+  return LOR_OK;
+}
+
+lor_status vec2d_discrete(lor_ctx c, int sp, lor_csr *out) {
+  lor_ctx_s::Vec2 &V = c->v2[sp];
+  if (!V.ok) return fail(c, LOR_ERR_UNSUPPORTED, "2D discrete operators: one rank only");
+  if (!out || !out->row_ptr || !out->col || !out->val) return fail(c, LOR_ERR_INVALID_ARGUMENT, "null output buffer");
+  if (out->cap_nnz < 2 * V.n) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 2 n_rows");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, V.n, 2, c->stream));
+  V2Disc d{sp, c->p, c->nel_local, 0, V.map, V.sgn, V.writer, c->sp[SP_H1].emap, out->col, out->val};
+  CUDA_TRY(c, launch_v2_disc(d, c->stream));
+  c->launches += 2;
   return LOR_OK;
 }
 
@@ -1100,6 +1233,32 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
       fprintf(stderr, "lor_setup: extended-frame path off: %s\n", why.c_str());
     }
   }
+  // column-id range each extended-frame space references (its restriction): the symbolic pass sorts
+  // keys relative to key_lo, packed in 32 bits when the range allows
+  for (int s2 = 0; s2 < 3; ++s2) {
+    SpaceDev &S2 = c->sp[s2];
+    const uint32_t *m = s2 == SP_H1 ? (S2.xok ? reinterpret_cast<const uint32_t *>(S2.xmap) : nullptr)
+                                    : (S2.xvok ? S2.xvmap : nullptr);
+    if (!m) continue;
+    const int64_t words = c->nel_local * (s2 == SP_H1 ? xmap_points(A.p, c->sp[SP_H1].xc)
+                                                      : xv_map_words(s2, A.p, c->sp[SP_H1].xc));
+    std::vector<uint32_t> h((size_t)words);
+    if (cudaMemcpy(h.data(), m, sizeof(uint32_t) * words, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return bail(LOR_ERR_CUDA, "key range");
+    int64_t lo = INT64_MAX, hi = -1;
+    for (uint32_t v : h) {
+      if (v == 0xffffffffu) continue;
+      const int64_t g = v & 0x7fffffffu;
+      lo = std::min(lo, g);
+      hi = std::max(hi, g);
+    }
+    S2.key_lo = hi < 0 ? 0 : lo;
+    S2.key_hi = hi + 1;
+  }
+  if (A.dim == 2 && A.nranks == 1) {
+    std::string why2;
+    if (!vec2d_setup(c, plan, why2)) return bail(LOR_ERR_CUDA, "2D vector spaces: " + why2);
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(LOR_ERR_CUDA, "setup sync");
   *out = c;
   return LOR_OK;
@@ -1143,6 +1302,15 @@ const char *lor_last_error(lor_ctx c) { return c ? c->last_error.c_str() : g_set
 lor_status lor_query(lor_ctx c, lor_space space, int64_t *n_rows_local, int64_t *row_begin, int64_t *n_rows_global,
                      int64_t *nnz_local) {
   if (!c || space < 0 || space > 2) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim == 2 && space != LOR_H1) {
+    const lor_ctx_s::Vec2 &V = c->v2[space];
+    if (!V.ok) return fail(c, LOR_ERR_UNSUPPORTED, "2D ND / RT: one rank only");
+    if (n_rows_local) *n_rows_local = V.n;
+    if (row_begin) *row_begin = 0;
+    if (n_rows_global) *n_rows_global = V.n;
+    if (nnz_local) *nnz_local = V.nnz;
+    return LOR_OK;
+  }
   const SpaceDev &S = c->sp[space];
   if (!S.valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
   if (n_rows_local) *n_rows_local = S.n_local;
@@ -1153,7 +1321,16 @@ lor_status lor_query(lor_ctx c, lor_space space, int64_t *n_rows_local, int64_t 
 }
 
 lor_status lor_query_discrete(lor_ctx c, int which, int64_t *n_rows_local, int64_t *nnz_local, int64_t *n_cols_global) {
-  if (!c || (which != 0 && which != 1)) return LOR_ERR_INVALID_ARGUMENT;
+  if (!c || which < 0 || which > 2) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim == 2 && which != 1) {  // 2D: gradient (ND rows) and rotated gradient (RT rows)
+    const lor_ctx_s::Vec2 &V = c->v2[which == 0 ? SP_ND : SP_RT];
+    if (!V.ok) return fail(c, LOR_ERR_UNSUPPORTED, "2D discrete operators: one rank only");
+    if (n_rows_local) *n_rows_local = V.n;
+    if (nnz_local) *nnz_local = 2 * V.n;
+    if (n_cols_global) *n_cols_global = c->sp[SP_H1].n_global;
+    return LOR_OK;
+  }
+  if (which == 2) return fail(c, LOR_ERR_UNSUPPORTED, "the rotated gradient is 2D");
   if (c->dim != 3) return fail(c, LOR_ERR_UNSUPPORTED, "discrete operators need dim == 3");
   const SpaceDev &R = c->sp[which == 0 ? SP_ND : SP_RT];
   const SpaceDev &C = c->sp[which == 0 ? SP_H1 : SP_ND];
@@ -1291,8 +1468,15 @@ lor_status lor_assemble_finish(lor_ctx c, lor_space space, lor_csr *out) {
   return LOR_OK;
 }
 
+lor_status lor_discrete_rotgrad(lor_ctx c, lor_csr *out) {
+  if (!c || !out) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim != 2) return fail(c, LOR_ERR_UNSUPPORTED, "the rotated gradient is 2D");
+  return vec2d_discrete(c, SP_RT, out);
+}
+
 lor_status lor_discrete_grad(lor_ctx c, lor_csr *out) {
   if (!c || !out) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim == 2) return vec2d_discrete(c, SP_ND, out);
   if (c->dim != 3) return fail(c, LOR_ERR_UNSUPPORTED, "dim == 3 only");
   const SpaceDev &R = c->sp[SP_ND];
   if (out->cap_nnz < 2 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 2 n_rows");
@@ -1347,6 +1531,14 @@ lor_status lor_discrete_curl(lor_ctx c, lor_csr *out) {
 
 lor_status lor_dof_map(lor_ctx c, lor_space space, int32_t *elem_dofs, int8_t *signs) {
   if (!c || space < 0 || space > 2 || !elem_dofs) return LOR_ERR_INVALID_ARGUMENT;
+  if (c->dim == 2 && space != LOR_H1) {
+    const lor_ctx_s::Vec2 &V = c->v2[space];
+    if (!V.ok) return fail(c, LOR_ERR_UNSUPPORTED, "2D ND / RT: one rank only");
+    const size_t n = (size_t)c->nel_local * 2 * c->p * (c->p + 1);
+    CUDA_TRY(c, cudaMemcpyAsync(elem_dofs, V.map, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+    if (signs) CUDA_TRY(c, cudaMemcpyAsync(signs, V.sgn, n, cudaMemcpyDeviceToDevice, c->stream));
+    return LOR_OK;
+  }
   const SpaceDev &S = c->sp[space];
   if (!S.valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
   CUDA_TRY(c, cudaSetDevice(c->device));
@@ -1417,6 +1609,7 @@ lor_status lor_coordinates(lor_ctx c, double *xyz) {
   a.row_begin = S.row_begin;
   a.n_local = S.n_local;
   a.out = xyz;
+  a.emap = S.emap;
   CUDA_TRY(c, launch_coords(c->dim, a, c->stream));
   if (c->nel_local > 0) c->launches++;
   return LOR_OK;
@@ -1426,9 +1619,10 @@ lor_status lor_query_elements(lor_ctx c, int64_t *elem_begin, int64_t *n_elem_lo
   if (!c) return LOR_ERR_INVALID_ARGUMENT;
   if (elem_begin) *elem_begin = c->elem_begin;
   if (n_elem_local) *n_elem_local = c->nel_local;
+  const int nv2 = c->dim == 2 ? 2 * c->p * (c->p + 1) : 0;  // 2D ND / RT: lattice edges
   if (nh1) *nh1 = c->sp[0].ndpe;
-  if (nnd) *nnd = c->sp[1].ndpe;
-  if (nrt) *nrt = c->sp[2].ndpe;
+  if (nnd) *nnd = c->dim == 2 ? nv2 : c->sp[1].ndpe;
+  if (nrt) *nrt = c->dim == 2 ? nv2 : c->sp[2].ndpe;
   return LOR_OK;
 }
 
@@ -1648,13 +1842,15 @@ lor_status lor_parcsr_fill(lor_ctx c, int op, const lor_csr *A, lor_parcsr *M) {
 
 lor_status lor_boundary_dofs(lor_ctx c, lor_space space, int32_t *rows, int64_t cap, int64_t *n) {
   if (!c || space < 0 || space > 2 || !n) return LOR_ERR_INVALID_ARGUMENT;
-  const SpaceDev &S = c->sp[space];
-  if (!S.valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
-  *n = (int64_t)S.bnd.size();
+  const bool v2 = c->dim == 2 && space != LOR_H1;
+  if (v2 && !c->v2[space].ok) return fail(c, LOR_ERR_UNSUPPORTED, "2D ND / RT: one rank only");
+  if (!v2 && !c->sp[space].valid) return fail(c, LOR_ERR_UNSUPPORTED, "space not available");
+  const std::vector<int32_t> &B = v2 ? c->v2[space].bnd : c->sp[space].bnd;
+  *n = (int64_t)B.size();
   if (!rows) return LOR_OK;
   if (cap < *n) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap < number of boundary dofs");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  if (*n > 0) CUDA_TRY(c, cudaMemcpy(rows, S.bnd.data(), sizeof(int32_t) * *n, cudaMemcpyHostToDevice));
+  if (*n > 0) CUDA_TRY(c, cudaMemcpy(rows, B.data(), sizeof(int32_t) * *n, cudaMemcpyHostToDevice));
   return LOR_OK;
 }
 

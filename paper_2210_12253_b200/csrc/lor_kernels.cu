@@ -693,8 +693,35 @@ __global__ void __launch_bounds__(128) k_coords(CoordArgs A) {
   }
 }
 
+// With the setup element restriction: one thread per (element, point) over the flat E-vector order --
+// the point's global id from the restriction (coalesced), the writer test from its entity slot's
+// flags in the element's topology record, its coordinates from the E-vector (coalesced).
+template <int DIM>
+__global__ void __launch_bounds__(256) k_coords_flat(CoordArgs A) {
+  const int np1 = A.p + 1, npt = DIM == 3 ? np1 * np1 * np1 : np1 * np1;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.nel_local * npt) return;
+  const int64_t e = t / npt;
+  const int l = (int)(t - e * npt);
+  const int x0 = l % np1, x1 = (l / np1) % np1, x2 = DIM == 3 ? l / (np1 * np1) : 0;
+  auto cls = [&](int x) { return x == 0 ? 0 : (x == A.p ? 2 : 1); };
+  const int tau = cls(x0) + 3 * cls(x1) + (DIM == 3 ? 9 * cls(x2) : 0);
+  const uint8_t f = __ldg(&A.topo[e].flags[tau]);
+  if ((f & (TF_MIN | TF_OWNED)) != (TF_MIN | TF_OWNED)) return;
+  const int64_t r = (int64_t)__ldg(A.emap + t) - A.row_begin;
+  const double *xe = A.X + e * A.xstride + l;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) __stcs(A.out + d * A.n_local + r, __ldg(xe + d * npt));
+}
+
 cudaError_t launch_coords(int dim, const CoordArgs &a, cudaStream_t st) {
   if (a.nel_local <= 0) return cudaSuccess;
+  if (a.emap) {
+    const int64_t n = a.nel_local * (dim == 3 ? (int64_t)(a.p + 1) * (a.p + 1) * (a.p + 1) : (int64_t)(a.p + 1) * (a.p + 1));
+    if (dim == 2) k_coords_flat<2><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
+    else k_coords_flat<3><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
+    return cudaGetLastError();
+  }
   if (dim == 2) k_coords<2><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
   else k_coords<3><<<(unsigned)a.nel_local, 128, 0, st>>>(a);
   return cudaGetLastError();

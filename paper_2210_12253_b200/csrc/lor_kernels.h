@@ -183,6 +183,7 @@ struct CoordArgs {
   int64_t xstride;
   int64_t row_begin, n_local;
   double *out;       // [dim][n_local]
+  const int32_t *emap = nullptr;  // H1 element restriction [nel_local][(p+1)^dim] (setup), or NULL
 };
 cudaError_t launch_coords(int dim, const CoordArgs &a, cudaStream_t st);
 

@@ -89,7 +89,8 @@ struct XFillArgs {
   unsigned long long *tstamp;  // debug (LOR_PHASE_TIMING=1): per-CTA phase clocks, 16 per CTA
   int64_t pf_dist;             // L2 prefetch distance in CTAs (resident CTAs of the grid; 0: off)
   int values_only;             // 1: numeric-only re-assembly, col is not written (pattern reuse)
-  int sort32;                  // 1: n_global < 2^26, the symbolic pass sorts packed 32-bit keys
+  int sort32;                  // 1: column ids - key_base < 2^26, the symbolic pass sorts packed 32-bit keys
+  int key_base;                // smallest column id this rank's rows can reference (slab neighbour r - 1)
   uint8_t cperm[128];          // one-chunk kernels: thread -> box cell (>= ncell: none), set by the launcher
   uint8_t cinv[128];           // box cell -> thread (storage slot)
 };
@@ -120,7 +121,8 @@ struct XvArgs {
   int ncx, ncy, ncz;
   int *err;
   int values_only;
-  int sort32;                  // ids < 2^(31 - slot bits): sorting network on packed keys
+  int sort32;                  // ids - key_base < 2^(31 - slot bits): sorting network on packed keys
+  int key_base;                // smallest column id this rank's rows can reference (slab neighbour r - 1)
 };
 cudaError_t launch_xv_setup(int space, int p, const XvArgs &a, cudaStream_t st);
 cudaError_t launch_xv_sym(int space, int p, const XvArgs &a, cudaStream_t st);

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(NT) k_xh1_sym(XFillArgs A) {
     for (int j = 0; j < 27; ++j) {
       const int dx = j % 3, dy = (j / 3) % 3, dz = j / 9;
       const bool v = (m[0] >> dx) & (m[1] >> dy) & (m[2] >> dz) & 1;
-      key[j] = v ? XG[px + (dx - 1) + PB * (dy - 1) + PB * PB * (dz - 1)] : 0x7fffffff;
+      key[j] = v ? XG[px + (dx - 1) + PB * (dy - 1) + PB * PB * (dz - 1)] - A.key_base : 0x7fffffff;
     }
     xdev::row_positions<27>(key, A.sort32 != 0, s_pos + tid * 28, pw);
   };

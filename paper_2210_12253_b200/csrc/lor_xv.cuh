@@ -207,14 +207,14 @@ __device__ __forceinline__ bool slot_valid(const int x[3], const int clo[3], con
 // keys of the row's slots: the global ids (absent: 0x7fffffff), and whether the slot is present
 template <int P, int NB, int SP, int S, int... K>
 __device__ __forceinline__ void slot_keys(const int x[3], const int clo[3], const int chi[3], const uint32_t *XV,
-                                          int (&key)[XvT<SP>::W], std::integer_sequence<int, K...>) {
+                                          int kb, int (&key)[XvT<SP>::W], std::integer_sequence<int, K...>) {
   constexpr int NVF = XvCfg<P, NB, SP>::NVF;
   auto one = [&](auto kc) {
     constexpr int k = decltype(kc)::value;
     using C = SlotC<SP, S, k>;
     if (slot_valid<SP, S, k>(x, clo, chi)) {
       const int u[3] = {x[0] + C::d0 - clo[0], x[1] + C::d1 - clo[1], x[2] + C::d2 - clo[2]};
-      key[k] = (int)(XV[C::s2 * NVF + fidx<SP, NB>(C::s2, u)] & 0x7fffffffu);
+      key[k] = (int)(XV[C::s2 * NVF + fidx<SP, NB>(C::s2, u)] & 0x7fffffffu) - kb;
     } else {
       key[k] = 0x7fffffff;
     }
@@ -321,7 +321,7 @@ __device__ __forceinline__ void sym_row(const XvArgs &A, const int x[3], const i
   using CF = XvCfg<P, NB, SP>;
   constexpr int W = CF::W;
   int key[W];
-  slot_keys<P, NB, SP, S>(x, clo, chi, XV, key, std::make_integer_sequence<int, W>{});
+  slot_keys<P, NB, SP, S>(x, clo, chi, XV, A.key_base, key, std::make_integer_sequence<int, W>{});
   const int u[3] = {x[0] - clo[0], x[1] - clo[1], x[2] - clo[2]};
   const int64_t r = (int64_t)(XV[S * CF::NVF + fidx<SP, NB>(S, u)] & 0x7fffffffu) - A.row_begin;
   int n = 0;

@@ -72,6 +72,7 @@ def lib():
             getattr(L, name).argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int, C.POINTER(_Csr)]
         L.lor_discrete_grad.argtypes = [C.c_void_p, C.POINTER(_Csr)]
         L.lor_discrete_curl.argtypes = [C.c_void_p, C.POINTER(_Csr)]
+        L.lor_discrete_rotgrad.argtypes = [C.c_void_p, C.POINTER(_Csr)]
         L.lor_dof_map.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.lor_query_elements.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -250,7 +251,7 @@ class LOR:
         return dict(n_local=v[0].value, row_begin=v[1].value, n_global=v[2].value, nnz=v[3].value)
 
     def query_discrete(self, which):
-        w = {"grad": 0, "curl": 1}.get(which, which)
+        w = {"grad": 0, "curl": 1, "rotgrad": 2}.get(which, which)
         v = [C.c_int64() for _ in range(3)]
         self._check(lib().lor_query_discrete(self.h, w, *[C.byref(x) for x in v]))
         return dict(n_local=v[0].value, nnz=v[1].value, n_cols=v[2].value)
@@ -296,7 +297,8 @@ class LOR:
         q = self.query_discrete(which)
         if out is None:
             out = self.alloc(q["n_local"], q["nnz"])
-        fn = lib().lor_discrete_grad if which in ("grad", 0) else lib().lor_discrete_curl
+        fn = {"grad": lib().lor_discrete_grad, 0: lib().lor_discrete_grad, "curl": lib().lor_discrete_curl,
+              1: lib().lor_discrete_curl, "rotgrad": lib().lor_discrete_rotgrad, 2: lib().lor_discrete_rotgrad}[which]
         self._check(fn(self.h, C.byref(self._csr(*out))))
         return out
 
