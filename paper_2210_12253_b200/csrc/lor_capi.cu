@@ -410,7 +410,9 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
     return LOR_OK;
   }
-  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX && !c->vc;  // variable coefficients: general path
+  // variable coefficients: the H1 extended frame on one rank (its neighbour coefficients come from the
+  // local E-vectors), the element + merge passes otherwise
+  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX && (!c->vc || (s == SP_H1 && c->nranks == 1));
   if (!reuse) {  // symbolic part (A2): row lengths per call, then the int64 scan
     if (xpath) {
       XFillArgs x = xfill_args(c, S);
@@ -431,6 +433,8 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     x.val = out->val;
     x.alpha = alpha;
     x.beta = beta;
+    x.ca = c->vc ? c->ca : nullptr;
+    x.cb = c->vc ? c->cb : nullptr;
     x.values_only = reuse ? 1 : 0;
     CUDA_TRY(c, launch_xh1_fill(c->p, x, c->stream, nullptr));
     if (c->nel_local > 0) c->launches++;
@@ -1646,7 +1650,8 @@ int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int
 
 int lor_fill_path(lor_ctx c, lor_space space) {
   if (!c || space < 0 || space > 2 || !c->sp[space].valid) return -1;
-  return ((c->sp[space].xok || c->sp[space].xvok) && !c->vc) ? 1 : 0;
+  if (c->vc) return (space == LOR_H1 && c->sp[space].xok && c->nranks == 1) ? 1 : 0;
+  return (c->sp[space].xok || c->sp[space].xvok) ? 1 : 0;
 }
 
 int lor_last_phase_ms(lor_ctx c, float *ms, int cap) {

@@ -84,6 +84,7 @@ struct XFillArgs {
   int32_t *col;
   double *val;
   double alpha, beta;
+  const double *ca, *cb;       // variable coefficient E-vectors [nel_local][(p+1)^3] (NEXT-3) or null
   int ncx, ncy, ncz;  // max cell-box extents over the elements (shared-memory sizing)
   int *err;
   unsigned long long *tstamp;  // debug (LOR_PHASE_TIMING=1): per-CTA phase clocks, 16 per CTA

@@ -49,7 +49,7 @@ __device__ __forceinline__ double dot3x(const double *a, const double *b) { retu
 // built for: P+1 (every element of the mesh has a box of at most P+1 cells per axis: elements
 // owning entities on one side per axis -- lexicographic and orientation-scrambled structured
 // meshes) or P+2 (general).  All box-local index arithmetic then has constant strides.
-template <int P, int NB>
+template <int P, int NB, int NCOMP = 3>  // NCOMP = 5: + the coefficient boxes a, b (NEXT-3)
 struct XCfg {
   static constexpr int PB = NB + 1;                 // points per axis of the point box
   static constexpr int NPB = PB * PB * PB;
@@ -73,7 +73,7 @@ struct XCfg {
   static constexpr int XR = ONE ? (PB % 2 ? PB : PB + 1) : PB;
   static constexpr int XS = ONE ? PB * XR + 1 : PB * PB;
   static constexpr int XN = ONE ? XS * PB : NPB;
-  static constexpr int XEB = 3 * XN * 8;
+  static constexpr int XEB = NCOMP * XN * 8;
   static constexpr int STAGE1 = MAXROW * 27 * 12;
   static constexpr int OFF_CM_1 = XEB;
   static constexpr int NSL = ONE ? 128 : NR * LAY;  // cell storage slots (one chunk: slot = thread)
@@ -326,7 +326,9 @@ __host__ __device__ constexpr bool first_touch(int q, int a, int b) {
   return true;
 }
 
-template <int XN, int XR, int XS, int FENCE = 1>
+// VC: variable coefficients -- the boxes XE[3 XN ...] (a) and XE[4 XN ...] (b) hold the coefficient
+// E-vectors; corner q's contributions are scaled by a and b at its point (vertex rule, reading P-28)
+template <int XN, int XR, int XS, int FENCE = 1, bool VC = false>
 __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, double a8, double b8, double *__restrict__ o) {
   auto X = [&](int v, int k) -> double { return XE[k * XN + pb + (v & 1) + XR * ((v >> 1) & 1) + XS * ((v >> 2) & 1)]; };
   // accumulate in the cell's (thread-private) shared-memory row: the first corner touching an
@@ -359,7 +361,7 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
     cross3x(j[0], j[1], r[2]);
     const double det = dot3x(j[0], r[0]);
     ok = ok && det > 0.0;
-    const double sa = a8 * rcp_pos(det);
+    const double sa = (VC ? a8 * X(q, 3) : a8) * rcp_pos(det);
     double Q[3][3];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -369,7 +371,7 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
     double Qs[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) Qs[d] = s0 * Q[d][0] + s1 * Q[d][1] + s2 * Q[d][2];
-    dg[q] += s0 * Qs[0] + s1 * Qs[1] + s2 * Qs[2] + b8 * det;
+    dg[q] += s0 * Qs[0] + s1 * Qs[1] + s2 * Qs[2] + (VC ? b8 * X(q, 4) : b8) * det;
     dg[q ^ 1] += Q[0][0];
     dg[q ^ 2] += Q[1][1];
     dg[q ^ 4] += Q[2][2];
@@ -387,9 +389,9 @@ __device__ __forceinline__ bool cell_h1v(const double *__restrict__ XE, int pb, 
 
 // WCOL = false: numeric-only re-assembly (pattern reuse): col keeps what the
 // previous full call wrote, only val is stored.
-template <int P, int NB, int MINB, bool WCOL>
+template <int P, int NB, int MINB, bool WCOL, bool VC = false>
 __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
-  using CF = XCfg<P, NB>;
+  using CF = XCfg<P, NB, VC ? 5 : 3>;
   constexpr int NP1 = P + 1, NPT = NP1 * NP1 * NP1, PB = CF::PB, NPB = CF::NPB, LAY = CF::LAY, CP = CF::CP;
   constexpr int NR = CF::NR;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -439,11 +441,11 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
     // extended element restriction (setup): global id of every point of the box
     const int32_t *xm = A.xmap + bs * NPB;
     for (int i = tid; i < NPB; i += blockDim.x) XG[i] = __ldg(xm + i);
-    // own E-vector, one lattice x-row per thread
+    // own E-vector (and coefficient E-vectors), one lattice x-row per thread
     const double *xs = A.X + el * A.xstride;
-    for (int rr = tid; rr < 3 * NP1 * NP1; rr += blockDim.x) {
+    for (int rr = tid; rr < (VC ? 5 : 3) * NP1 * NP1; rr += blockDim.x) {
       const int d = rr / (NP1 * NP1), x12 = rr - d * NP1 * NP1, x1 = x12 % NP1, x2 = x12 / NP1;
-      const double *src = xs + d * NPT + x12 * NP1;
+      const double *src = d < 3 ? xs + d * NPT + x12 * NP1 : (d == 3 ? A.ca : A.cb) + el * NPT + x12 * NP1;
       double *dst = XE + d * CF::XN + (x1 - clo1) * CF::XR + (x2 - clo2) * CF::XS - clo0;
 #pragma unroll
       for (int i = 0; i < NP1; ++i) dst[i] = __ldg(src + i);
@@ -457,6 +459,11 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
         XE[q] = __ldg(A.X + hv.x);
         XE[CF::XN + q] = __ldg(A.X + hv.x + NPT);
         XE[2 * CF::XN + q] = __ldg(A.X + hv.x + 2 * NPT);
+        if (VC) {  // the neighbour's coefficient at the same point (its element e', point l)
+          const int64_t e2 = hv.x / A.xstride, l2 = hv.x - e2 * A.xstride;
+          XE[3 * CF::XN + q] = __ldg(A.ca + e2 * NPT + l2);
+          XE[4 * CF::XN + q] = __ldg(A.cb + e2 * NPT + l2);
+        }
       }
     }
   }
@@ -487,7 +494,7 @@ __global__ void __launch_bounds__(128, MINB) k_xh1_fill(XFillArgs A) {
         double *dstc = cm + (CF::ONE ? c : ((uz % NR) * LAY + uy * NB + ux)) * CP;
         // det J <= 0 in any cell of the box -- own or a neighbour's, which may be computed by no
         // other CTA (an element owning no rows) -- is reported (extended-frame cell coordinates)
-        if (!cell_h1v<CF::XN, CF::XR, CF::XS>(XE, ux + CF::XR * uy + CF::XS * uz, a8, b8, dstc))
+        if (!cell_h1v<CF::XN, CF::XR, CF::XS, 1, VC>(XE, ux + CF::XR * uy + CF::XS * uz, a8, b8, dstc))
           s_bad = 1 + (clo0 + ux + 1) + (P + 2) * ((clo1 + uy + 1) + (P + 2) * (clo2 + uz + 1));
       }
     }
@@ -1001,12 +1008,35 @@ static cudaError_t xh1_fill_pers(const XFillArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// variable coefficients: the non-persistent kernel with the coefficient boxes (one rank)
+template <int P, int NB>
+static cudaError_t xh1_fill_vc(const XFillArgs &a, cudaStream_t st) {
+  using CF = XCfg<P, NB, 5>;
+  constexpr int smem = CF::SMEM;
+  constexpr int MINB = ((smem + 1024) * 5 <= 228 * 1024) ? XMINB : ((smem + 1024) * 4 <= 228 * 1024 ? 4 : 3);
+  auto k = a.values_only ? k_xh1_fill<P, NB, MINB, false, true> : k_xh1_fill<P, NB, MINB, true, true>;
+  static bool attr = false;
+  if (!attr) {
+    for (auto kk : {k_xh1_fill<P, NB, MINB, false, true>, k_xh1_fill<P, NB, MINB, true, true>}) {
+      cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(kk, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    attr = true;
+  }
+  XFillArgs b = a;
+  b.pf_dist = 0;
+  cell_perm<P, NB>(b.cperm, b.cinv);
+  k<<<(unsigned)a.nel_local, 128, smem, st>>>(b);
+  return cudaGetLastError();
+}
+
 template <int P, int NB>
 static cudaError_t xh1_fill_nb(const XFillArgs &a, cudaStream_t st, int *smem_out) {
   using CF = XCfg<P, NB>;
   constexpr int smem = CF::SMEM;
   if (smem_out) { *smem_out = smem; return cudaSuccess; }
   if (a.nel_local <= 0) return cudaSuccess;
+  if (a.ca) return xh1_fill_vc<P, NB>(a, st);
   constexpr int MINB = ((smem + 1024) * 5 <= 228 * 1024) ? XMINB : 3;  // 228 KB shared memory per SM
   if constexpr (CF::ONE) {
     static int pers = -1;

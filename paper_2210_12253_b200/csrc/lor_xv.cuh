@@ -693,13 +693,25 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
       w_dst[warp * 32 + lane] = rout[rr] - rso[rr];
       __syncwarp();
       const int S0 = __shfl_sync(0xffffffffu, rso[rr], 0), E0 = __shfl_sync(0xffffffffu, rso[rr] + rn[rr], 31);
-      for (int k = S0 + lane; k < E0; k += 32) {
-        int cur = 0;  // the entry's row: first of the warp's rows whose staged end exceeds k (5 steps)
+      // one contiguous CSR run (every row with entries starts where the previous one ends; common
+      // for element-interior rows): a single destination offset, no search
+      const int64_t dst = rout[rr] - rso[rr];
+      const long long dfirst = __shfl_sync(0xffffffffu, (long long)dst, __ffs(__ballot_sync(0xffffffffu, rn[rr] > 0) | 0x80000000u) - 1);
+      const bool one_run = __all_sync(0xffffffffu, rn[rr] == 0 || dst == dfirst);
+      if (one_run) {
+        for (int k = S0 + lane; k < E0; k += 32) {
+          if (WCOL) __stcs(A.col + dfirst + k, stc[k]);
+          __stcs(A.val + dfirst + k, stv[k]);
+        }
+      } else {
+        for (int k = S0 + lane; k < E0; k += 32) {
+          int cur = 0;  // the entry's row: first of the warp's rows whose staged end exceeds k (5 steps)
 #pragma unroll
-        for (int st = 16; st > 0; st >>= 1) cur += (w_end[warp * 32 + cur + st - 1] <= k) ? st : 0;
-        const int64_t d = w_dst[warp * 32 + cur] + k;
-        if (WCOL) __stcs(A.col + d, stc[k]);
-        __stcs(A.val + d, stv[k]);
+          for (int st = 16; st > 0; st >>= 1) cur += (w_end[warp * 32 + cur + st - 1] <= k) ? st : 0;
+          const int64_t d = w_dst[warp * 32 + cur] + k;
+          if (WCOL) __stcs(A.col + d, stc[k]);
+          __stcs(A.val + d, stv[k]);
+        }
       }
       __syncwarp();
     }
