@@ -73,6 +73,10 @@ typedef struct {
                                    rank 0, broadcast by the caller; NULL when nranks == 1      */
   void *cuda_stream;            /* cudaStream_t for all work (NULL = legacy default stream)    */
   int device;                   /* CUDA device ordinal of this rank                            */
+  int space_mask;               /* bit s set: set up space s (H1 = 1, ND = 2, RT = 4; H1 always);
+                                   0 = all.  The element + merge passes keep per-element buffers of
+                                   every local dof, so skipping unused spaces saves device memory on
+                                   large meshes (48^3 elements at p = 8: > 100 GB for ND + RT). */
 } lor_setup_args;
 
 /* Caller-owned DEVICE buffers.  cap_nnz = capacity of col/val (entries); row_ptr must hold

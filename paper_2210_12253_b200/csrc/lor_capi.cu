@@ -925,8 +925,8 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
   for (int s = 0; s < 3; ++s) {
     const SpacePlan &P = plan.sp[s];
     SpaceDev &S = c->sp[s];
-    S.valid = P.valid;
-    if (!P.valid) continue;
+    S.valid = P.valid && (s == SP_H1 || A.space_mask == 0 || ((A.space_mask >> s) & 1));
+    if (!S.valid) continue;
     S.ndpe = P.ndpe;
     S.maxl = P.maxl;
     S.rstride = ((P.maxl + 1) * 16 + 127) / 128 * 8;  // entries + header, padded to whole 128-byte lines
@@ -1335,6 +1335,8 @@ lor_status lor_query_discrete(lor_ctx c, int which, int64_t *n_rows_local, int64
     return LOR_OK;
   }
   if (which == 2) return fail(c, LOR_ERR_UNSUPPORTED, "the rotated gradient is 2D");
+  if (!c->sp[which == 0 ? SP_ND : SP_RT].valid || !c->sp[which == 0 ? SP_H1 : SP_ND].valid)
+    return fail(c, LOR_ERR_UNSUPPORTED, "space not set up (space_mask)");
   if (c->dim != 3) return fail(c, LOR_ERR_UNSUPPORTED, "discrete operators need dim == 3");
   const SpaceDev &R = c->sp[which == 0 ? SP_ND : SP_RT];
   const SpaceDev &C = c->sp[which == 0 ? SP_H1 : SP_ND];
@@ -1483,6 +1485,7 @@ lor_status lor_discrete_grad(lor_ctx c, lor_csr *out) {
   if (c->dim == 2) return vec2d_discrete(c, SP_ND, out);
   if (c->dim != 3) return fail(c, LOR_ERR_UNSUPPORTED, "dim == 3 only");
   const SpaceDev &R = c->sp[SP_ND];
+  if (!R.valid) return fail(c, LOR_ERR_UNSUPPORTED, "ND not set up (space_mask)");
   if (out->cap_nnz < 2 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 2 n_rows");
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 2, c->stream));
@@ -1510,6 +1513,7 @@ lor_status lor_discrete_curl(lor_ctx c, lor_csr *out) {
   if (!c || !out) return LOR_ERR_INVALID_ARGUMENT;
   if (c->dim != 3) return fail(c, LOR_ERR_UNSUPPORTED, "dim == 3 only");
   const SpaceDev &R = c->sp[SP_RT];
+  if (!R.valid || !c->sp[SP_ND].valid) return fail(c, LOR_ERR_UNSUPPORTED, "RT / ND not set up (space_mask)");
   if (out->cap_nnz < 4 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 4 n_rows");
   CUDA_TRY(c, cudaSetDevice(c->device));
   CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 4, c->stream));

@@ -31,7 +31,7 @@ class _SetupArgs(C.Structure):
     _fields_ = [("dim", C.c_int), ("p", C.c_int), ("n_vert", C.c_int64), ("vert_xyz", C.c_void_p),
                 ("n_elem", C.c_int64), ("elem_vert", C.c_void_p), ("elem_nodes", C.c_void_p), ("rank", C.c_int),
                 ("nranks", C.c_int), ("elem_rank_begin", C.c_void_p), ("nccl_unique_id", C.c_void_p),
-                ("cuda_stream", C.c_void_p), ("device", C.c_int)]
+                ("cuda_stream", C.c_void_p), ("device", C.c_int), ("space_mask", C.c_int)]
 
 
 class _Csr(C.Structure):
@@ -160,7 +160,7 @@ class LOR:
     """One context per rank/GPU.  ``mesh`` provides ``dim, p, vert, elem, X`` (numpy)."""
 
     def __init__(self, mesh, *, rank=0, nranks=1, elem_rank_begin=None, nccl_id: bytes | None = None,
-                 stream=None, device=None, use_evector=True):
+                 stream=None, device=None, use_evector=True, spaces=None):
         import torch
         if not torch.cuda.is_available():
             raise LorError(4, "no CUDA device: the LOR library has no CPU path")
@@ -187,6 +187,8 @@ class LOR:
         a.nccl_unique_id = C.cast(self._nccl, C.c_void_p) if self._nccl is not None else None
         a.cuda_stream = self.stream.cuda_stream
         a.device = self.device.index
+        # spaces to set up (None: all); H1 always (its frame records serve the vector spaces)
+        a.space_mask = 0 if spaces is None else sum(1 << SPACES[x] for x in set(spaces) | {"h1"})
         h = C.c_void_p()
         rc = lib().lor_setup(C.byref(a), C.byref(h))
         if rc:

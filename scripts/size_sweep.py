@@ -34,10 +34,12 @@ def t_ms(fn, reps=10):
 
 
 cases = [("cartesian", 4, n) for n in (8, 12, 16, 24, 32, 48, 64)] + [("kershaw", 8, n) for n in (6, 12, 24, 36, 48)]
+if len(sys.argv) > 1:  # e.g. "kershaw:8:48" -- selected cases only
+    cases = [(c.split(":")[0], int(c.split(":")[1]), int(c.split(":")[2])) for c in sys.argv[1:]]
 for kind, p, n in cases:
     m = mg.box_mesh(3, (n, n, n), p, kershaw=0.3 if kind == "kershaw" else None)
     t0 = time.perf_counter()
-    ctx = LOR(m, stream=st)
+    ctx = LOR(m, stream=st, spaces=("h1",))
     torch.cuda.synchronize()
     setup = (time.perf_counter() - t0) * 1e3
     q = ctx.query("h1")
