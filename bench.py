@@ -50,6 +50,7 @@ WORKLOADS = {
             "dense 8x8 cell matrices, direct CSR assembly (PAPER.md l.593-606, NEXT-4)",
     "C2-V": "C2-V: C2 with variable coefficients alpha a(x), beta b(x) given as E-vectors at the LOR vertices (NEXT-3)",
     "C4-V": "C4-V: C4 (ND) with variable coefficients a(x), b(x) at the LOR vertices (NEXT-3)",
+    "C5-V": "C5-V: C5 (RT) with variable coefficients a(x), b(x) at the LOR vertices (NEXT-3)",
 }
 DISCRETE = {"C4-G": ("C4", "grad"), "C5-C": ("C5", "curl")}
 # steps after the assembly: A3 layout + A4, coordinate vectors (l.400-404)

@@ -388,7 +388,9 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   c->nphase = 0;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   lor_status st = LOR_OK;
-  if (S.xvok && quad == LOR_QUAD_VERTEX && !c->vc) {  // ND / RT extended-frame path: every owned row in one pass
+  // variable coefficients on the ND frame would need 2 more E-vector boxes beside 78 KB of resident
+  // cells: 1 CTA/SM, slower (7.3 vs 5.2 ms at C4) than the element + merge passes
+  if (S.xvok && quad == LOR_QUAD_VERTEX && (!c->vc || (c->nranks == 1 && s == SP_RT))) {  // ND / RT extended frame
     XvArgs x = xv_args(c, s);
     if (!reuse) {
       CUDA_TRY(c, launch_xv_sym(s, c->p, x, c->stream));
@@ -402,6 +404,8 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     x.val = out->val;
     x.alpha = alpha;
     x.beta = beta;
+    x.ca = c->vc ? c->ca : nullptr;
+    x.cb = c->vc ? c->cb : nullptr;
     x.values_only = reuse ? 1 : 0;
     CUDA_TRY(c, launch_xv_fill(s, c->p, x, c->stream));
     if (c->nel_local > 0) c->launches++;
@@ -410,9 +414,9 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
     return LOR_OK;
   }
-  // variable coefficients: the H1 extended frame on one rank (its neighbour coefficients come from the
+  // variable coefficients: the extended frames on one rank (the neighbour coefficients come from the
   // local E-vectors), the element + merge passes otherwise
-  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX && (!c->vc || (s == SP_H1 && c->nranks == 1));
+  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX && (!c->vc || c->nranks == 1);
   if (!reuse) {  // symbolic part (A2): row lengths per call, then the int64 scan
     if (xpath) {
       XFillArgs x = xfill_args(c, S);
@@ -1654,7 +1658,7 @@ int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int
 
 int lor_fill_path(lor_ctx c, lor_space space) {
   if (!c || space < 0 || space > 2 || !c->sp[space].valid) return -1;
-  if (c->vc) return (space == LOR_H1 && c->sp[space].xok && c->nranks == 1) ? 1 : 0;
+  if (c->vc) return ((c->sp[space].xok || (space == LOR_RT && c->sp[space].xvok)) && c->nranks == 1) ? 1 : 0;
   return (c->sp[space].xok || c->sp[space].xvok) ? 1 : 0;
 }
 

@@ -119,6 +119,7 @@ struct XvArgs {
   int32_t *col;
   double *val;
   double alpha, beta;
+  const double *ca, *cb;       // variable coefficient E-vectors [nel_local][(p+1)^3] (NEXT-3) or null
   int ncx, ncy, ncz;
   int *err;
   int values_only;

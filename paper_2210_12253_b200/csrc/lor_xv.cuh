@@ -47,7 +47,7 @@ struct XvT<SP_RT> {
   static constexpr int W = 11, NE = 21, PW = 4;
 };
 
-template <int P, int NB, int SP>
+template <int P, int NB, int SP, int NCOMP = 3>  // NCOMP = 5: + coefficient boxes a, b (NEXT-3)
 struct XvCfg {
   static constexpr int PB = NB + 1, NPB = PB * PB * PB, LAY = NB * NB;
   static constexpr int NVF = SP == SP_ND ? NB * PB * PB : PB * NB * NB;  // box positions per family
@@ -70,7 +70,7 @@ struct XvCfg {
   static constexpr int MAXG = B1 + NF0;
   static constexpr int RPT = (MAXG + 127) / 128;
   static constexpr int NSLOT = ONE ? NB : 2;
-  static constexpr int OFF_CM = 3 * NPB * 8;                       // E-vector box [3][NPB]
+  static constexpr int OFF_CM = NCOMP * NPB * 8;                   // E-vector box [3][NPB] (+ a, b)
   static constexpr int OFF_ST = OFF_CM + NSLOT * NE * NCP * 8;     // cell layers [NSLOT][NE][NCP]
   static constexpr int NROWS = NF2 + 2 * NF0;                      // rows of a group (staging capacity)
   static constexpr int OFF_SC = OFF_ST + NROWS * W * 8;            // staged values [NROWS][W]
@@ -375,7 +375,8 @@ __global__ void __launch_bounds__(128) k_xv_sym(XvArgs A) {
 // RT vertex rule straight into the cell's packed slots out[t * NC]: mass M[F_d(q)][F_e(q)] +=
 // w beta (J^T J / det)_de at corner q, div-div (sum_q w alpha / det_q) d d^T (lor_cells.cuh cell_rt)
 template <typename XF>
-__device__ __forceinline__ bool cell_rt_vertex_to(XF X, double alpha, double beta, double *__restrict__ out, int NC) {
+__device__ __forceinline__ bool cell_rt_vertex_to(XF X, double alpha, double beta, double *__restrict__ out, int NC,
+                                                  const double *ca = nullptr, const double *cb = nullptr) {
   double M[21];
 #pragma unroll
   for (int i = 0; i < 21; ++i) M[i] = 0.0;
@@ -395,8 +396,8 @@ __device__ __forceinline__ bool cell_rt_vertex_to(XF X, double alpha, double bet
                        J.j[0][1] * (J.j[1][2] * J.j[2][0] - J.j[1][0] * J.j[2][2]) +
                        J.j[0][2] * (J.j[1][0] * J.j[2][1] - J.j[1][1] * J.j[2][0]);
     ok = ok && det > 0.0;
-    const double rd = rcp_pos(det), sm = w * beta * rd;
-    sdiv += w * alpha * rd;
+    const double rd = rcp_pos(det), sm = w * beta * coef_q<0, 8>(cb, q) * rd;
+    sdiv += w * alpha * coef_q<0, 8>(ca, q) * rd;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
@@ -511,9 +512,9 @@ __device__ __forceinline__ void fill_row(const XvArgs &A, const int x[3], const 
   stage_row<P, NB, SP, S>(x, clo, XV, (mr >> 31) != 0, pw, acc, sv, sc, std::make_integer_sequence<int, W>{});
 }
 
-template <int P, int NB, int SP, int MINB, bool WCOL>
+template <int P, int NB, int SP, int MINB, bool WCOL, bool VC = false>
 __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
-  using CF = XvCfg<P, NB, SP>;
+  using CF = XvCfg<P, NB, SP, VC ? 5 : 3>;
   constexpr int PB = CF::PB, NPB = CF::NPB, NP1 = P + 1, NPT = NP1 * NP1 * NP1, W = CF::W, NE = CF::NE;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_bad;
@@ -573,10 +574,11 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
     for (int i = tid; i < 3 * CF::NVF; i += 128) XV[i] = __ldg(A.xvmap + bs * 3 * CF::NVF + i);
     // own E-vector into the dense box, then the neighbour points (gather list of the H1 setup)
     const double *xs = A.X + el * A.xstride;
-    for (int i = tid; i < 3 * NPT; i += 128) {
+    for (int i = tid; i < (VC ? 5 : 3) * NPT; i += 128) {
       const int d = i / NPT, l = i - d * NPT;
       const int x0 = l % NP1, x1 = (l / NP1) % NP1, x2 = l / (NP1 * NP1);
-      XE[d * NPB + (x0 - clo[0]) + PB * ((x1 - clo[1]) + PB * (x2 - clo[2]))] = __ldg(xs + i);
+      XE[d * NPB + (x0 - clo[0]) + PB * ((x1 - clo[1]) + PB * (x2 - clo[2]))] =
+          d < 3 ? __ldg(xs + i) : __ldg((d == 3 ? A.ca : A.cb) + el * NPT + l);
     }
     constexpr int HC = NPB - NPT;
     const int2 *hl = A.xhalo + bs * HC;
@@ -586,6 +588,11 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
         XE[hv.y] = __ldg(A.X + hv.x);
         XE[NPB + hv.y] = __ldg(A.X + hv.x + NPT);
         XE[2 * NPB + hv.y] = __ldg(A.X + hv.x + 2 * NPT);
+        if (VC) {  // the neighbour's coefficients at the same point
+          const int64_t e2 = hv.x / A.xstride, l2 = hv.x - e2 * A.xstride;
+          XE[3 * NPB + hv.y] = __ldg(A.ca + e2 * NPT + l2);
+          XE[4 * NPB + hv.y] = __ldg(A.cb + e2 * NPT + l2);
+        }
       }
     }
   }
@@ -608,8 +615,19 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
           return XE[k * NPB + pb + (v & 1) + PB * ((v >> 1) & 1) + PB * PB * ((v >> 2) & 1)];
         };
         bool ok;
-        if (SP == SP_ND) ok = cell_nd_vertex_to(X, alpha, beta, cl + cc, CF::NCP);
-        else ok = cell_rt_vertex_to(X, alpha, beta, cl + cc, CF::NCP);
+        if (VC) {  // the cell's corner coefficient values (NEXT-3)
+          double a8[8], b8[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            a8[v] = X(v, 3);
+            b8[v] = X(v, 4);
+          }
+          if (SP == SP_ND) ok = cell_nd_vertex_to(X, alpha, beta, cl + cc, CF::NCP, a8, b8);
+          else ok = cell_rt_vertex_to(X, alpha, beta, cl + cc, CF::NCP, a8, b8);
+        } else {
+          if (SP == SP_ND) ok = cell_nd_vertex_to(X, alpha, beta, cl + cc, CF::NCP);
+          else ok = cell_rt_vertex_to(X, alpha, beta, cl + cc, CF::NCP);
+        }
         if (!ok) s_bad = 1 + (clo[0] + b0 + 1) + (P + 2) * ((clo[1] + b1 + 1) + (P + 2) * (cz + 1));
       }
     }
@@ -730,11 +748,36 @@ static int nb_of(const XvArgs &a) {
   return (a.ncx <= P + 1 && a.ncy <= P + 1 && a.ncz <= P + 1) ? P + 1 : P + 2;
 }
 
+// variable coefficients: the instantiation with the coefficient boxes (one rank)
+template <int P, int NB, int SP>
+static cudaError_t fill_nb_vc(const XvArgs &a, cudaStream_t st) {
+  using CF = XvCfg<P, NB, SP, 5>;
+  if constexpr (CF::SMEM > 200 * 1024) {
+    return cudaErrorInvalidValue;
+  } else {
+    constexpr int smem = CF::SMEM;
+    constexpr int MINB = (smem + 1024) * 5 <= 228 * 1024 ? 5 : ((smem + 1024) * 4 <= 228 * 1024 ? 4 :
+                         ((smem + 1024) * 3 <= 228 * 1024 ? 3 : ((smem + 1024) * 2 <= 228 * 1024 ? 2 : 1)));
+    static bool attr = false;
+    if (!attr) {
+      for (auto k : {k_xv_fill<P, NB, SP, MINB, false, true>, k_xv_fill<P, NB, SP, MINB, true, true>}) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      }
+      attr = true;
+    }
+    if (a.values_only) k_xv_fill<P, NB, SP, MINB, false, true><<<(unsigned)a.nel_local, 128, smem, st>>>(a);
+    else k_xv_fill<P, NB, SP, MINB, true, true><<<(unsigned)a.nel_local, 128, smem, st>>>(a);
+    return cudaGetLastError();
+  }
+}
+
 template <int P, int NB, int SP>
 static cudaError_t fill_nb(const XvArgs &a, cudaStream_t st) {
   if constexpr (!xv_fits<P, NB, SP>()) {
     return cudaErrorInvalidValue;
   } else {
+    if (a.ca) return fill_nb_vc<P, NB, SP>(a, st);
     using CF = XvCfg<P, NB, SP>;
     constexpr int smem = CF::SMEM;
     // CTAs per SM the shared memory allows (at most 5: >= 96 registers per thread)
