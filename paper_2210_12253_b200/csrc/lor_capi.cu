@@ -1905,7 +1905,11 @@ lor_status lor_eliminate_bc(lor_ctx c, lor_space space, const int32_t *ess, int6
   BcArgs b{P.n, M->diag_row_ptr, M->offd_row_ptr, M->diag_col, M->diag_val, M->offd_val};
   CUDA_TRY(c, launch_bc_rows(ess, n_ess, b, c->stream));
   if (n_ess > 0) c->launches++;
-  if (!remote) return LOR_OK;
+  if (!remote) {
+    // the sends may still be in flight: later work on the context stream (the next pack) waits
+    if (use_nccl) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_xchg, 0));
+    return LOR_OK;
+  }
   if (!use_nccl) {
     P.pending = 1;
     return LOR_OK;

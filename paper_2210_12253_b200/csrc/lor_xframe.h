@@ -120,6 +120,7 @@ struct XvArgs {
   double *val;
   double alpha, beta;
   const double *ca, *cb;       // variable coefficient E-vectors [nel_local][(p+1)^3] (NEXT-3) or null
+  int64_t pf_dist;             // L2 prefetch distance in CTAs (resident CTAs of the grid; 0: off)
   int ncx, ncy, ncz;
   int *err;
   int values_only;

@@ -568,6 +568,24 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
       for (int a = 0; a < 3; ++a) nx[rr][a] = xx[a];
     }
   };
+  // L2 prefetch for the CTA that takes this CTA's place one residency later: its record, extended
+  // restriction and gather list now, its E-vector once its element id has arrived (as k_xh1_fill)
+  {
+    const int64_t nbs = bs + A.pf_dist;
+    if (A.pf_dist > 0 && nbs < A.nel_local) {
+      constexpr int HC2 = NPB - NPT;
+      constexpr int LX = (int)((sizeof(XElem) + 127) / 128), LM = (3 * CF::NVF * 4 + 127) / 128 + 1,
+                    LH = (HC2 * 8 + 127) / 128 + 1;
+      if (tid < LX) pf_l2(reinterpret_cast<const char *>(A.xe + nbs) + 128 * tid);
+      else if (tid < LX + LM) pf_l2(reinterpret_cast<const char *>(A.xvmap + nbs * 3 * CF::NVF) + 128 * (tid - LX));
+      else if (tid < LX + LM + LH) pf_l2(reinterpret_cast<const char *>(A.xhalo + nbs * HC2) + 128 * (tid - LX - LM));
+      else if (tid == 127) {
+        const int64_t pe = __ldg(&A.xe[nbs].el);
+        const char *xp = reinterpret_cast<const char *>(A.X + pe * A.xstride);
+        for (int l = 0; l < (3 * NPT * 8 + 127) / 128; ++l) pf_l2(xp + 128 * l);
+      }
+    }
+  }
   load_layer(0);
   {
     if (tid == 0) s_bad = 0;
@@ -791,8 +809,20 @@ static cudaError_t fill_nb(const XvArgs &a, cudaStream_t st) {
       }
       attr = true;
     }
-    if (a.values_only) k_xv_fill<P, NB, SP, MINB, false><<<(unsigned)a.nel_local, 128, smem, st>>>(a);
-    else k_xv_fill<P, NB, SP, MINB, true><<<(unsigned)a.nel_local, 128, smem, st>>>(a);
+    // L2 prefetch distance = resident CTAs of the grid (cached per instantiation; LOR_XPF=0: off)
+    static int64_t resident = -1;
+    if (resident < 0) {
+      int dev = 0, nsm = 0, occ = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xv_fill<P, NB, SP, MINB, true>, 128, smem);
+      const char *e = getenv("LOR_XPF");
+      resident = (e && !atoi(e)) ? 0 : (int64_t)nsm * occ;
+    }
+    XvArgs b = a;
+    b.pf_dist = resident;
+    if (a.values_only) k_xv_fill<P, NB, SP, MINB, false><<<(unsigned)a.nel_local, 128, smem, st>>>(b);
+    else k_xv_fill<P, NB, SP, MINB, true><<<(unsigned)a.nel_local, 128, smem, st>>>(b);
     return cudaGetLastError();
   }
 }
