@@ -26,6 +26,9 @@
 #include "lor_xdev.cuh"
 #include "lor_xframe.h"
 
+#ifndef XV_RT_GZ
+#define XV_RT_GZ(P) ((P) + 1)  // RT with resident cells: row layers per group (all of them)
+#endif
 #ifndef XV_ND_ONE_KB
 #define XV_ND_ONE_KB 80  // ND: all cell layers resident up to this size (p <= 4: 78 KB, 2 CTAs/SM)
 #endif
@@ -62,7 +65,7 @@ struct XvCfg {
   static constexpr bool ONE = NB * NE * NCP * 8 <= (SP == SP_ND ? XV_ND_ONE_KB : 40) * 1024;
   // rows processed per group of GZ z-layers: all of them at once for RT with resident cells (short
   // rows: per-layer barriers would dominate), one layer otherwise
-  static constexpr int GZ = (ONE && SP == SP_RT) ? P + 1 : 1;
+  static constexpr int GZ = (ONE && SP == SP_RT) ? XV_RT_GZ(P) : 1;
   // rows of a group in family-major segments, each starting at a warp boundary (a warp then runs
   // one family's code: no divergence between the families' unrolled row kernels)
   static constexpr int NF2 = GZ * NRF2, NF0 = GZ * NRF0;
