@@ -127,3 +127,48 @@ def test_discrete_map_path_equals_block_path(torch_cuda, monkeypatch, which):
         ctx.close()
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C4", "C5"])
+def test_variable_coefficients_full_size(torch_cuda, oracle_lib, cfg):
+    """BASELINE configs with the bench's coefficient fields (C2-V / C4-V / C5-V, the launch
+    configuration bench.py times): 3000 sampled rows + all rows of the first and last element against
+    the row oracle with the same coefficient E-vectors"""
+    from paper_2210_12253_b200.lor import LOR
+    from tests.parity import compare_rows
+    m, form = mg.config_mesh(cfg)
+    xs = [m.X[:, d, :] for d in range(3)]
+    ca = np.ascontiguousarray(1.0 + 0.5 * np.sin(3.0 * xs[0]) * np.cos(2.0 * xs[1]) + xs[2] * xs[2])
+    cb = np.ascontiguousarray(2.0 + np.cos(xs[0] + xs[1] + xs[2]))
+    ctx = LOR(m)
+    ctx.set_coefficients(ca, cb)
+    sp = form["space"]
+    rp, col, val = (to_host(t) for t in ctx.assemble(sp, 1.0, 1.0, "vertex"))
+    ctx.sync()
+    n = rp.shape[0] - 1
+    rng = np.random.default_rng(5)
+    rows = np.unique(np.concatenate([rng.choice(n, 3000, replace=False), np.arange(100), np.arange(n - 100, n)]))
+    ref = oracle_lib.assemble_rows(m, rows, sp, "vertex", 1.0, 1.0, coef=(ca, cb))
+    compare_rows(rp, col, val, ref, 0, None, f"{cfg}-V sampled rows")
+    ctx.close()
+
+
+def test_coordinates_full_size_c2(torch_cuda):
+    """C2-X: the coordinate vectors at full size -- every owned vertex equals its E-vector copy in the
+    minimal element (the copies of a shared vertex agree to rounding) and the Cartesian lattice"""
+    from paper_2210_12253_b200.lor import LOR
+    m, _ = mg.config_mesh("C2")
+    ctx = LOR(m)
+    xyz = to_host(ctx.coordinates())
+    mp, _ = ctx.dof_map("h1")
+    mp = to_host(mp)
+    ctx.sync()
+    # every element's E-vector agrees with the deduplicated coordinates of its dofs
+    for d in range(3):
+        assert np.max(np.abs(xyz[d][mp] - m.X[:, d, :])) < 1e-15
+    # the lattice: 32 elements x GLL(4) per axis, each point once
+    x1 = mg.gll_points_01(4)
+    axis = np.unique(np.round(np.concatenate([(e + x1) / 32 for e in range(32)]), 14))
+    assert axis.shape[0] == 129
+    for d in range(3):
+        assert np.max(np.min(np.abs(xyz[d][:, None] - axis[None, :]), axis=1)) < 1e-14
