@@ -254,3 +254,62 @@ def ho_vector_matrix(mesh, space, gll_nodes_01, vmap, vsign, n, alpha=1.0, beta=
         sg = vsign[e].astype(float)
         A[np.ix_(idx, idx)] += Ae * np.outer(sg, sg)
     return A
+
+
+def ho_vector_matrix_2d(mesh, space, gll_nodes_01, vmap, vsign, n, alpha=1.0, beta=1.0, q=None):
+    """2D analogue of ho_vector_matrix (reading P-29 local order): ND family a = e_a h(t_a) l(t_o)
+    with scalar curl, RT family a = e_a l(t_a) h(t_o) with divergence (the interpolation--histopolation
+    bases of l.142-150 on quadrilaterals), covariant / contravariant Piola maps, q = p+2 Gauss points,
+    assembled with the oracle's 2D ND / RT dof map and signs."""
+    assert mesh.dim == 2 and space in ("nd", "rt")
+    p = mesh.p
+    q = q or p + 2
+    nodes = np.asarray(gll_nodes_01, dtype=float)
+    _nodes_cache[p] = nodes
+    xq, wq = gauss(q)
+    B, D = lagrange_1d(nodes, xq)
+    H, Dh = _hist_deriv(p, xq)
+    nb = 2 * p * (p + 1)
+    val = np.zeros((q, q, nb, 2))   # [point along x, point along y, basis, component]
+    der = np.zeros((q, q, nb))
+    for a in range(2):
+        o = 1 - a
+        ext = [(p if b == a else p + 1) if space == "nd" else (p + 1 if b == a else p) for b in range(2)]
+        for x1 in range(ext[1]):
+            for x0 in range(ext[0]):
+                x = (x0, x1)
+                i = a * p * (p + 1) + x0 + ext[0] * x1
+                # factor along each axis: histopolant along the edge (ND: a; RT: o), Lagrange across
+                hist_axis = a if space == "nd" else o
+                f = [H[:, x[b]] if b == hist_axis else B[:, x[b]] for b in range(2)]
+                df = [Dh[:, x[b]] if b == hist_axis else D[:, x[b]] for b in range(2)]
+                val[:, :, i, a] = np.outer(f[0], f[1])
+                if space == "nd":  # curl (F e_a) = d(F)/dx for a = y, -d(F)/dy for a = x
+                    der[:, :, i] = np.outer(df[0], f[1]) if a == 1 else -np.outer(f[0], df[1])
+                else:              # div (F e_a) = dF/dx_a
+                    der[:, :, i] = np.outer(df[0], f[1]) if a == 0 else np.outer(f[0], df[1])
+    corners = mesh.vert[mesh.elem]
+    A = np.zeros((n, n))
+    for e in range(mesh.nel):
+        C = corners[e]
+        Ae = np.zeros((nb, nb))
+        for ia in range(q):
+            for ib in range(q):
+                t = (xq[ia], xq[ib])
+                J = np.zeros((2, 2))
+                for v in range(4):
+                    bits = [(v >> d) & 1 for d in range(2)]
+                    f = [t[d] if bits[d] else 1 - t[d] for d in range(2)]
+                    dfv = [1.0 if bits[d] else -1.0 for d in range(2)]
+                    J[:, 0] += C[v] * dfv[0] * f[1]
+                    J[:, 1] += C[v] * f[0] * dfv[1]
+                det = np.linalg.det(J)
+                ph = val[ia, ib]                                   # [nb, 2] reference
+                phi = ph @ np.linalg.inv(J) if space == "nd" else ph @ J.T / det   # J^{-T} / J phi / det
+                s = der[ia, ib] / det
+                w = wq[ia] * wq[ib] * det
+                Ae += w * (alpha * np.outer(s, s) + beta * phi @ phi.T)
+        idx = vmap[e]
+        sg = vsign[e].astype(float)
+        A[np.ix_(idx, idx)] += Ae * np.outer(sg, sg)
+    return A

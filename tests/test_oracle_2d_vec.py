@@ -111,3 +111,47 @@ def test_counts_brute_force(oracle_lib, space, p):
                     loc.append(mp[e, fam * p * (p + 1) + x[0] + ext0 * x[1]])
                 pairs.update((a, b) for a in loc for b in loc)
     assert A.nnz == len(pairs)
+
+
+def _ho2(O, m, space, alpha, beta):
+    from oracle import ho
+    vm, vs = O.dof_map(m, space)
+    n = int(vm.max()) + 1
+    x, _ = O.gll(m.p)
+    return ho.ho_vector_matrix_2d(m, space, (x + 1) / 2, vm, vs, n, alpha, beta)
+
+
+@pytest.mark.parametrize("space", ["nd", "rt"])
+def test_ho2d_p1_is_lowest_order(oracle_lib, space):
+    """the p = 1 interpolation-histopolation matrix (q = 3 Gauss) equals the lowest-order
+    matrix under the Gauss-2 rule (exact on a Cartesian mesh)"""
+    m = mg.box_mesh(2, (3, 2), 1)
+    A_lor = _dense(oracle_lib.assemble(m, space, "gauss2", 1.3, 0.7))
+    A_ho = _ho2(oracle_lib, m, space, 1.3, 0.7)
+    assert np.abs(A_ho - A_lor).max() <= 1e-14 * np.abs(A_lor).max()
+
+
+@pytest.mark.parametrize("space,p", [("nd", 2), ("nd", 4), ("rt", 2), ("rt", 4)])
+def test_ho2d_commuting(oracle_lib, space, p):
+    """the topological G / G_perp map into the kernels of the HO curl-curl / div-div (exact sequence)"""
+    m = mg.box_mesh(2, (3, 2), p, jitter=True)
+    K = _ho2(oracle_lib, m, space, 1.0, 0.0)
+    D = _dense(oracle_lib.discrete(m, "grad" if space == "nd" else "rotgrad"))
+    assert np.abs(K @ D).max() <= 1e-12 * np.abs(K).max()
+
+
+@pytest.mark.parametrize("space", ["nd", "rt"])
+def test_spectral_equivalence_2d(oracle_lib, space):
+    """kappa(A_LOR^-1 A_HO) bounded in p for the 2D vector spaces (curl-curl / div-div +
+    mass, vertex-rule LOR, warped 3x2 mesh, p = 1..6; SURVEY c.4 bound 12 for 2D ND)"""
+    import scipy.linalg as sla
+    kappas = []
+    for p in range(1, 7):
+        m = mg.box_mesh(2, (3, 2), p, jitter=True)
+        A_lor = _dense(oracle_lib.assemble(m, space, "vertex", 1.0, 1.0))
+        A_ho = _ho2(oracle_lib, m, space, 1.0, 1.0)
+        ev = sla.eigh(A_ho, A_lor, eigvals_only=True)
+        kappas.append(ev.max() / ev.min())
+    print(f"2D {space} kappa(A_LOR^-1 A_HO), p = 1..6: {[round(k, 3) for k in kappas]}")
+    assert max(kappas) <= 12.0, kappas
+    assert kappas[5] - kappas[4] <= kappas[1] - kappas[0]  # increments shrink: no blow-up
