@@ -250,9 +250,10 @@ typedef struct {
   int64_t cap_col_map;
 } lor_parcsr;
 
-/* Operators for lor_parcsr_*: 0 = H1, 1 = ND, 2 = RT (the matrices of lor_assemble_*), 3 = discrete
- * gradient (rows ND, columns H1), 4 = discrete curl (rows RT, columns ND). */
-enum { LOR_OP_H1 = 0, LOR_OP_ND = 1, LOR_OP_RT = 2, LOR_OP_GRAD = 3, LOR_OP_CURL = 4 };
+/* Operators for lor_parcsr_*: 0 = H1, 1 = ND, 2 = RT (the matrices of lor_assemble_*, 2D included), 3 =
+ * discrete gradient (rows ND, columns H1), 4 = discrete curl (rows RT, columns ND; 3D), 5 = rotated
+ * gradient (rows RT, columns H1; 2D). */
+enum { LOR_OP_H1 = 0, LOR_OP_ND = 1, LOR_OP_RT = 2, LOR_OP_GRAD = 3, LOR_OP_CURL = 4, LOR_OP_ROTGRAD = 5 };
 
 /* Symbolic part of the split of the assembled operator A (row_ptr / col as written by the
  * assembly call, DEVICE): per-row diag / offd counts and their scans, the off-rank column set and,

@@ -171,7 +171,7 @@ struct lor_ctx_s {
   int fin_smem = 0;
   int dbg = 0;  // LOR_DBG at setup (dev experiments; 0 in production)
   std::vector<void *> allocs;
-  PcState pc[5];                     // lor_parcsr_* / lor_eliminate_bc per operator
+  PcState pc[6];                     // lor_parcsr_* / lor_eliminate_bc per operator
   double *ca = nullptr, *cb = nullptr;  // variable coefficient E-vectors (lor_set_coefficients)
   // unstructured comparator (lor_legacy_*): LOR element restriction, broken LOR coordinates, element
   // matrices, dof -> (cell, corner) transpose
@@ -191,6 +191,7 @@ struct lor_ctx_s {
     int64_t *off = nullptr, *rp = nullptr;
     double *ea = nullptr;
     std::vector<int32_t> bnd;
+    int64_t *droff = nullptr;  // {0, n}: the one rank's row range (ParCSR)
   } v2[3];
   bool vc = false;
   cudaStream_t side = nullptr;       // marker exchange stream (overlap)
@@ -653,6 +654,11 @@ bool vec2d_setup(lor_ctx c, const HostPlan &plan, std::string &why) {
         dev_upload(c, &V.writer, wr.data(), wr.size()) || dev_alloc(c, &V.cmap, ncell * 4) ||
         dev_alloc(c, &V.csgn, ncell * 4) || dev_alloc(c, &V.ent, ncell * 4) || dev_alloc(c, &V.off, V.n + 1) ||
         dev_alloc(c, &V.rp, V.n + 1) || dev_alloc(c, &V.cnt, V.n + 1) || dev_alloc(c, &V.ea, ncell * 16)) {
+      why = "out of memory";
+      return false;
+    }
+    const int64_t roff[2] = {0, V.n};
+    if (dev_upload(c, &V.droff, roff, 2)) {
       why = "out of memory";
       return false;
     }
@@ -1683,8 +1689,24 @@ bool op_spaces(lor_ctx c, int op, int &rs, int &cs) {
   if (op >= 0 && op <= 2) { rs = cs = op; }
   else if (op == 3) { rs = SP_ND; cs = SP_H1; }
   else if (op == 4) { rs = SP_RT; cs = SP_ND; }
+  else if (op == 5) { rs = SP_RT; cs = SP_H1; }
   else return false;
-  return c->sp[rs].valid && c->sp[cs].valid && (op <= 2 || c->dim == 3);
+  if (c->dim == 2) {  // 2D: ND / RT from lor_vec2d (one rank); gradient and rotated gradient
+    if (op == 4) return false;
+    auto ok = [&](int sp) { return sp == SP_H1 ? c->sp[SP_H1].valid : c->v2[sp].ok; };
+    return ok(rs) && ok(cs);
+  }
+  return op != 5 && c->sp[rs].valid && c->sp[cs].valid;
+}
+
+// rows / columns of an operator: local rows, first row, owned column range, global columns and the
+// device rank ranges of the column space
+void op_dims(lor_ctx c, int rs, int cs, int64_t &n, int64_t &rb, int64_t &cb, int64_t &cn, int64_t &ng,
+             const int64_t *&croff) {
+  if (c->dim == 2 && rs != SP_H1) { n = c->v2[rs].n; rb = 0; }
+  else { n = c->sp[rs].n_local; rb = c->sp[rs].row_begin; }
+  if (c->dim == 2 && cs != SP_H1) { cb = 0; cn = ng = c->v2[cs].n; croff = c->v2[cs].droff; }
+  else { cb = c->sp[cs].row_begin; cn = c->sp[cs].n_local; ng = c->sp[cs].n_global; croff = c->sp[cs].droff; }
 }
 
 template <class T>
@@ -1740,19 +1762,15 @@ lor_status lor_parcsr_prepare(lor_ctx c, int op, const lor_csr *A, int64_t *nnz_
   if (!c || !A || !A->row_ptr) return LOR_ERR_INVALID_ARGUMENT;
   if (!op_spaces(c, op, rs, cs)) return fail(c, LOR_ERR_UNSUPPORTED, "operator not available for this mesh");
   if (c->nranks > 32) return fail(c, LOR_ERR_UNSUPPORTED, "ParCSR split: nranks > 32");
-  const SpaceDev &R = c->sp[rs], &C = c->sp[cs];
   PcState &P = c->pc[op];
   CUDA_TRY(c, cudaSetDevice(c->device));
   P.ready = false;
   P.pending = 0;
-  P.n = R.n_local;
-  P.row_begin = R.row_begin;
-  P.cb = C.row_begin;
-  P.ce = C.row_begin + C.n_local;
+  int64_t cn = 0;
+  op_dims(c, rs, cs, P.n, P.row_begin, P.cb, cn, P.ncols, P.croff);
+  P.ce = P.cb + cn;
   P.square = op <= 2;
-  P.croff = C.droff;
-  P.ncols = C.n_global;
-  P.nw = (C.n_global + 31) / 32;
+  P.nw = (P.ncols + 31) / 32;
   const int64_t n1 = P.n + 1;
   if (!P.bitmap) {  // sizes are topological: allocated once per operator
     if (dev_alloc(c, &P.bitmap, P.nw + 1) || dev_alloc(c, &P.rowmask, n1) || dev_alloc(c, &P.cnt_d, n1) ||

@@ -45,7 +45,7 @@ class _ParCsr(C.Structure):
                 ("cap_col_map", C.c_int64)]
 
 
-OPS = {"h1": 0, "nd": 1, "rt": 2, "grad": 3, "curl": 4}
+OPS = {"h1": 0, "nd": 1, "rt": 2, "grad": 3, "curl": 4, "rotgrad": 5}
 
 
 _lib = None

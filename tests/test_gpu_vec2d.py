@@ -66,3 +66,41 @@ def test_vec2d_coefficients_and_boundary(torch_cuda, oracle_lib):
         compare_full(to_host(rp), to_host(col), to_host(val),
                      oracle_lib.assemble(m, space, "vertex", 1.3, 0.7, coef=(a, b)), 0, q["n_local"], f"2D coef {space}")
         assert np.array_equal(to_host(ctx.boundary_dofs(space)).astype(np.int64), bc.boundary_dofs(m, space))
+
+
+@pytest.mark.parametrize("space", ["nd", "rt"])
+def test_vec2d_parcsr_and_a4(torch_cuda, oracle_lib, space):
+    """NEXT-1 on the 2D vector spaces: ParCSR split (one rank: diag block = the matrix with the
+    diagonal first) and A4 with the boundary dofs, against oracle/bc.py; the 2D gradient / rotated
+    gradient split (all ascending)"""
+    from oracle import bc
+    from paper_2210_12253_b200.lor import LOR
+    m = mg.box_mesh(2, (4, 3), 3, jitter=True, scramble=True)
+    ctx = LOR(m)
+    A = ctx.assemble(space, 1.3, 0.7, "vertex")
+    ctx.sync()
+    P = ctx.parcsr(space, A)
+    ess = ctx.boundary_dofs(space)
+    ctx.eliminate_bc(space, ess, P)
+    ctx.sync()
+    ref = oracle_lib.assemble(m, space, "vertex", 1.3, 0.7)
+    n = ref.row_ptr.shape[0] - 1
+    R = bc.parcsr_split(bc.eliminate(ref, bc.boundary_dofs(m, space)), 0, n, 0, n)
+    assert np.array_equal(to_host(P["diag_row_ptr"]), R["diag_row_ptr"])
+    nd = len(R["diag_col"])
+    assert np.array_equal(to_host(P["diag_col"])[:nd], R["diag_col"])
+    dv = to_host(P["diag_val"])[:nd]
+    mark = np.zeros(n, dtype=bool)
+    mark[bc.boundary_dofs(m, space)] = True
+    rows = np.repeat(np.arange(n), np.diff(R["diag_row_ptr"]))
+    k = mark[rows] | mark[R["diag_col"]]
+    assert np.array_equal(dv[k], R["diag_val"][k])
+    assert np.allclose(dv[~k], R["diag_val"][~k], rtol=1e-12, atol=1e-14 * np.abs(ref.val).max())
+    which = "grad" if space == "nd" else "rotgrad"
+    D = ctx.discrete(which)
+    ctx.sync()
+    PD = ctx.parcsr(which, D)
+    ctx.sync()
+    RD = bc.parcsr_split(oracle_lib.discrete(m, which), 0, n, 0, int(oracle_lib.space_size(m, "h1")[0]), square=False)
+    for key in ("diag_row_ptr", "diag_col", "diag_val"):
+        assert np.array_equal(to_host(PD[key])[:len(RD[key])], RD[key]), key
