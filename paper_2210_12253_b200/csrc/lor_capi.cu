@@ -1498,12 +1498,15 @@ lor_status lor_discrete_grad(lor_ctx c, lor_csr *out) {
   if (!R.valid) return fail(c, LOR_ERR_UNSUPPORTED, "ND not set up (space_mask)");
   if (out->cap_nnz < 2 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 2 n_rows");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 2, c->stream));
   const SpaceDev &Cs = c->sp[SP_H1];
-  if (R.emap && Cs.emap) {
-    DiscMapArgs m{c->p, c->nel_local, c->topo, R.emap, R.esgn, Cs.emap, Cs.esgn, R.row_begin, out->col, out->val};
+  if (R.emap && Cs.emap) {  // one pass: columns, values and the stride row pointer
+    DiscMapArgs m{c->p, c->nel_local, c->topo, R.emap, R.esgn, Cs.emap, Cs.esgn, R.row_begin, out->col, out->val,
+                  out->row_ptr, R.n_local};
+    if (R.n_local == 0) CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, 0, 2, c->stream));
     CUDA_TRY(c, launch_discrete_map(0, m, c->stream));
+    c->launches--;  // no separate row-pointer kernel
   } else {
+    CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 2, c->stream));
     DiscArgs a;
     a.p = c->p;
     a.nel_local = c->nel_local;
@@ -1526,12 +1529,15 @@ lor_status lor_discrete_curl(lor_ctx c, lor_csr *out) {
   if (!R.valid || !c->sp[SP_ND].valid) return fail(c, LOR_ERR_UNSUPPORTED, "RT / ND not set up (space_mask)");
   if (out->cap_nnz < 4 * R.n_local) return fail(c, LOR_ERR_BUFFER_TOO_SMALL, "cap_nnz < 4 n_rows");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 4, c->stream));
   const SpaceDev &Cs = c->sp[SP_ND];
-  if (R.emap && Cs.emap) {
-    DiscMapArgs m{c->p, c->nel_local, c->topo, R.emap, R.esgn, Cs.emap, Cs.esgn, R.row_begin, out->col, out->val};
+  if (R.emap && Cs.emap) {  // one pass: columns, values and the stride row pointer
+    DiscMapArgs m{c->p, c->nel_local, c->topo, R.emap, R.esgn, Cs.emap, Cs.esgn, R.row_begin, out->col, out->val,
+                  out->row_ptr, R.n_local};
+    if (R.n_local == 0) CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, 0, 4, c->stream));
     CUDA_TRY(c, launch_discrete_map(1, m, c->stream));
+    c->launches--;
   } else {
+    CUDA_TRY(c, launch_rowptr_stride(out->row_ptr, R.n_local, 4, c->stream));
     DiscArgs a;
     a.p = c->p;
     a.nel_local = c->nel_local;

@@ -574,6 +574,10 @@ __global__ void __launch_bounds__(128) k_discrete_map(DiscMapArgs A) {
     if ((flags[tr] & (TF_OWNED | TF_MIN)) != (TF_OWNED | TF_MIN)) continue;
     const int64_t row = (int64_t)__ldg(A.rmap + el * ndr + l) - A.row_begin;
     const double sg = (double)__ldg(A.rsgn + el * ndr + l);
+    if (A.row_ptr) {  // the stride row pointer, fused (every owned row is written exactly once)
+      A.row_ptr[row] = (WHICH == 0 ? 2 : 4) * row;
+      if (row == A.n_rows - 1) A.row_ptr[A.n_rows] = (WHICH == 0 ? 2 : 4) * A.n_rows;
+    }
     if (WHICH == 0) {
       const int lt = x[0] + (p + 1) * (x[1] + (p + 1) * x[2]);
       const int lh = lt + (s == 0 ? 1 : (s == 1 ? p + 1 : (p + 1) * (p + 1)));

@@ -162,6 +162,8 @@ struct DiscMapArgs {
   int64_t row_begin;
   int32_t *col;
   double *val;
+  int64_t *row_ptr = nullptr;  // written in the same pass (row_ptr[i] = w i, w = 2 / 4), or null
+  int64_t n_rows = 0;
 };
 
 struct DofmapArgs {
