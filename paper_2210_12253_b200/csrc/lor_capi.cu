@@ -73,7 +73,7 @@ struct SpaceDev {
   int32_t *base[4] = {nullptr, nullptr, nullptr, nullptr};
   ElemSpace *esp = nullptr;
   Ose *ose = nullptr;
-  int32_t *ose_slots = nullptr, *counters = nullptr, *defer = nullptr;
+  int32_t *ose_slots = nullptr, *defer = nullptr;
   int n_ose = 0, n_defer = 0;
   MergeRow *mrows = nullptr;  // merge-pass rows
   int64_t *ownbase = nullptr;  // own-row position table: first row per element
@@ -466,7 +466,6 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   a.rstride = S.rstride;
   a.ose = S.ose;
   a.ose_slots = S.ose_slots;
-  a.counters = S.counters;
   a.nval = S.nval;
   a.ose_elem = S.ose_elem;
   a.pbase = S.pbase;
@@ -967,7 +966,6 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     if (dev_upload(c, &S.defer, P.defer.data(), P.defer.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "defer");
     S.n_ose = (int)P.ose.size();
     S.n_defer = (int)P.defer.size();
-    if (dev_alloc(c, &S.counters, P.ose.size()) != cudaSuccess) return bail(LOR_ERR_OUT_OF_MEMORY, "counters");
     S.n_records = P.n_records;
     if (P.n_records > 0) {
       cudaError_t e = cudaMalloc((void **)&S.scratch, (size_t)P.n_records * S.rstride * sizeof(RecEntry));
@@ -1064,8 +1062,7 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
     a.rstride = S.rstride;
     a.ose = S.ose;
     a.ose_slots = S.ose_slots;
-    a.counters = S.counters;
-    a.maxl = S.maxl;
+      a.maxl = S.maxl;
     a.plan_mode = 1;
     a.alpha = 1.0;
     a.beta = 1.0;

@@ -32,8 +32,7 @@ enum : uint8_t {
   SF_SEND = 4,    // entity owned by another rank: records go to the send region
 };
 
-constexpr int MAX_VALENCE = 16;           // weights use lcm(1..16) = 720720
-constexpr int WEIGHT_L = 720720;
+constexpr int MAX_VALENCE = 16;           // elements sharing a coarse entity (setup check)
 
 // One per element (local elements first, then ghost elements).  3D uses 27 slots, 2D 9.
 struct __align__(16) ElemTopo {

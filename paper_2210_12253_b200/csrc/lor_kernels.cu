@@ -5,17 +5,16 @@
 //               under the minimal-macro-element rule; exclusive rows are
 //               stored, shared rows accumulated with integer atomics.
 //   k_scan      A2: decoupled look-back exclusive scan -> int64 row_ptr.
-//   k_assemble  A1 + A2 part 2, fused: one CTA per macro element ("one block of
-//               threads per macro element"): sub-cell matrices from the E-vector geometry staged
-//               in shared memory (never written to HBM), then per local row the values gathered
-//               from the <= 2^d cells containing it and the columns emitted in ascending global
-//               order from the element's affine "block" numbering (no sort).  Rows owned by one
-//               element go straight to CSR; rows on shared coarse entities go to per-element
-//               partial-row records, merged by the LAST element to arrive (integer counter),
-//               which writes the final row -- the "minimal element" duplicate rule of l.358 is
-//               replaced by exact weighted merge counts.
-//   k_finalize_deferred  interface rows whose partial rows came over NCCL (A3 replacement).
-//   k_grad / k_curl      discrete gradient (Algorithm 1, l.417-438) / curl (l.440-445).
+//   k_assemble  A1 + A2 part 2 of the general path (lor_asm.cuh; Gauss-2, 2D H1, variable-coefficient
+//               ND, ...): one CTA per macro element ("one block of threads per macro
+//               element"): sub-cell matrices staged in shared memory (never written to HBM), then per
+//               local row the values gathered from the <= 2^d cells containing it and the columns
+//               emitted in ascending global order from the element's affine "block" numbering (no
+//               sort).  Rows owned by one element go straight to CSR; rows on shared coarse
+//               entities go out as natural-order partial rows, summed by k_merge_rows with the setup
+//               merge plan.
+//   k_finalize_list  interface rows whose partial rows came over NCCL (A3 replacement).
+//   k_discrete_map / k_discrete  discrete gradient (Algorithm 1, l.417-438) / curl (l.440-445).
 //   k_dofmap    element restriction (for parity tests of the numbering).
 //   k_coords    LOR vertex coordinate vectors: E-vector -> owned H1 dofs.
 #include <cuda_runtime.h>

@@ -73,7 +73,6 @@ struct AsmArgs {
   int rstride;                   // entries per record
   const Ose *ose;
   const int32_t *ose_slots;
-  int32_t *counters;
   // shared rows whose contributors are all local: every contributor
   // writes its partial row in natural stencil-slot order; the last one to arrive emits the row
   double *nval;                  // [nel_local][NDPE][rec_w8(W)] natural-order partial rows (row sign applied)

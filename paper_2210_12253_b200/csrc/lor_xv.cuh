@@ -359,15 +359,38 @@ __global__ void __launch_bounds__(128) k_xv_sym(XvArgs A) {
   const int chi[3] = {(int8_t)((hw.y >> 24) & 255), (int8_t)(hw.z & 255), (int8_t)((hw.z >> 8) & 255)};
   const uint32_t own = (uint32_t)hw.x;
   __syncthreads();
-  // all rows of the element in family-major warp-aligned segments (no divergence between the
-  // families' unrolled code paths within a warp)
+  // the element's OWNED rows, compacted per family (about 2/3 of its dofs), then processed in
+  // family-major warp-aligned segments (no divergence between the families' unrolled code paths
+  // within a warp, no lanes spent on rows other elements own)
   constexpr int NRF2 = CF::NRF2, NRF0 = CF::NRF0;
   constexpr int NF2 = (P + 1) * NRF2, NF0 = (P + 1) * NRF0;
   constexpr int B0 = (NF2 + 31) / 32 * 32, B1 = B0 + (NF0 + 31) / 32 * 32, NT = B1 + NF0;
-  for (int i = tid; i < NT; i += 128) {
+  __shared__ uint16_t s_list[3][NF2 > NF0 ? NF2 : NF0];
+  __shared__ int s_nf[3];
+  if (tid < 3) s_nf[tid] = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < NT; i0 += 128) {
+    const int i = i0 + tid;
+    int s = -1, x[3];
+    const bool ok = i < NT && group_row<P, SP, P + 1, B0, B1, NF2, NF0>(0, i, s, x) && ((own >> dof_tau<P, SP>(s, x)) & 1);
+    // segments are warp-aligned per family: a warp's slots belong to one family
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    int base = 0;
+    const int fam = __shfl_sync(0xffffffffu, s, __ffs(m | 0x80000000u) - 1);
+    if ((tid & 31) == 0 && m) base = atomicAdd(&s_nf[fam], __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (ok) s_list[s][base + __popc(m & ((1u << (tid & 31)) - 1u))] = (uint16_t)i;
+  }
+  __syncthreads();
+  const int n2 = s_nf[2], n0 = s_nf[0], n1 = s_nf[1];
+  const int c0 = (n2 + 31) / 32 * 32, c1 = c0 + (n0 + 31) / 32 * 32, ct = c1 + n1;
+  for (int t = tid; t < ct; t += 128) {
+    int fam, k;
+    if (t < c0) { fam = 2; k = t; if (k >= n2) continue; }
+    else if (t < c1) { fam = 0; k = t - c0; if (k >= n0) continue; }
+    else { fam = 1; k = t - c1; }
     int s, x[3];
-    if (!group_row<P, SP, P + 1, B0, B1, NF2, NF0>(0, i, s, x)) continue;
-    if (!((own >> dof_tau<P, SP>(s, x)) & 1)) continue;
+    group_row<P, SP, P + 1, B0, B1, NF2, NF0>(0, s_list[fam][k], s, x);
     if (s == 0) sym_row<P, NB, SP, 0>(A, x, clo, chi, XV, s_pos + tid * 36);
     else if (s == 1) sym_row<P, NB, SP, 1>(A, x, clo, chi, XV, s_pos + tid * 36);
     else sym_row<P, NB, SP, 2>(A, x, clo, chi, XV, s_pos + tid * 36);
