@@ -3,8 +3,8 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 TAG=r02_v3
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu_r02_v4.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu_r02_v4.log
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r02_v4.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke_r02_v4.log
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu_r02_v6.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu_r02_v6.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r02_v6.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke_r02_v6.log
 for cfg in C4 C5 C4-J C5-J C5-V; do
   timeout 900 python bench.py --config $cfg > gpurun_out/bench_${TAG}_$cfg.json 2>> gpurun_out/bench.err; echo "bench $cfg rc=$?"
 done
