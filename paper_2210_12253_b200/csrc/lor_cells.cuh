@@ -18,6 +18,10 @@
 
 #include "lor_device.cuh"
 
+#ifndef ND_FENCE
+#define ND_FENCE 1  // cell_nd_vertex_to: corners between compiler fences
+#endif
+
 namespace lorb {
 
 // ---------------------------------------------------------------- reference cell tables (ND/RT)
@@ -398,7 +402,7 @@ __device__ __forceinline__ bool cell_nd_vertex_to(XF X, double alpha, double bet
   bool ok = true;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    asm volatile("" ::: "memory");  // one corner at a time (register pressure)
+    if (q % ND_FENCE == 0) asm volatile("" ::: "memory");  // ND_FENCE corners at a time (registers vs ILP)
     Jac3 J;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {

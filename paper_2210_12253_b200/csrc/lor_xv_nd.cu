@@ -1,4 +1,7 @@
 // lor_xv_nd.cu -- Nedelec instantiations of the extended-frame vector-space kernels (lor_xv.cuh).
+// four cell corners between compiler fences in the ND cell routine (more ILP in the cell phase of
+// k_xv_fill; C4 fill 3.23 -> 3.18 ms; the element pass keeps one at a time)
+#define ND_FENCE 4
 #include "lor_xv.cuh"
 
 namespace lorb {
