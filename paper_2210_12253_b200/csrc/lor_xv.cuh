@@ -26,6 +26,9 @@
 #include "lor_xdev.cuh"
 #include "lor_xframe.h"
 
+#ifndef XV_PF_ROWS
+#define XV_PF_ROWS 0  // k_xv_fill: L2 prefetch of the next-residency CTA's row pointers / positions
+#endif
 #ifndef XV_RT_GZ
 #define XV_RT_GZ(P) ((P) + 1)  // RT with resident cells: row layers per group (all of them)
 #endif
@@ -642,6 +645,25 @@ __global__ void __launch_bounds__(128, MINB) k_xv_fill(XvArgs A) {
   }
   __syncthreads();
   const double alpha = A.alpha, beta = A.beta;
+  // L2 prefetch of the row pointers and slot positions of the rows of the CTA one residency later
+  // (their addresses need its record and extended restriction, prefetched into L2 at the start):
+  // the dependent chain record -> restriction -> row_ptr / positions of its first row group
+  if (XV_PF_ROWS && A.pf_dist > 0 && bs + A.pf_dist < A.nel_local) {
+    const int64_t nbs = bs + A.pf_dist;
+    const int4 nh = __ldg(reinterpret_cast<const int4 *>(A.xe + nbs));
+    const int nclo[3] = {(int8_t)(nh.y & 255), (int8_t)((nh.y >> 8) & 255), (int8_t)((nh.y >> 16) & 255)};
+    const uint32_t nown = (uint32_t)nh.x;
+    for (int tg = tid; tg < CF::MAXG; tg += 128) {
+      int sf = 0, xx[3];
+      if (!group_row<P, SP, CF::GZ, CF::B0, CF::B1, CF::NF2, CF::NF0>(0, tg, sf, xx) || !((nown >> dof_tau<P, SP>(sf, xx)) & 1))
+        continue;
+      const int u[3] = {xx[0] - nclo[0], xx[1] - nclo[1], xx[2] - nclo[2]};
+      const int idx = sf == 0 ? fidx<SP, NB>(0, u) : (sf == 1 ? fidx<SP, NB>(1, u) : fidx<SP, NB>(2, u));
+      const int64_t r = (int64_t)(__ldg(A.xvmap + nbs * 3 * CF::NVF + sf * CF::NVF + idx) & 0x7fffffffu) - A.row_begin;
+      pf_l2(A.row_ptr + r);
+      pf_l2(A.pos + r * CF::PW);
+    }
+  }
   for (int z = 0; z <= P; z += CF::GZ) {
     // cell layers of this row layer: z - 1 (first layer only; later it is still resident) and z
     // cells: all layers at the first row layer (ONE), else layer z (and z - 1 at the first)

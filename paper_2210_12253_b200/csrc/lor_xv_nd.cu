@@ -2,6 +2,9 @@
 // four cell corners between compiler fences in the ND cell routine (more ILP in the cell phase of
 // k_xv_fill; C4 fill 3.23 -> 3.18 ms; the element pass keeps one at a time)
 #define ND_FENCE 4
+// and the next-residency CTA's row pointers / positions prefetched into L2 (C4 fill 3.18 -> 3.15 ms;
+// RT is slower with it: 0.90 -> 1.00 ms)
+#define XV_PF_ROWS 1
 #include "lor_xv.cuh"
 
 namespace lorb {
