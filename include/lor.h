@@ -183,6 +183,11 @@ lor_status lor_update_coordinates(lor_ctx ctx, const double *elem_nodes);
  * variable coefficients every space takes the element + merge passes (lor_fill_path returns 0).
  * INVALID_ARGUMENT if exactly one pointer is NULL. */
 lor_status lor_set_coefficients(lor_ctx ctx, const double *alpha_e, const double *beta_e);
+/* The same from the GLOBAL coefficient E-vectors [n_elem][(p+1)^dim] (HOST, every rank passes the
+ * whole mesh's, as elem_nodes at setup): the context also keeps the coefficients of its ghost layer,
+ * so on several ranks H1 and RT keep the extended-frame single pass with variable coefficients
+ * (lor_set_coefficients alone: the element + merge passes there).  Synchronous. */
+lor_status lor_set_coefficients_global(lor_ctx ctx, const double *alpha_all, const double *beta_all);
 
 /* Unstructured ("legacy") comparator -- NOT the product path:
  * the LOR mesh treated as an arbitrary low-order hex mesh.  lor_legacy_setup builds the explicit LOR

@@ -173,6 +173,9 @@ struct lor_ctx_s {
   std::vector<void *> allocs;
   PcState pc[6];                     // lor_parcsr_* / lor_eliminate_bc per operator
   double *ca = nullptr, *cb = nullptr;  // variable coefficient E-vectors (lor_set_coefficients)
+  bool vc_ghosts = false;               // ca / cb also hold the ghost layer (lor_set_coefficients_global)
+  double *ca_l = nullptr, *cb_l = nullptr, *ca_g = nullptr, *cb_g = nullptr;  // local-only / with ghosts
+  std::vector<int64_t> xghost_ids;      // global ids of the ghost-layer elements (after the local ones)
   // unstructured comparator (lor_legacy_*): LOR element restriction, broken LOR coordinates, element
   // matrices, dof -> (cell, corner) transpose
   int64_t leg_ncell = 0;
@@ -391,7 +394,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   lor_status st = LOR_OK;
   // variable coefficients on the ND frame would need 2 more E-vector boxes beside 78 KB of resident
   // cells: 1 CTA/SM, slower (7.3 vs 5.2 ms at C4) than the element + merge passes
-  if (S.xvok && quad == LOR_QUAD_VERTEX && (!c->vc || (c->nranks == 1 && s == SP_RT))) {  // ND / RT extended frame
+  if (S.xvok && quad == LOR_QUAD_VERTEX && (!c->vc || ((c->nranks == 1 || c->vc_ghosts) && s == SP_RT))) {  // ND / RT extended frame
     XvArgs x = xv_args(c, s);
     if (!reuse) {
       CUDA_TRY(c, launch_xv_sym(s, c->p, x, c->stream));
@@ -417,7 +420,7 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
   }
   // variable coefficients: the extended frames on one rank (the neighbour coefficients come from the
   // local E-vectors), the element + merge passes otherwise
-  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX && (!c->vc || c->nranks == 1);
+  const bool xpath = S.xok && quad == LOR_QUAD_VERTEX && (!c->vc || c->nranks == 1 || c->vc_ghosts);
   if (!reuse) {  // symbolic part (A2): row lengths per call, then the int64 scan
     if (xpath) {
       XFillArgs x = xfill_args(c, S);
@@ -523,6 +526,7 @@ bool xframe_ghost_layer(lor_ctx c, const HostPlan &plan, const lor_setup_args &A
                         std::string &why) {
   const int64_t ng = (int64_t)xg.size();
   c->n_xghost = ng;
+  c->xghost_ids = xg;
   if (ng == 0) return true;
   const int np = (A.dim == 3) ? (A.p + 1) * (A.p + 1) * (A.p + 1) : (A.p + 1) * (A.p + 1);
   const int64_t raw = (int64_t)A.dim * np;
@@ -1387,6 +1391,8 @@ lor_status lor_update_coordinates(lor_ctx c, const double *elem_nodes) {
 lor_status lor_set_coefficients(lor_ctx c, const double *alpha_e, const double *beta_e) {
   if (!c || (!alpha_e) != (!beta_e)) return LOR_ERR_INVALID_ARGUMENT;
   CUDA_TRY(c, cudaSetDevice(c->device));
+  c->vc_ghosts = false;
+  if (c->ca_l) { c->ca = c->ca_l; c->cb = c->cb_l; }  // back to the local-only arrays
   if (!alpha_e) {
     c->vc = false;
     return LOR_OK;
@@ -1396,6 +1402,8 @@ lor_status lor_set_coefficients(lor_ctx c, const double *alpha_e, const double *
   if (!c->ca) {
     if (dev_alloc(c, &c->ca, bytes / sizeof(double)) || dev_alloc(c, &c->cb, bytes / sizeof(double)))
       return fail(c, LOR_ERR_OUT_OF_MEMORY, "coefficient E-vectors");
+    c->ca_l = c->ca;
+    c->cb_l = c->cb;
   }
   if (c->nel_local > 0) {
     CUDA_TRY(c, cudaMemcpyAsync(c->ca, alpha_e, sizeof(double) * c->nel_local * np, cudaMemcpyDefault, c->stream));
@@ -1445,6 +1453,32 @@ lor_status lor_legacy_assemble_h1(lor_ctx c, double alpha, double beta, lor_csr 
   CUDA_TRY(c, launch_leg_rows(a, true, c->stream));
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   c->launches += 4;
+  return LOR_OK;
+}
+
+lor_status lor_set_coefficients_global(lor_ctx c, const double *alpha_all, const double *beta_all) {
+  if (!c || !alpha_all || !beta_all) return LOR_ERR_INVALID_ARGUMENT;
+  const int64_t np = (c->dim == 3) ? (int64_t)(c->p + 1) * (c->p + 1) * (c->p + 1) : (int64_t)(c->p + 1) * (c->p + 1);
+  lor_status st = lor_set_coefficients(c, alpha_all + c->elem_begin * np, beta_all + c->elem_begin * np);
+  if (st || c->n_xghost == 0) return st;
+  // the ghost layer's coefficients after the local ones (the layout of the coordinate array X)
+  const int64_t nl = c->nel_local, ng = c->n_xghost;
+  if (!c->ca_g && (dev_alloc(c, &c->ca_g, (nl + ng) * np) || dev_alloc(c, &c->cb_g, (nl + ng) * np)))
+    return fail(c, LOR_ERR_OUT_OF_MEMORY, "ghost coefficients");
+  double *a2 = c->ca_g, *b2 = c->cb_g;
+  CUDA_TRY(c, cudaMemcpyAsync(a2, c->ca, sizeof(double) * nl * np, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(b2, c->cb, sizeof(double) * nl * np, cudaMemcpyDeviceToDevice, c->stream));
+  std::vector<double> ga((size_t)(ng * np)), gb((size_t)(ng * np));
+  for (int64_t g = 0; g < ng; ++g) {
+    memcpy(&ga[(size_t)(g * np)], alpha_all + c->xghost_ids[(size_t)g] * np, sizeof(double) * np);
+    memcpy(&gb[(size_t)(g * np)], beta_all + c->xghost_ids[(size_t)g] * np, sizeof(double) * np);
+  }
+  CUDA_TRY(c, cudaMemcpy(a2 + nl * np, ga.data(), sizeof(double) * ga.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaMemcpy(b2 + nl * np, gb.data(), sizeof(double) * gb.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->ca = a2;
+  c->cb = b2;
+  c->vc_ghosts = true;
   return LOR_OK;
 }
 
@@ -1667,7 +1701,8 @@ int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int
 
 int lor_fill_path(lor_ctx c, lor_space space) {
   if (!c || space < 0 || space > 2 || !c->sp[space].valid) return -1;
-  if (c->vc) return ((c->sp[space].xok || (space == LOR_RT && c->sp[space].xvok)) && c->nranks == 1) ? 1 : 0;
+  if (c->vc)
+    return ((c->sp[space].xok || (space == LOR_RT && c->sp[space].xvok)) && (c->nranks == 1 || c->vc_ghosts)) ? 1 : 0;
   return (c->sp[space].xok || c->sp[space].xvok) ? 1 : 0;
 }
 

@@ -98,6 +98,7 @@ def lib():
         L.lor_parcsr_exchange_counts.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.lor_coordinates.argtypes = [C.c_void_p, C.c_void_p]
         L.lor_set_coefficients.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.lor_set_coefficients_global.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.lor_legacy_setup.argtypes = [C.c_void_p]
         L.lor_legacy_assemble_h1.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(_Csr)]
         _lib = L
@@ -416,6 +417,13 @@ class LOR:
         self._coef = (a, b)  # keep alive until the copy on the context stream has run
         self._check(lib().lor_set_coefficients(self.h, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr())))
         self.sync()
+
+    def set_coefficients_global(self, a, b):
+        """Coefficient E-vectors of the WHOLE mesh [n_elem, (p+1)^dim] (host numpy): the context keeps its
+        local elements' and its ghost layer's (extended frames across ranks)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        self._check(lib().lor_set_coefficients_global(self.h, a.ctypes.data, b.ctypes.data))
 
     # ------------------------------------------------------------------ unstructured comparator (NEXT-4)
     def legacy_setup(self):

@@ -100,3 +100,23 @@ def test_coef_reassemble_and_reset(torch_cuda, oracle_lib, space):
     ctx.sync()
     compare_full(*(to_host(t) for t in out), oracle_lib.assemble(m, space, "vertex", 1.3, 0.7), 0, q["n_local"],
                  f"{space} constant again")
+
+
+@pytest.mark.parametrize("space", ["h1", "rt"])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_coef_multirank_extended_frame(torch_cuda, oracle_lib, space, nranks):
+    """global coefficient E-vectors: every rank keeps its ghost layer's coefficients and the
+    extended-frame single pass (no partial-row exchange), rows equal to the oracle's"""
+    from paper_2210_12253_b200.lor import LOR
+    m = mg.box_mesh(3, (2, 3, 2 * nranks), 3, kershaw=0.3, scramble=True, nranks=nranks)
+    a, b = _coefs(m)
+    ref = oracle_lib.assemble(m, space, "vertex", 1.3, 0.7, nranks=nranks, coef=(a, b))
+    for r in range(nranks):
+        c = LOR(m, rank=r, nranks=nranks)
+        c.set_coefficients_global(a, b)
+        assert c.fill_path(space) == 1
+        q = c.query(space)
+        out = c.assemble(space, 1.3, 0.7, "vertex")
+        c.sync()
+        compare_full(*(to_host(t) for t in out), ref, q["row_begin"], q["n_local"], f"{space} coef rank {r}/{nranks}")
+        c.close()
