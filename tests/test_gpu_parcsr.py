@@ -202,24 +202,28 @@ def test_coordinates(torch_cuda, oracle_lib, dim, p, nranks):
         ctx.close()
 
 
-def test_parcsr_eliminate_fullsize_c2(torch_cuda):
-    """C2 (2.1 M rows): split + A4 on the full headline matrix -- properties that hold at any size:
-    row pointers add up, diagonal first, unit rows of the boundary dofs, no entry of a boundary
-    column left, every other value equal to the assembled one."""
+@pytest.mark.parametrize("cfg", ["C2", "C4", "C5"])
+def test_parcsr_eliminate_fullsize(torch_cuda, cfg):
+    """C2 / C4 / C5 at full size: split + A4 on the full matrix -- properties that hold at any size:
+    the number of boundary dofs (closed form of the LOR surface lattice), row pointers, diagonal
+    first, unit rows of the boundary dofs, no entry of a boundary column left, every other value
+    equal to the assembled one"""
     import torch
     from paper_2210_12253_b200.lor import LOR
-    m, form = mg.config_mesh("C2")
+    m, form = mg.config_mesh(cfg)
+    sp = form["space"]
     ctx = LOR(m)
-    A = ctx.assemble("h1", 1.0, 1.0, "vertex")
+    A = ctx.assemble(sp, 1.0, 1.0, "vertex")
     ctx.sync()
-    P = ctx.parcsr("h1", A)
-    ess = ctx.boundary_dofs("h1")
-    Nc = 32 * 4
-    assert ess.numel() == (Nc + 1) ** 3 - (Nc - 1) ** 3
+    P = ctx.parcsr(sp, A)
+    ess = ctx.boundary_dofs(sp)
+    N = 32 * 4
+    closed = {"h1": (N + 1) ** 3 - (N - 1) ** 3, "nd": 3 * N * ((N + 1) ** 2 - (N - 1) ** 2), "rt": 6 * N * N}[sp]
+    assert ess.numel() == closed
     ctx.sync()
     assert P["sizes"][1] == 0 and P["sizes"][2] == 0
     assert torch.equal(P["diag_row_ptr"], A[0])
-    ctx.eliminate_bc("h1", ess, P)
+    ctx.eliminate_bc(sp, ess, P)
     ctx.sync()
     rp = P["diag_row_ptr"]
     n = rp.numel() - 1
