@@ -182,6 +182,7 @@ struct lor_ctx_s {
   int32_t *leg_lmap = nullptr, *leg_ent = nullptr;
   double *leg_lx = nullptr, *leg_ea = nullptr;
   int64_t *leg_off = nullptr;
+  bool h1_rows = false;  // p = 1, one rank: H1 through the per-row path (lor_setup)
   // 2D Nedelec / Raviart-Thomas (lor_vec2d.cu, one rank): per space the element restriction with
   // signs, the row writers of the discrete operators, the LOR cells' signed dofs, the dof -> cell
   // transpose, the cell matrices, sizes and the boundary dofs
@@ -413,6 +414,22 @@ lor_status assemble(lor_ctx c, int s, double alpha, double beta, lor_quad quad, 
     x.values_only = reuse ? 1 : 0;
     CUDA_TRY(c, launch_xv_fill(s, c->p, x, c->stream));
     if (c->nel_local > 0) c->launches++;
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    return LOR_OK;
+  }
+  if (s == SP_H1 && c->h1_rows && !c->vc && quad == LOR_QUAD_VERTEX) {  // p = 1 per-row path (lor_setup)
+    LegArgs a{S.n_local, c->leg_off, c->leg_ent, c->leg_lmap, c->leg_ea, out->row_ptr, out->col, out->val, S.cnt};
+    if (!reuse) {
+      CUDA_TRY(c, launch_leg_rows(a, false, c->stream));
+      CUDA_TRY(c, launch_scan(S.cnt, out->row_ptr, S.n_local, S.scan_status, S.tile_ctr, c->stream));
+      c->launches += 2;
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
+    CUDA_TRY(c, launch_leg_ea(c->leg_ncell, 1, c->leg_lx, alpha, beta, c->leg_ea, c->err, c->stream));
+    CUDA_TRY(c, launch_leg_rows(a, true, c->stream));
+    c->launches += 2;
     CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
@@ -719,6 +736,15 @@ lor_status vec2d_discrete(lor_ctx c, int sp, lor_csr *out) {
   CUDA_TRY(c, launch_v2_disc(d, c->stream));
   c->launches += 2;
   return LOR_OK;
+}
+
+// Orders at which the one-pass extended frame of a vector space beats the element + merge passes on
+// one GPU (full calls, Cartesian N^3-cell meshes, N = 96 / 105, 1xB200, profiles/vector_sweep_r02_v4.jsonl):
+// ND at p = 4-5 only (1.2-1.3x faster there; 1.3-2.7x slower at p = 1-3, 6, 7), RT at every order
+// but 5 (1.2-1.6x faster; 1.4x slower at p = 5, a tie at 6).
+bool xv_preferred(int sv, int p) {
+  if (sv == SP_ND) return p == 4 || p == 5;
+  return p != 5;
 }
 
 }  // namespace
@@ -1222,6 +1248,10 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
         if (!V.valid || (xv_env && !atoi(xv_env)) || (sv == SP_ND && xvnd_env && !atoi(xvnd_env)) ||
             !xv_supported(sv, A.p, S.xc))
           continue;
+        // one rank: the frame only at the orders where it measured faster than the element + merge
+        // passes (xv_preferred); several ranks: wherever it fits (it needs no partial-row exchange).
+        // LOR_XV=1 forces it at every supported order (tests).
+        if (A.nranks == 1 && !(xv_env && atoi(xv_env) == 1) && !xv_preferred(sv, A.p)) continue;
         if (dev_alloc(c, &V.xvmap, (size_t)c->nel_local * xv_map_words(sv, A.p, S.xc)) != cudaSuccess ||
             dev_alloc(c, &V.xvpos, (size_t)std::max<int64_t>(V.n_local, 1) * xv_pos_words(sv)) != cudaSuccess)
           return bail(LOR_ERR_OUT_OF_MEMORY, "xframe (vector spaces)");
@@ -1273,6 +1303,15 @@ lor_status lor_setup(const lor_setup_args *args, lor_ctx *out) {
   if (A.dim == 2 && A.nranks == 1) {
     std::string why2;
     if (!vec2d_setup(c, plan, why2)) return bail(LOR_ERR_CUDA, "2D vector spaces: " + why2);
+  }
+  // p = 1: a macro-element is a single LOR cell, nothing of its structure is left to exploit, and
+  // one CTA per element spends its time on per-element overhead; on one rank the H1 assembly takes
+  // the per-row path of lor_legacy.cu instead (dense 8x8 cell matrices, one warp per row over the
+  // dof -> cell transpose; 4.4x faster at 96^3 elements). LOR_ROWPATH=0 keeps the extended frame.
+  if (A.dim == 3 && A.p == 1 && A.nranks == 1 && c->sp[SP_H1].valid && c->nel_local > 0 &&
+      !(getenv("LOR_ROWPATH") && !atoi(getenv("LOR_ROWPATH")))) {
+    c->h1_rows = lor_legacy_setup(c) == LOR_OK;
+    c->last_error.clear();
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(LOR_ERR_CUDA, "setup sync");
   *out = c;
@@ -1385,6 +1424,8 @@ lor_status lor_update_coordinates(lor_ctx c, const double *elem_nodes) {
   if (c->nel_local > 0)
     CUDA_TRY(c, cudaMemcpy2DAsync(c->X, c->xstride * sizeof(double), elem_nodes, raw, raw, (size_t)c->nel_local,
                                   cudaMemcpyDefault, c->stream));
+  if (c->leg_lmap)  // the broken LOR coordinates of the per-row path follow
+    CUDA_TRY(c, launch_leg_mesh(c->p, c->nel_local, c->sp[SP_H1].emap, c->X, c->xstride, c->leg_lmap, c->leg_lx, c->stream));
   return exchange_ghost_coords(c);  // extended frame on several ranks: the ghost layer follows
 }
 
@@ -1444,7 +1485,7 @@ lor_status lor_legacy_assemble_h1(lor_ctx c, double alpha, double beta, lor_csr 
   CUDA_TRY(c, cudaSetDevice(c->device));
   c->nphase = 0;
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
-  CUDA_TRY(c, launch_leg_ea(c->leg_ncell, c->leg_lx, alpha, beta, c->leg_ea, c->err, c->stream));
+  CUDA_TRY(c, launch_leg_ea(c->leg_ncell, c->p * c->p * c->p, c->leg_lx, alpha, beta, c->leg_ea, c->err, c->stream));
   CUDA_TRY(c, cudaEventRecord(c->ev[c->nphase++], c->stream));
   LegArgs a{S.n_local, c->leg_off, c->leg_ent, c->leg_lmap, c->leg_ea, out->row_ptr, out->col, out->val, S.cnt};
   CUDA_TRY(c, launch_leg_rows(a, false, c->stream));
@@ -1701,6 +1742,7 @@ int64_t lor_debug_dump(lor_ctx c, int what, lor_space space, void *host_out, int
 
 int lor_fill_path(lor_ctx c, lor_space space) {
   if (!c || space < 0 || space > 2 || !c->sp[space].valid) return -1;
+  if (space == LOR_H1 && c->h1_rows && !c->vc) return 2;
   if (c->vc)
     return ((c->sp[space].xok || (space == LOR_RT && c->sp[space].xvok)) && (c->nranks == 1 || c->vc_ghosts)) ? 1 : 0;
   return (c->sp[space].xok || c->sp[space].xvok) ? 1 : 0;

@@ -13,7 +13,8 @@
 //                (column, value) pairs of the <= 8 cells containing the row through the transpose,
 //                ranks them by (column, candidate index) in shared memory, and counts / writes the
 //                distinct columns in ascending order with the duplicates summed in candidate order.
-// H1, 3D, vertex rule.  A comparator, not the product path.
+// H1, 3D, vertex rule.  The comparator of lor_legacy_*; at p = 1 (a macro-element is one LOR cell)
+// also the product path of lor_assemble_h1 on one rank (lor_fill_path 2).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,7 +42,7 @@ __global__ void k_leg_mesh(int p, int64_t nel, const int32_t *__restrict__ emap,
 
 constexpr int EA_T = 64;  // cells per block of k_leg_ea
 
-__global__ void __launch_bounds__(EA_T) k_leg_ea(int64_t ncell, const double *__restrict__ lx, double alpha,
+__global__ void __launch_bounds__(EA_T) k_leg_ea(int64_t ncell, int ncpe, const double *__restrict__ lx, double alpha,
                                                   double beta, double *__restrict__ ea, int *err) {
   __shared__ double s[EA_T * 64];
   const int64_t c0 = (int64_t)blockIdx.x * EA_T;
@@ -53,7 +54,10 @@ __global__ void __launch_bounds__(EA_T) k_leg_ea(int64_t ncell, const double *__
 #pragma unroll
       for (int d = 0; d < 3; ++d) C[q][d] = lx[cell * 24 + d * 8 + q];
     double A[36];
-    if (!cell_h1_3d<0>(C, alpha, beta, A)) atomicExch(err, 1);
+    if (!cell_h1_3d<0>(C, alpha, beta, A) && atomicCAS(err, 0, 1) == 0) {  // (element, cell) as lor_sync reports
+      err[1] = (int)(cell / ncpe);
+      err[2] = (int)(cell % ncpe);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -146,9 +150,9 @@ cudaError_t launch_leg_mesh(int p, int64_t nel, const int32_t *emap, const doubl
   if (n > 0) k_leg_mesh<<<nblk(n, 256), 256, 0, st>>>(p, nel, emap, X, xstride, lmap, lx);
   return cudaGetLastError();
 }
-cudaError_t launch_leg_ea(int64_t ncell, const double *lx, double alpha, double beta, double *ea, int *err,
+cudaError_t launch_leg_ea(int64_t ncell, int ncpe, const double *lx, double alpha, double beta, double *ea, int *err,
                           cudaStream_t st) {
-  if (ncell > 0) k_leg_ea<<<nblk(ncell, EA_T), EA_T, 0, st>>>(ncell, lx, alpha, beta, ea, err);
+  if (ncell > 0) k_leg_ea<<<nblk(ncell, EA_T), EA_T, 0, st>>>(ncell, ncpe, lx, alpha, beta, ea, err);
   return cudaGetLastError();
 }
 cudaError_t launch_leg_rows(const LegArgs &a, bool fill, cudaStream_t st) {

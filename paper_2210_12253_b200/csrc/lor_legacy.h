@@ -19,7 +19,7 @@ struct LegArgs {
 
 cudaError_t launch_leg_mesh(int p, int64_t nel, const int32_t *emap, const double *X, int64_t xstride, int32_t *lmap,
                             double *lx, cudaStream_t st);
-cudaError_t launch_leg_ea(int64_t ncell, const double *lx, double alpha, double beta, double *ea, int *err,
+cudaError_t launch_leg_ea(int64_t ncell, int ncpe, const double *lx, double alpha, double beta, double *ea, int *err,
                           cudaStream_t st);
 cudaError_t launch_leg_rows(const LegArgs &a, bool fill, cudaStream_t st);
 

@@ -66,7 +66,8 @@ def run(O, m, expect_path, alpha=1.3, beta=0.7, what=""):
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 8])
 @pytest.mark.parametrize("kind", ["cartesian", "jitscr", "kershaw", "shuffled"])
-def test_xframe_parity(torch_cuda, oracle_lib, kind, p):
+def test_xframe_parity(torch_cuda, oracle_lib, monkeypatch, kind, p):
+    monkeypatch.setenv("LOR_ROWPATH", "0")  # p = 1 takes the per-row path by default (test_gpu_rowpath.py)
     shape = (3, 3, 2) if p <= 4 else (2, 2, 2)
     if kind == "cartesian":
         m = mg.box_mesh(3, shape, p)
@@ -82,7 +83,7 @@ def test_xframe_parity(torch_cuda, oracle_lib, kind, p):
 @pytest.mark.parametrize("p", [1, 2, 4])
 def test_irregular_mesh_uses_general_path(torch_cuda, oracle_lib, p):
     m = l_shaped(mg.box_mesh(3, (3, 3, 2), p, jitter=True, scramble=True))
-    run(oracle_lib, m, 0, what=f"L-shaped p={p}")
+    run(oracle_lib, m, 2 if p == 1 else 0, what=f"L-shaped p={p}")  # p = 1: the per-row path needs no frame
 
 
 def test_forced_general_path(torch_cuda, oracle_lib, monkeypatch):

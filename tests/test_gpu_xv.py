@@ -1,8 +1,10 @@
 """GPU parity of the extended-frame ("owner computes") path of the vector spaces (lor_xv.cuh,
 DESIGN.md section 4 "k_xv"): H(curl) Nedelec and H(div) Raviart-Thomas rows written complete by
 their owning element, the neighbour cells recomputed in its frame, orientation signs of the box
-dofs from the neighbours' restrictions.  RT and ND take this path by default (LOR_XV=0 / LOR_XV_ND=0:
-the element + merge passes); ND at p >= 6 falls back to them when the frame does not fit.  Both
+dofs from the neighbours' restrictions.  On one rank RT and ND take this path by default at the
+orders where it measured faster (ND p = 4-5, RT p != 5; LOR_XV=1 forces it at every order it fits,
+LOR_XV=0 / LOR_XV_ND=0 keep the element + merge passes); ND at p >= 6 falls back to them when the
+frame does not fit.  Both
 are compared with the oracle element by element (bit-exact pattern, P-10b values), on meshes whose
 numbering is shuffled (ownership on every side of an element) and orientation-scrambled, for every
 p the instantiations cover."""
@@ -26,7 +28,7 @@ def torch_cuda():
 
 def run(O, m, space, expect_path, what):
     from paper_2210_12253_b200.lor import LOR
-    ctx = LOR(m)
+    ctx = LOR(m)  # LOR_XV=1 (the tests below): the frame at every order it supports
     if expect_path is not None:
         assert ctx.fill_path(space) == expect_path, what
     q = ctx.query(space)
@@ -44,7 +46,8 @@ def run(O, m, space, expect_path, what):
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("kind", ["scrambled", "shuffled"])
-def test_rt_xframe(torch_cuda, oracle_lib, p, kind):
+def test_rt_xframe(torch_cuda, oracle_lib, monkeypatch, p, kind):
+    monkeypatch.setenv("LOR_XV", "1")
     shape = (3, 3, 2) if p <= 4 else (3, 2, 2)
     m = mg.box_mesh(3, shape, p, jitter=True, scramble=(kind == "scrambled"))
     if kind == "shuffled":
@@ -54,7 +57,8 @@ def test_rt_xframe(torch_cuda, oracle_lib, p, kind):
 
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("kind", ["scrambled", "shuffled", "kershaw"])
-def test_nd_xframe(torch_cuda, oracle_lib, p, kind):
+def test_nd_xframe(torch_cuda, oracle_lib, monkeypatch, p, kind):
+    monkeypatch.setenv("LOR_XV", "1")
     if kind == "kershaw":
         m = mg.box_mesh(3, (6, 2, 2), p, kershaw=0.3)
     else:
@@ -70,3 +74,14 @@ def test_xframe_off_is_general_path(torch_cuda, oracle_lib, monkeypatch, space):
     monkeypatch.setenv("LOR_XV", "0")
     m = mg.box_mesh(3, (3, 2, 2), 3, jitter=True, scramble=True)
     run(oracle_lib, m, space, 0, f"{space} general path")
+
+
+@pytest.mark.parametrize("space,p,expect", [("nd", 3, 0), ("nd", 4, 1), ("nd", 5, 1), ("nd", 6, 0),
+                                            ("rt", 3, 1), ("rt", 5, 0), ("rt", 6, 1)])
+def test_default_routing(torch_cuda, oracle_lib, monkeypatch, space, p, expect):
+    """default one-rank routing follows the measured table (xv_preferred in lor_capi.cu); same
+    oracle parity on either path"""
+    monkeypatch.delenv("LOR_XV", raising=False)
+    monkeypatch.delenv("LOR_XV_ND", raising=False)
+    m = mg.box_mesh(3, (3, 2, 2), p, jitter=True, scramble=True)
+    run(oracle_lib, m, space, expect, f"{space} p={p} default routing")
