@@ -37,8 +37,9 @@ def _run(O, m, space, quad, p_what, nranks=1):
         e0, e1 = int(m.elem_rank_begin[r]), int(m.elem_rank_begin[r + 1])
         fp0 = c.fill_path(space)
         c.set_coefficients(a[e0:e1], b[e0:e1])
-        # the extended frames are kept on one rank (coefficient boxes beside the coordinates)
-        assert c.fill_path(space) == (fp0 if (nranks == 1 and space != "nd") else 0)
+        # the extended frames are kept on one rank (coefficient boxes beside the coordinates); the
+        # p = 1 per-row path (fill path 2) has no coefficients and hands over to the frame
+        assert c.fill_path(space) == ((1 if fp0 == 2 else fp0) if (nranks == 1 and space != "nd") else 0)
         outs.append(c.assemble(space, 1.3, 0.7, quad))
         c.sync()
     if nranks > 1:
