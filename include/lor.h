@@ -325,9 +325,10 @@ int lor_last_phase_ms(lor_ctx ctx, float *ms, int cap);
  * neighbour cells that touch its rows recomputed; 3D H1, one rank, meshes whose elements all have
  * a regular 3x3x3 coarse neighbourhood -- checked at setup; ND / RT on one rank at the orders where
  * it measured faster, LOR_XV=1 forces it wherever it fits), 0 = element pass + merge pass, 2 = per-row
- * path (3D H1, p = 1, one rank, constant coefficients: a macro-element is a single LOR cell; dense
- * 8x8 cell matrices, one warp per row gathers its <= 64 candidates through the dof -> cell transpose
- * and writes them in ascending column order, duplicates summed; LOR_ROWPATH=0 at setup turns it off).
+ * path (3D, p = 1, one rank, constant coefficients, vertex rule, every space: a macro-element is a
+ * single LOR cell; dense cell matrices (H1 8x8, ND 12x12, RT 6x6, orientation signs applied), one
+ * warp per row gathers its <= 64 candidates through the dof -> cell transpose and writes them in
+ * ascending column order, duplicates summed; LOR_ROWPATH=0 at setup turns it off).
  * LOR_XFRAME=0 in the environment at setup forces 0.  Returns -1 for an invalid context/space. */
 int lor_fill_path(lor_ctx ctx, lor_space space);
 

@@ -140,6 +140,125 @@ __global__ void __launch_bounds__(256) k_leg_rows(LegArgs a) {
   }
 }
 
+// ---- p = 1 vector spaces (fill path 2 of lor_assemble_nd / _rt): the element is the LOR cell, its
+// element-local dofs are the cell-local ones (ND edge eps = 4a + b1 + 2 b2, RT face 2a + side: the
+// App. A.3 family-major lattice order at p = 1), the element restriction and orientation signs are
+// the space's own (emap / esgn).
+template <int SP>
+struct RvK {
+  static constexpr int K = SP == 1 ? 12 : 6;  // dofs per cell
+  static constexpr int KP = K * (K + 1) / 2;   // packed triangle
+  static constexpr int T = SP == 1 ? 32 : 64;  // cells per block of k_rv_ea (staging <= 20 KB)
+};
+
+template <int SP>
+__global__ void __launch_bounds__(RvK<SP>::T) k_rv_ea(int64_t ncell, const double *__restrict__ X, int64_t xstride,
+                                                     double alpha, double beta, double *__restrict__ ea, int *err) {
+  constexpr int KP = RvK<SP>::KP, T = RvK<SP>::T;
+  __shared__ double s[T * KP];
+  const int64_t c0 = (int64_t)blockIdx.x * T;
+  const int64_t cell = c0 + threadIdx.x;
+  if (cell < ncell) {
+    double C[8][3];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) C[q][d] = X[cell * xstride + d * 8 + q];  // p = 1: lattice point = corner q
+    double A[KP];
+    bool ok;
+    if (SP == 1) ok = cell_nd<0>(C, alpha, beta, A);
+    else ok = cell_rt<0>(C, alpha, beta, A);
+    if (!ok && atomicCAS(err, 0, 1) == 0) {
+      err[1] = (int)cell;
+      err[2] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < KP; ++k) s[threadIdx.x * KP + k] = A[k];
+  }
+  __syncthreads();
+  const int64_t nv = (ncell - c0 < T ? ncell - c0 : T) * KP;
+  for (int64_t k = threadIdx.x; k < nv; k += T) ea[c0 * KP + k] = s[k];
+}
+
+// one warp per row over its <= 4 (ND) / 2 (RT) cells: candidates (column, candidate index) ranked
+// as in k_leg_rows, values s_i s_j A_ij
+template <int SP, bool FILL>
+__global__ void __launch_bounds__(256) k_rv_rows(RvArgs a) {
+  constexpr int K = RvK<SP>::K, KP = RvK<SP>::KP;
+  __shared__ int64_t s_key[8][64];
+  __shared__ double s_val[8][64];
+  __shared__ int s_pos[8][64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * 8 + w);
+  if (r >= a.n) return;
+  const int64_t e0 = a.off[r], ne = a.off[r + 1] - e0;
+  const int nc = (int)(ne * K);
+  if (nc > 64) {  // not a conforming hex mesh (an edge in more than 5 cells)
+    if (lane == 0) atomicCAS(a.err, 0, 3);
+    return;
+  }
+  int64_t key[2];
+  double val[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = lane + 32 * h;
+    key[h] = INT64_MAX;
+    val[h] = 0.0;
+    if (t < nc) {
+      const int32_t en = a.ent[e0 + t / K];
+      const int64_t cell = en / K;
+      const int i = en - (int)cell * K, j = t % K;
+      key[h] = ((int64_t)a.map[cell * K + j] << 6) | t;
+      if (FILL) {
+        const double v = a.ea[cell * KP + (i <= j ? tri(K, i, j) : tri(K, j, i))];
+        val[h] = (a.sgn[cell * K + i] * a.sgn[cell * K + j]) > 0 ? v : -v;
+      }
+    }
+    s_key[w][t] = key[h];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int rk = 0;
+    for (int u = 0; u < nc; ++u) rk += s_key[w][u] < key[h];
+    const int t = lane + 32 * h;
+    if (t < nc) s_pos[w][t] = rk;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = lane + 32 * h;
+    if (t < nc) {
+      s_key[w][s_pos[w][t]] = key[h];
+      if (FILL) s_val[w][s_pos[w][t]] = val[h];
+    }
+  }
+  __syncwarp();
+  bool head[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = lane + 32 * h;
+    head[h] = t < nc && (t == 0 || (s_key[w][t] >> 6) != (s_key[w][t - 1] >> 6));
+  }
+  const unsigned b0 = __ballot_sync(0xffffffffu, head[0]), b1 = __ballot_sync(0xffffffffu, head[1]);
+  if (!FILL) {
+    if (lane == 0) a.cnt[r] = __popc(b0) + __popc(b1);
+    return;
+  }
+  const int64_t o = a.row_ptr[r];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!head[h]) continue;
+    const int t = lane + 32 * h;
+    const int k = h == 0 ? __popc(b0 & ((1u << lane) - 1u)) : __popc(b0) + __popc(b1 & ((1u << lane) - 1u));
+    const int64_t col = s_key[w][t] >> 6;
+    double v = s_val[w][t];
+    for (int u = t + 1; u < nc && (s_key[w][u] >> 6) == col; ++u) v += s_val[w][u];
+    a.col[o + k] = (int32_t)col;
+    a.val[o + k] = v;
+  }
+}
+
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t > 0 ? (n + t - 1) / t : 1); }
 
 }  // namespace
@@ -161,5 +280,27 @@ cudaError_t launch_leg_rows(const LegArgs &a, bool fill, cudaStream_t st) {
   else k_leg_rows<false><<<nblk(a.n, 8), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
+
+cudaError_t launch_rv_ea(int sp, int64_t ncell, const double *X, int64_t xstride, double alpha, double beta, double *ea,
+                         int *err, cudaStream_t st) {
+  if (ncell <= 0) return cudaSuccess;
+  if (sp == 1) k_rv_ea<1><<<nblk(ncell, RvK<1>::T), RvK<1>::T, 0, st>>>(ncell, X, xstride, alpha, beta, ea, err);
+  else k_rv_ea<2><<<nblk(ncell, RvK<2>::T), RvK<2>::T, 0, st>>>(ncell, X, xstride, alpha, beta, ea, err);
+  return cudaGetLastError();
+}
+cudaError_t launch_rv_rows(int sp, const RvArgs &a, bool fill, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  const unsigned g = nblk(a.n, 8);
+  if (sp == 1) {
+    if (fill) k_rv_rows<1, true><<<g, 256, 0, st>>>(a);
+    else k_rv_rows<1, false><<<g, 256, 0, st>>>(a);
+  } else {
+    if (fill) k_rv_rows<2, true><<<g, 256, 0, st>>>(a);
+    else k_rv_rows<2, false><<<g, 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+int rv_dofs_per_cell(int sp) { return sp == 1 ? 12 : 6; }
+int64_t rv_ea_words(int sp) { return sp == 1 ? 78 : 21; }
 
 }  // namespace lorb

@@ -225,8 +225,8 @@ class LOR:
         return int(lib().lor_kernel_launches(self.h))
 
     def fill_path(self, space="h1") -> int:
-        """1: extended-frame single-pass fill, 0: element pass + merge pass, 2: per-row path (3D H1
-        at p = 1 on one rank) -- lor_fill_path."""
+        """1: extended-frame single-pass fill, 0: element pass + merge pass, 2: per-row path (3D, p = 1,
+        one rank, every space) -- lor_fill_path."""
         return int(lib().lor_fill_path(self.h, SPACES[space]))
 
     def phase_ms(self):

@@ -1,4 +1,4 @@
-"""GPU parity of the per-row path lor_assemble_h1 takes at p = 1 on one rank (lor_fill_path 2,
+"""GPU parity of the per-row path lor_assemble_{h1,nd,rt} take at p = 1 on one rank (lor_fill_path 2,
 lor_legacy.cu, DESIGN.md section 4 "p = 1"): a macro-element of order 1 is a single LOR cell
 (the LOR mesh is then the mesh itself), so the assembly is the unstructured one --
 dense 8x8 cell matrices (the sub-cell math of every other path, P-10b values), one warp per row
@@ -6,7 +6,8 @@ gathering the <= 64 candidates of its <= 8 cells through the dof -> cell transpo
 columns, duplicates summed.  Compared with the oracle row by row on Cartesian, jittered/scrambled,
 Kershaw, shuffled-numbering and irregular (L-shaped, valence-3 edge) meshes, through numeric
 re-assembly, a coordinate update, degenerate geometry and the fallbacks (coefficients, Gauss-2,
-LOR_ROWPATH=0)."""
+LOR_ROWPATH=0).  ND / RT: the element restriction and orientation signs of the space (element =
+cell), 12x12 / 6x6 cell matrices, values s_i s_j A_ij; orientation-scrambled meshes included."""
 import numpy as np
 import pytest
 
@@ -133,3 +134,86 @@ def test_rowpath_sampled_large(torch_cuda, oracle_lib):
     ref = oracle_lib.assemble_rows(m, rows, "h1", "vertex", 1.0, 1.0)
     compare_rows(rp, col, val, ref, 0, what="p=1 96^3 sampled")
     ctx.close()
+
+
+@pytest.mark.parametrize("space", ["nd", "rt"])
+@pytest.mark.parametrize("kind", ["cartesian", "jitscr", "kershaw", "shuffled", "lshaped"])
+def test_rowpath_vector_parity(torch_cuda, oracle_lib, space, kind):
+    from paper_2210_12253_b200.lor import LOR
+    m = _mesh(kind)
+    ctx = LOR(m)
+    assert ctx.fill_path(space) == 2
+    q = ctx.query(space)
+    rp, col, val = ctx.assemble(space, 1.3, 0.7, "vertex")
+    ctx.sync()
+    ref = oracle_lib.assemble(m, space, "vertex", 1.3, 0.7)
+    assert q["nnz"] == ref.nnz
+    compare_full(to_host(rp), to_host(col), to_host(val), ref, 0, q["n_local"], f"rowpath {space} {kind}")
+    ctx.reassemble(space, 0.4, 2.5, "vertex", out=(rp, col, val))
+    ctx.sync()
+    compare_full(to_host(rp), to_host(col), to_host(val), oracle_lib.assemble(m, space, "vertex", 0.4, 2.5), 0,
+                 q["n_local"], f"rowpath {space} {kind} reassembly")
+    ctx.close()
+
+
+@pytest.mark.parametrize("space", ["nd", "rt"])
+@pytest.mark.parametrize("what", ["coef", "gauss2", "off", "coords"])
+def test_rowpath_vector_fallbacks(torch_cuda, oracle_lib, monkeypatch, space, what):
+    """coefficients / Gauss-2 / LOR_ROWPATH=0 take the other paths; a coordinate update is seen"""
+    import torch
+    from paper_2210_12253_b200.lor import LOR
+    from tests.test_gpu_coef import _coefs
+    if what == "off":
+        monkeypatch.setenv("LOR_ROWPATH", "0")
+    m = mg.box_mesh(3, (4, 3, 3), 1, jitter=True, scramble=True)
+    ctx = LOR(m if what != "coords" else mg.box_mesh(3, (4, 3, 3), 1, scramble=True))
+    quad, coef = ("gauss2" if what == "gauss2" else "vertex"), None
+    if what == "coef":
+        coef = _coefs(m)
+        ctx.set_coefficients(*coef)
+    if what == "coords":
+        ctx.update_coordinates(torch.from_numpy(np.ascontiguousarray(m.X)).cuda())
+    assert ctx.fill_path(space) == (2 if what in ("gauss2", "coords") else (0 if space == "nd" else 1))
+    q = ctx.query(space)
+    out = ctx.assemble(space, 1.3, 0.7, quad)
+    ctx.sync()
+    compare_full(*(to_host(t) for t in out), oracle_lib.assemble(m, space, quad, 1.3, 0.7, coef=coef), 0,
+                 q["n_local"], f"p=1 {space} {what}")
+    ctx.close()
+
+
+@pytest.mark.parametrize("space", ["nd", "rt"])
+def test_rowpath_vector_sampled_large(torch_cuda, oracle_lib, space):
+    """96^3 Kershaw elements: closed-form row lengths (ND 12..33, RT 6..11 on a hex lattice), 2000
+    sampled rows against the oracle's row routine"""
+    from paper_2210_12253_b200.lor import LOR
+    n = 96
+    m = mg.box_mesh(3, (n, n, n), 1, kershaw=0.3)
+    ctx = LOR(m, spaces=(space,))
+    assert ctx.fill_path(space) == 2
+    q = ctx.query(space)
+    assert q["n_local"] == (3 * n * (n + 1) ** 2 if space == "nd" else 3 * n * n * (n + 1))
+    rp, col, val = ctx.assemble(space, 1.0, 1.0, "vertex")
+    ctx.sync()
+    rp, col, val = to_host(rp), to_host(col), to_host(val)
+    d = np.diff(rp)
+    assert (d.min(), d.max()) == ((12, 33) if space == "nd" else (6, 11))
+    rng = np.random.default_rng(5)
+    rows = np.unique(np.concatenate([rng.integers(0, q["n_local"], 2000), [0, q["n_local"] - 1]]))
+    ref = oracle_lib.assemble_rows(m, rows, space, "vertex", 1.0, 1.0)
+    compare_rows(rp, col, val, ref, 0, what=f"p=1 {space} 96^3 sampled")
+    ctx.close()
+
+
+def test_rowpath_vector_degenerate_reported(torch_cuda):
+    from paper_2210_12253_b200.lor import LOR, LorError
+    m = mg.box_mesh(3, (3, 3, 3), 1)
+    X = m.X.copy()
+    X[13, :, 0] = X[13, :, 7] + (X[13, :, 7] - X[13, :, 0])
+    m.X = X
+    ctx = LOR(m)
+    assert ctx.fill_path("rt") == 2
+    ctx.assemble("rt")
+    with pytest.raises(LorError) as ei:
+        ctx.sync()
+    assert "degenerate-geometry(element=13" in str(ei.value)

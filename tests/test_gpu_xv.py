@@ -48,6 +48,7 @@ def run(O, m, space, expect_path, what):
 @pytest.mark.parametrize("kind", ["scrambled", "shuffled"])
 def test_rt_xframe(torch_cuda, oracle_lib, monkeypatch, p, kind):
     monkeypatch.setenv("LOR_XV", "1")
+    monkeypatch.setenv("LOR_ROWPATH", "0")  # p = 1: the per-row path otherwise (test_gpu_rowpath.py)
     shape = (3, 3, 2) if p <= 4 else (3, 2, 2)
     m = mg.box_mesh(3, shape, p, jitter=True, scramble=(kind == "scrambled"))
     if kind == "shuffled":
@@ -59,6 +60,7 @@ def test_rt_xframe(torch_cuda, oracle_lib, monkeypatch, p, kind):
 @pytest.mark.parametrize("kind", ["scrambled", "shuffled", "kershaw"])
 def test_nd_xframe(torch_cuda, oracle_lib, monkeypatch, p, kind):
     monkeypatch.setenv("LOR_XV", "1")
+    monkeypatch.setenv("LOR_ROWPATH", "0")
     if kind == "kershaw":
         m = mg.box_mesh(3, (6, 2, 2), p, kershaw=0.3)
     else:
